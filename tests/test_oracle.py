@@ -1,0 +1,373 @@
+"""CPU pins of the fp64 oracle (DESIGN.md §Oracle pins S1-S8).
+
+Each pin checks the oracle against something other than itself: the paper's printed
+numbers, SPEC worked values derived from Eq. 2, closed forms, exact rational arithmetic,
+exhaustive enumeration, or algebraic invariants -- chosen so that a dropped term, a wrong
+sign or bit index, or a transposed operand fails at least one of them.
+"""
+
+import json
+import math
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+def _rng(seed=0):
+    return np.random.default_rng(seed)
+
+
+def _rand_fp16(rng, shape, scale=1.0):
+    return (rng.standard_normal(shape) * scale).astype(np.float16)
+
+
+def _frac(v):
+    return Fraction(float(v))
+
+
+# ------------------------------------------------------------------------- S1: the LUT
+@pytest.mark.parametrize("case", ["random", "onehot", "zero", "extreme", "tiny"])
+def test_s1_lut_exhaustive_256_keys(case):
+    """256 signed partial sums per 8 activations.  Direct, incremental
+     and an exact-rational brute force agree on every key."""
+    rng = _rng(1)
+    if case == "random":
+        x8 = _rand_fp16(rng, 8)
+    elif case == "onehot":
+        x8 = np.zeros(8, np.float16)
+        x8[0] = 1.0
+    elif case == "zero":
+        x8 = np.zeros(8, np.float16)
+    elif case == "extreme":
+        x8 = np.array([65504, -65504, 6.1e-5, -2.0 ** -24, 1024, -3.5, 0.0, 2.0 ** -14], np.float16)
+    else:
+        x8 = np.array([2.0 ** -24] * 8, np.float16)
+    d = oracle.lut_direct(x8)
+    inc = oracle.lut_incremental(x8)
+    xs = [_frac(v) for v in x8]
+    for key in range(256):
+        exact = sum((xs[b] if (key >> b) & 1 else -xs[b]) for b in range(8))
+        assert Fraction(float(d[key])) == exact
+        assert Fraction(float(inc[key])) == exact
+    if case == "onehot":  # T[key] = +1 if bit0 else -1
+        assert all(d[k] == (1.0 if k & 1 else -1.0) for k in range(256))
+    if case == "zero":
+        assert np.all(d == 0.0)
+    # complement symmetry: T[~key] = -T[key]
+    assert np.all(d[::-1] == -d)
+
+
+# ------------------------------------------------------------------------ S5: pack (a1)
+def test_s5_pot_round_spec_values():
+    gold = _gold("pot_round_spec.json")
+    for case in gold["pot_round"]:
+        e, nclamp = oracle.pot_exponent(np.array([case["alpha"]], np.float32))
+        assert int(e[0]) == case["P"] and nclamp == 0
+    # the sign lives in the bits after the sign fold: alpha = -0.25 flips every sign
+    s = np.ones((1, 1, 8), np.int8)
+    planes, exps, _ = oracle.pack_canonical(s, np.array([[[-0.25]]], np.float32), 8)
+    assert planes[0, 0, 0] == 0x00 and exps[0, 0, 0] == -2
+    planes, exps, _ = oracle.pack_canonical(s, np.array([[[4.0]]], np.float32), 8)
+    assert planes[0, 0, 0] == 0xFF and exps[0, 0, 0] == 2
+
+
+def _pot_bracket(alpha, P):
+    """Exact rational check that P = round(log2|alpha|): 2^(2P-1) <= alpha^2 < 2^(2P+1)."""
+    a2 = Fraction(float(np.float32(alpha))) ** 2
+    return Fraction(2) ** (2 * P - 1) <= a2 < Fraction(2) ** (2 * P + 1)
+
+
+def test_s5_pot_exact_rational_bracket():
+    """P = round(log2|a|)  <=>  2^(2P-1) <= a^2 < 2^(2P+1), checked in exact rationals
+    (no log2) on random fp32 scales spanning many binades, and at the sqrt(2) boundary."""
+    rng = _rng(2)
+    a = (np.exp2(rng.uniform(-40, 40, 20000)) * rng.choice([-1, 1], 20000)).astype(np.float32)
+    # the two fp32 neighbours of every 2^(k+1/2) boundary
+    b = []
+    for k in range(-30, 30):
+        m = np.float32(2.0 ** (k + 0.5))
+        b += [np.nextafter(m, np.float32(0)), m, np.nextafter(m, np.float32(np.inf))]
+    a = np.concatenate([a, np.array(b, np.float32)])
+    e, nclamp = oracle.pot_exponent(a)
+    assert nclamp == 0
+    for v, p in zip(a.tolist(), e.tolist()):
+        assert _pot_bracket(v, p), (v, p)
+
+
+def test_s5_pot_edge_cases():
+    e, n = oracle.pot_exponent(np.array([0.0, -0.0], np.float32))
+    assert list(e) == [oracle.EXP_ZERO, oracle.EXP_ZERO] and n == 0
+    sub = np.float32(1e-42)  # subnormal -> P ~ -139 -> clamp to -100
+    e, n = oracle.pot_exponent(np.array([sub, 2.0 ** 101, 2.0 ** -101, 2.0 ** 100, 2.0 ** -100], np.float32))
+    assert list(e) == [-100, 100, -100, 100, -100] and n == 3
+    for bad in (np.nan, np.inf, -np.inf):
+        with pytest.raises(ValueError):
+            oracle.pot_exponent(np.array([bad], np.float32))
+
+
+@pytest.mark.parametrize("K", [8, 24, 64])
+def test_s5_bit_order_single_positive(K):
+    """LSB = lowest k of the 8 grouped weights, 1 <-> +1."""
+    for j in range(K):
+        s = -np.ones((1, 1, K), np.int8)
+        s[0, 0, j] = 1
+        planes, _, _ = oracle.pack_canonical(s, np.ones((1, 1, K // 8), np.float32), 8)
+        expect = np.zeros(K // 8, np.uint8)
+        expect[j >> 3] = 1 << (j & 7)
+        assert np.array_equal(planes[0, 0], expect)
+        assert np.array_equal(oracle.unpack_signs(planes, K)[0, 0], s[0, 0])
+
+
+def test_s5_sign_fold_identity():
+    """alpha*b == (-alpha)*(-b): dequant of the packed layer equals sum_i POT(alpha_i) b_i
+    computed directly from the unpacked inputs with exact rationals (tiny shape)."""
+    rng = _rng(3)
+    q, N, K, g = 2, 3, 16, 8
+    s = rng.choice([-1, 1], (q, N, K)).astype(np.int8)
+    a = (rng.standard_normal((q, N, K // g)) * 0.1).astype(np.float32)
+    planes, exps, _ = oracle.pack_canonical(s, a, g)
+    w = oracle.dequant(planes, exps, g, K)
+    for n in range(N):
+        for k in range(K):
+            exact = Fraction(0)
+            for i in range(q):
+                al = float(a[i, n, k // g])
+                P = round(math.log2(abs(al)))
+                exact += (1 if al > 0 else -1) * Fraction(2) ** P * int(s[i, n, k])
+            assert Fraction(float(w[n, k])) == exact
+
+
+# ------------------------------------------------------------- S2: brute force, tiny K
+def _exact_y(x, s, e, g):
+    """Exact rational y for one row from unpacked signs s[q][K] and exponents e[q][K/g]."""
+    acc = Fraction(0)
+    for i in range(s.shape[0]):
+        for k in range(s.shape[1]):
+            ei = int(e[i][k // g])
+            if ei == oracle.EXP_ZERO:
+                continue
+            acc += int(s[i][k]) * Fraction(2) ** ei * _frac(x[k])
+    return acc
+
+
+@pytest.mark.parametrize("q,K", [(1, 8), (2, 8), (1, 16)])
+def test_s2_bruteforce_every_sign_pattern(q, K):
+    """Every one of the 2^(qK) sign patterns of one output row: gemm == lut_gemm == exact."""
+    rng = _rng(4)
+    g = 8
+    x = _rand_fp16(rng, (1, K))
+    e = rng.integers(-3, 4, (q, 1, K // g)).astype(np.int8)
+    npat = 1 << (q * K)
+    pats = ((np.arange(npat)[:, None] >> np.arange(q * K)[None, :]) & 1).astype(np.int8)
+    signs = np.where(pats == 1, 1, -1).astype(np.int8).reshape(npat, q, K).transpose(1, 0, 2)
+    alpha = np.repeat(np.ldexp(1.0, e.astype(np.int64)).astype(np.float32), npat, axis=1)
+    planes, exps, _ = oracle.pack_canonical(signs, alpha, g)
+    y1 = oracle.gemm(x, planes, exps, g)[0]
+    y2 = oracle.lut_gemm(x, planes, exps, g)[0]
+    assert np.array_equal(y1, y2)
+    for p in range(0, npat, max(1, npat // 512)):   # exact rationals on a spread sample
+        assert Fraction(float(y1[p])) == _exact_y(x[0], signs[:, p], exps[:, p], g)
+
+
+# --------------------------------------------------------------------- S3/S4 closed forms
+def test_s3_all_ones_closed_form_and_exponent_shift():
+    rng = _rng(5)
+    q, N, K, g = 3, 5, 256, 128
+    x = _rand_fp16(rng, (2, K))
+    e = rng.integers(-8, 9, (q, N, K // g)).astype(np.int8)
+    planes = np.full((q, N, K // 8), 0xFF, np.uint8)
+    y = oracle.gemm(x, planes, e, g)
+    for m in range(2):
+        for n in range(N):
+            exact = Fraction(0)
+            for G in range(K // g):
+                sx = sum(_frac(v) for v in x[m, G * g:(G + 1) * g])
+                exact += sum(Fraction(2) ** int(e[i, n, G]) for i in range(q)) * sx
+            assert Fraction(float(y[m, n])) == exact
+    for d in (-5, 1, 7):
+        y_d = oracle.gemm(x, planes, (e + d).astype(np.int8), g)
+        assert np.array_equal(y_d, np.ldexp(y, d))
+
+
+def test_s3_flip_plane_group_negates_its_term():
+    rng = _rng(6)
+    q, N, K, g = 2, 4, 256, 128
+    s = rng.choice([-1, 1], (q, N, K)).astype(np.int8)
+    a = np.ldexp(1.0, rng.integers(-6, 0, (q, N, K // g))).astype(np.float32)
+    planes, exps, _ = oracle.pack_canonical(s, a, g)
+    x = _rand_fp16(rng, (1, K))
+    y = oracle.gemm(x, planes, exps, g)[0]
+    i, G = 1, 1
+    flipped = planes.copy()
+    flipped[i, :, G * g // 8:(G + 1) * g // 8] ^= 0xFF
+    y_f = oracle.gemm(x, flipped, exps, g)[0]
+    for n in range(N):
+        term = sum(int(s[i, n, k]) * _frac(x[0, k]) for k in range(G * g, (G + 1) * g))
+        term *= Fraction(float(a[i, n, G]))
+        assert Fraction(float(y_f[n])) == Fraction(float(y[n])) - 2 * term
+
+
+@pytest.mark.parametrize("e", [-7, 0, 3])
+def test_s4_q1_all_ones_is_scaled_sum(e):
+    """north_star invariant: q = 1, all-ones B, alpha = 2^e  ->  y = 2^e * sum(x)."""
+    rng = _rng(7)
+    K = 768
+    x = _rand_fp16(rng, (3, K))
+    signs = np.ones((1, 4, K), np.int8)
+    planes, exps, _ = oracle.pack_canonical(signs, np.full((1, 4, K // 128), 2.0 ** e, np.float32), 128)
+    y = oracle.gemm(x, planes, exps, 128)
+    for m in range(3):
+        exact = Fraction(2) ** e * sum(_frac(v) for v in x[m])
+        assert all(Fraction(float(v)) == exact for v in y[m])
+    ys = oracle.gemm_scalar(x[:1], planes, exps, 128)
+    assert np.allclose(ys, y[:1], rtol=1e-12, atol=0)
+
+
+# ------------------------------------------------------------ S6: formula-defined weights
+def _formula_layer(q, N, K, g):
+    """Weights defined by a formula so column j of W_hat is known without the oracle:
+    s_i[n][k] = +1 iff (3n + 5k + 7i) mod 4 < 2;  alpha_i[n][G] = 2^-(i + (n + G) mod 3)."""
+    n = np.arange(N)[:, None]
+    k = np.arange(K)[None, :]
+    s = np.stack([np.where((3 * n + 5 * k + 7 * i) % 4 < 2, 1, -1) for i in range(q)]).astype(np.int8)
+    G = np.arange(K // g)[None, :]
+    a = np.stack([np.ldexp(1.0, -(i + (n + G) % 3)) for i in range(q)]).astype(np.float32)
+    return s, a
+
+
+def _formula_w(q, n, k, g):
+    return sum((1 if (3 * n + 5 * k + 7 * i) % 4 < 2 else -1) * Fraction(2) ** -(i + (n + k // g) % 3)
+               for i in range(q))
+
+
+def test_s6_basis_vectors_select_columns_not_rows():
+    """x = e_j -> y[n] = W_hat[n][j]: with N != K this fails for a transposed operand."""
+    q, N, K, g = 3, 40, 256, 128
+    s, a = _formula_layer(q, N, K, g)
+    planes, exps, _ = oracle.pack_canonical(s, a, g)
+    for j in (0, 1, 7, 8, 127, 128, 255):
+        x = np.zeros((1, K), np.float16)
+        x[0, j] = 1.0
+        y = oracle.gemm(x, planes, exps, g)[0]
+        assert all(Fraction(float(y[n])) == _formula_w(q, n, j, g) for n in range(N))
+
+
+def test_s6_linearity_and_odd_symmetry():
+    rng = _rng(8)
+    q, N, K, g = 2, 64, 512, 128
+    s, a = _formula_layer(q, N, K, g)
+    planes, exps, _ = oracle.pack_canonical(s, a, g)
+    x1 = _rand_fp16(rng, (1, K))
+    x2 = _rand_fp16(rng, (1, K))
+    y1 = oracle.gemm(x1, planes, exps, g)
+    assert np.array_equal(oracle.gemm(-x1, planes, exps, g), -y1)
+    y12 = oracle.gemm(x1.astype(np.float64) + x2.astype(np.float64), planes, exps, g)
+    assert np.allclose(y12, y1 + oracle.gemm(x2, planes, exps, g), rtol=0, atol=1e-12)
+
+
+def test_gemm_matches_scalar_and_lut_routes_on_synthetic_layer():
+    q, N, K, g = 3, 24, 512, 128
+    signs, alpha = synth.gen_layer(q, N, K, g, seed=synth.seed_for(0))
+    planes, exps, _ = oracle.pack_canonical(signs.numpy(), alpha.numpy(), g)
+    x = synth.gen_x(2, K, seed=synth.seed_for(0, 1)).numpy()
+    y = oracle.gemm(x, planes, exps, g)
+    assert np.allclose(oracle.lut_gemm(x, planes, exps, g), y, rtol=1e-13, atol=1e-15)
+    assert np.allclose(oracle.gemm_scalar(x, planes, exps, g), y, rtol=1e-13, atol=1e-15)
+
+
+@pytest.mark.slow
+def test_config0_scalar_loop_agrees():
+    """Config 0 (OPT-125M q_proj 768x768, 3-bit, g=128): the pure-Python loop (the
+    'CPU oracle in seconds' case) equals the numpy route."""
+    q, N, K, g = 3, 768, 768, 128
+    signs, alpha = synth.gen_layer(q, N, K, g, seed=synth.seed_for(0))
+    planes, exps, _ = oracle.pack_canonical(signs.numpy(), alpha.numpy(), g)
+    x = synth.gen_x(1, K, seed=synth.seed_for(0, 1)).numpy()
+    y = oracle.gemm(x, planes, exps, g)
+    ys = oracle.gemm_scalar(x, planes, exps, g)
+    assert np.allclose(ys, y, rtol=1e-12, atol=1e-14)
+
+
+# ------------------------------------------------------------------ tiled layout (a1 opt.)
+def test_tiled_layout_definition_and_roundtrip():
+    rng = _rng(9)
+    for q, N, K, g in [(3, 40, 512, 128), (2, 16, 256, 256), (1, 33, 768, 768)]:
+        planes = rng.integers(0, 256, (q, N, K // 8)).astype(np.uint8)
+        exps = rng.integers(-100, 101, (q, N, K // g)).astype(np.int8)
+        pt, et = oracle.to_tiled(planes, exps, g)
+        assert (pt.size, et.size) == oracle.tiled_sizes(q, N, K)
+        RG = -(-N // 16)
+        # walk the definition independently for random positions
+        for _ in range(300):
+            s, rg, i = rng.integers(K // 256), rng.integers(RG), rng.integers(q)
+            r, h, j = rng.integers(16), rng.integers(2), rng.integers(16)
+            n = 16 * rg + r
+            off = ((s * RG + rg) * q + i) * 512 + r * 32 + h * 16 + j
+            want = planes[i, n, 32 * s + 16 * h + (j + r) % 16] if n < N else 0
+            assert pt[off] == want
+            eoff = ((s * RG + rg) * q + i) * 32 + r * 2 + h
+            ewant = exps[i, n, (256 * s + 128 * h) // g] if n < N else oracle.EXP_ZERO
+            assert et[eoff] == ewant
+        p2, e2 = oracle.from_tiled(pt, et, q, N, K, g)
+        assert np.array_equal(p2, planes) and np.array_equal(e2, exps)
+
+
+def test_tiled_rotation_gives_distinct_groups_per_step():
+    """The layout's purpose: at every step j the 32 lanes (16 rows x 2 halves) of a warp
+    read 32 *different* groups t = 16h + (j + r) mod 16 of the 256-k slice."""
+    for j in range(16):
+        groups = {16 * h + (j + r) % 16 for r in range(16) for h in range(2)}
+        assert len(groups) == 32
+
+
+# ----------------------------------------------------------- S7: byte accounting vs paper
+def test_s7_memory_accounting_matches_paper():
+    gold = _gold("paper_memory.json")
+    tol = gold["tolerance_gib"]
+    for name, m in gold["models"].items():
+        H, F, L, kv = m["hidden"], m["ffn"], m["layers"], m["kv_dim"]
+        shapes = [(H, H), (kv, H), (kv, H), (H, H)]
+        shapes += [(F, H), (F, H), (H, F)] if m.get("gated_mlp") else [(F, H), (H, F)]
+        emb = m["emb_copies"] * m["vocab"] * H * 2
+        for bits, printed in m["printed_gb"].items():
+            b = int(bits)
+            if b == 16:
+                lin = sum(N * K * 2 for N, K in shapes)
+            else:
+                lin = sum(oracle.packed_bytes(b, N, K, K)[0] for N, K in shapes)
+            gib = (L * lin + emb) / 2 ** 30
+            assert abs(gib - printed) <= tol, (name, bits, gib, printed)
+
+
+def test_algorithmic_bytes_config_table():
+    """221,184 + 13,824 + 1,536 + 1,536 = 238,080 bytes."""
+    assert oracle.algorithmic_bytes(1, 3, 768, 768, 128) == 238080
+    assert oracle.packed_bytes(3, 28672, 8192, 128) == (88080384, 5505024)
+
+
+# ------------------------------------------------------------------------ metric sanity
+def test_err_floor_metric():
+    y = np.array([[1.0, -2.0, 0.0, 1e-9]])
+    assert oracle.err_floor(y, y) == 0.0
+    rms = math.sqrt((1 + 4 + 1e-18) / 4)
+    yb = y.copy()
+    yb[0, 3] += 1e-3
+    assert math.isclose(oracle.err_floor(yb, y), 1e-3 / rms, rel_tol=1e-9)
+    assert oracle.err_floor(np.zeros((1, 3)), np.zeros((1, 3))) == 0.0
+
+
+def test_fp16_output_rounding_is_rne():
+    # 2049 is a tie between 2048 and 2050 in fp16 -> even mantissa 2048; 2051 -> 2052
+    assert oracle.to_fp16(np.array([2049.0, 2051.0, 1e6])).tolist() == [2048.0, 2052.0, float("inf")]
