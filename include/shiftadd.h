@@ -1,0 +1,130 @@
+/*
+ * shiftadd.h -- C ABI of the B200 (sm_100a) ShiftAddLLM LUT-GEMV hot path.
+ *
+ * The operation (arxiv 2406.05981, §4.1):
+ *   y = sum_i alpha_i (.) (B_i x)    -- BCQ weights w_q = sum_i alpha_i b_i,
+ *   alpha_i = sign * 2^P, P = round(log2|alpha|)  (Eq. 2),
+ *   x * 2^P done as an integer add on the float exponent field,
+ *   B_i x done by building 256 partial sums per 8 activations and querying them with
+ *   8-bit keys formed by 8 grouped binary weights, output FP16 (:186).
+ *
+ * Conventions (all functions):
+ *   - Every pointer argument is a caller-owned CUDA DEVICE pointer unless stated otherwise.
+ *     The library never allocates, frees or synchronises; every launch is stream-ordered
+ *     on `stream` (a cudaStream_t passed as void*; NULL = legacy default stream).
+ *   - Arguments are validated synchronously before anything is launched; a validation
+ *     failure returns SHIFTADD_ERR_INVALID / _UNSUPPORTED and launches nothing.
+ *   - Launch failures return SHIFTADD_ERR_CUDA; asynchronous device faults surface at the
+ *     caller's next synchronisation.  shiftadd_last_error() returns a thread-local detail.
+ *   - No C++ exception crosses the ABI.  No global mutable state beyond per-device
+ *     immutable caches (SM count, kernel attributes), so calls are thread-safe per stream.
+ *   - fp16 tensors are passed as uint16_t IEEE binary16 bit patterns.
+ *
+ * Notation: x[M][K] activations (K = reduction dim), N outputs, q bit-planes, scale group
+ * g along K.  A key byte holds 8 consecutive k of one output row n of one plane i:
+ * bit (k & 7) of byte k >> 3 is 1 <=> the weight sign is +1 (LSB = lowest k).
+ */
+#ifndef SHIFTADD_H
+#define SHIFTADD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SHIFTADD_ABI_VERSION 1
+
+typedef enum {
+  SHIFTADD_OK = 0,
+  SHIFTADD_ERR_INVALID = 2,      /* bad argument (null pointer, shape, alignment, range)   */
+  SHIFTADD_ERR_UNSUPPORTED = 6,  /* valid request this build has no kernel for (e.g. M>16) */
+  SHIFTADD_ERR_CUDA = 7          /* CUDA runtime error (no device, not sm_100, launch)     */
+} shiftadd_status;
+
+/* Exponent encoding of a PoT scale (reading R5 in DESIGN.md). */
+#define SHIFTADD_EXP_ZERO ((int8_t)-128) /* alpha == 0: the group contributes nothing */
+#define SHIFTADD_EXP_MIN (-100)          /* finite exponents are clamped to [MIN, MAX]  */
+#define SHIFTADD_EXP_MAX (100)
+
+/* Weight layouts.  Both hold the same bytes (one a permutation of the other).
+ *  CANONICAL: planes u8 [q][N][K/8], exps i8 [q][N][K/g]  (the north_star layout).
+ *  TILED    : device-tiled, for the fast kernels.  Tiles of 16 rows x
+ *             256 k per plane, stored in (slice s, row-group rg, plane i) order, 512 B each:
+ *               byte ((s*RG + rg)*q + i)*512 + r*32 + h*16 + j
+ *                 = canonical planes[i][16rg + r][32s + 16h + ((j + r) & 15)]   (0 if n >= N)
+ *             and one exponent per 128-k chunk:
+ *               exps ((s*RG + rg)*q + i)*32 + r*2 + h
+ *                 = canonical exps[i][16rg + r][(256s + 128h) / g]            (EXP_ZERO if n >= N)
+ *             with RG = ceil(N/16).  Requires K % 256 == 0 and g % 128 == 0. */
+typedef enum { SHIFTADD_LAYOUT_CANONICAL = 0, SHIFTADD_LAYOUT_TILED = 1 } shiftadd_layout;
+
+/* Flags for shiftadd_lut_gemm. */
+#define SHIFTADD_FLAG_PDL 1u /* launch with programmatic dependent launch: the kernel's weight
+                                prefetch may overlap the previous kernel on the stream; x,
+                                y and the workspace are touched only after it completes. */
+
+int shiftadd_abi_version(void);
+const char* shiftadd_status_string(int status);
+const char* shiftadd_last_error(void);
+
+/* Bytes of the packed planes for a layout (returned) and of its exponents (*exps_bytes if
+ * non-NULL).  Returns 0 (and sets last_error) for shapes the layout cannot hold. */
+size_t shiftadd_packed_bytes(int layout, int q, int N, int K, int g, size_t* exps_bytes);
+
+/* a1 -- bit-plane packing and PoT exponent encoding.
+ *   signs : i8  [q][N][K], each -1 or +1                 (b_i)
+ *   alpha : f32 [q][N][K/g]                              (group scales alpha_i)
+ *   planes: out, shiftadd_packed_bytes(layout,...) bytes, 16-byte aligned
+ *   exps  : out, *exps_bytes bytes
+ *   counts: out, optional (may be NULL) i32[2] device scalars, ACCUMULATED into (caller
+ *           zeroes them): counts[0] += clamped exponents, counts[1] += invalid inputs
+ *           (non-finite alpha or a sign not in {-1,+1}; their exponent is EXP_ZERO).
+ * Steps: a group with alpha < 0 has its signs negated and keeps |alpha| (exact, reading R3);
+ * e = round(log2|alpha|) (exact integer mantissa rule), EXP_ZERO for alpha = +-0, clamped to
+ * [EXP_MIN, EXP_MAX].  Constraints: 1 <= q <= 8, N >= 1, K % 8 == 0, g % 8 == 0, K % g == 0;
+ * TILED additionally K % 256 == 0 and g % 128 == 0. */
+shiftadd_status shiftadd_pack(const int8_t* signs, const float* alpha, int q, int N, int K,
+                              int g, int layout, uint8_t* planes, int8_t* exps,
+                              int32_t* counts, void* stream);
+
+/* Workspace bytes a shiftadd_lut_gemm call with these arguments needs (0 if none).  The
+ * caller zeroes a fresh workspace once (cudaMemsetAsync).  Layout: 256 KB of split-K arrival
+ * counters at offset 0, then fp32 partials; every call leaves the counter region zeroed
+ * again, so one workspace can be reused by calls of any shape without re-clearing.  One
+ * workspace must not be used by two calls that can run concurrently.  N <= 1,048,576. */
+size_t shiftadd_workspace_bytes(int layout, int M, int N, int K, int q, int g);
+
+/* a2-a7 -- shift-and-add LUT-GEMM, M in [1, 16] (App. D :804-817):
+ *   y[m][n] = fp16_rne( sum_i sum_G 2^{e[i][n][G]} sum_{k in G} s(i,n,k) x[m][k] )
+ *   x    : fp16 [M][ldx], ldx >= K, rows 16-byte aligned
+ *   planes, exps : packed by shiftadd_pack in `layout`, with the same q, N, K, g
+ *   y    : fp16 [M][ldy], ldy >= N (a shard may write into a wider buffer)
+ *   workspace: shiftadd_workspace_bytes(...) bytes, 16-byte aligned (NULL if 0)
+ *   q    : 1..4 bits per weight of THIS layer (mixed-bit dispatch)
+ *   flags: 0 or SHIFTADD_FLAG_PDL
+ * Accumulation is fp32 in a fixed order per launch shape: results are bit-identical run to
+ * run on one device.  Exponents outside [EXP_MIN, EXP_MAX] (other than EXP_ZERO) are
+ * undefined behaviour (pack never emits them).  NaN/Inf in x propagate to the outputs
+ * whose dot product they enter. */
+shiftadd_status shiftadd_lut_gemm(const uint16_t* x, int ldx, const uint8_t* planes,
+                                  const int8_t* exps, int layout, int M, int N, int K, int q,
+                                  int g, uint16_t* y, int ldy, void* workspace,
+                                  size_t workspace_bytes, unsigned flags, void* stream);
+
+/* Batch-1 convenience: shiftadd_lut_gemm with M = 1, ldx = K, ldy = N. */
+shiftadd_status shiftadd_lut_gemv(const uint16_t* x, const uint8_t* planes, const int8_t* exps,
+                                  int layout, int N, int K, int q, int g, uint16_t* y,
+                                  void* workspace, size_t workspace_bytes, unsigned flags,
+                                  void* stream);
+
+/* Launch geometry the gemm call would use (for measurement/reporting; host only):
+ * out[0] = grid CTAs, out[1] = threads per CTA, out[2] = dynamic smem bytes,
+ * out[3] = kernel id (0 generic, 1 tiled M=1, 2 tiled small-batch).  Needs a device. */
+shiftadd_status shiftadd_gemm_plan(int layout, int M, int N, int K, int q, int g, int out[4]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SHIFTADD_H */

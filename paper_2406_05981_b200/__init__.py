@@ -1,0 +1,224 @@
+"""B200-native ShiftAddLLM LUT-GEMV hot path (arxiv 2406.05981) -- thin Python binding.
+
+Every step of the path runs in the CUDA kernels of ``libshiftadd.so`` (built from ``csrc/``
+for sm_100a by ``__graft_entry__.build()``) behind the C ABI declared in
+``include/shiftadd.h``.  This module only marshals arguments: torch provides device memory,
+the current stream and (in ``dist``) the process group.  There is no CPU or eager fallback:
+if the library is missing or the device is not sm_100a, calls raise.
+
+    layer = pack(signs, alpha, g)          # §8 a1, on the device
+    y = lut_gemm(x, layer)                 # §8 a2-a7, x: fp16 [M][K] (M <= 16) or [K]
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from dataclasses import dataclass
+
+import torch
+
+__all__ = [
+    "LAYOUT_CANONICAL", "LAYOUT_TILED", "FLAG_PDL", "EXP_ZERO", "ShiftAddError", "lib",
+    "PackedLayer", "packed_bytes", "pack", "lut_gemm", "lut_gemv", "workspace_bytes",
+    "gemm_plan", "Workspace",
+]
+
+LAYOUT_CANONICAL = 0
+LAYOUT_TILED = 1
+FLAG_PDL = 1
+EXP_ZERO = -128
+_ABI_VERSION = 1
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libshiftadd.so")
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+class ShiftAddError(RuntimeError):
+    pass
+
+
+def lib():
+    """Load libshiftadd.so (once) and declare its C signatures.  Raises if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(_LIB_PATH):
+            raise ShiftAddError(
+                "libshiftadd.so not built (%s); run __graft_entry__.build() -- there is no "
+                "fallback path" % _LIB_PATH)
+        L = ctypes.CDLL(_LIB_PATH)
+        c_int, c_size, vp = ctypes.c_int, ctypes.c_size_t, ctypes.c_void_p
+        L.shiftadd_abi_version.restype = c_int
+        L.shiftadd_status_string.restype = ctypes.c_char_p
+        L.shiftadd_status_string.argtypes = [c_int]
+        L.shiftadd_last_error.restype = ctypes.c_char_p
+        L.shiftadd_packed_bytes.restype = c_size
+        L.shiftadd_packed_bytes.argtypes = [c_int, c_int, c_int, c_int, c_int, ctypes.POINTER(c_size)]
+        L.shiftadd_pack.restype = c_int
+        L.shiftadd_pack.argtypes = [vp, vp, c_int, c_int, c_int, c_int, c_int, vp, vp, vp, vp]
+        L.shiftadd_workspace_bytes.restype = c_size
+        L.shiftadd_workspace_bytes.argtypes = [c_int] * 6
+        L.shiftadd_lut_gemm.restype = c_int
+        L.shiftadd_lut_gemm.argtypes = [vp, c_int, vp, vp, c_int, c_int, c_int, c_int, c_int, c_int,
+                                        vp, c_int, vp, c_size, ctypes.c_uint, vp]
+        L.shiftadd_lut_gemv.restype = c_int
+        L.shiftadd_lut_gemv.argtypes = [vp, vp, vp, c_int, c_int, c_int, c_int, c_int, vp, vp, c_size,
+                                        ctypes.c_uint, vp]
+        L.shiftadd_gemm_plan.restype = c_int
+        L.shiftadd_gemm_plan.argtypes = [c_int] * 6 + [ctypes.POINTER(c_int * 4)]
+        v = L.shiftadd_abi_version()
+        if v != _ABI_VERSION:
+            raise ShiftAddError("libshiftadd ABI %d, binding expects %d" % (v, _ABI_VERSION))
+        _lib = L
+        return L
+
+
+def _check(status: int, what: str):
+    if status != 0:
+        L = lib()
+        raise ShiftAddError("%s failed: %s: %s" % (
+            what, L.shiftadd_status_string(status).decode(), L.shiftadd_last_error().decode()))
+
+
+def _stream_ptr(stream, device):
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def packed_bytes(layout: int, q: int, N: int, K: int, g: int):
+    """(plane bytes, exponent bytes) of a packed layer in ``layout``."""
+    e = ctypes.c_size_t(0)
+    p = lib().shiftadd_packed_bytes(layout, q, N, K, g, ctypes.byref(e))
+    if p == 0:
+        _check(2, "packed_bytes")
+    return int(p), int(e.value)
+
+
+@dataclass
+class PackedLayer:
+    """A reparameterised linear layer on the device (output of ``pack``)."""
+    planes: torch.Tensor      # uint8, layout-dependent permutation of [q][N][K/8]
+    exps: torch.Tensor        # int8, layout-dependent permutation of [q][N][K/g]
+    q: int
+    N: int
+    K: int
+    g: int
+    layout: int
+    counts: torch.Tensor      # int32[2] on device: clamped exponents, invalid inputs
+
+    @property
+    def device(self):
+        return self.planes.device
+
+    def nbytes(self) -> int:
+        return self.planes.numel() + self.exps.numel()
+
+
+def pack(signs: torch.Tensor, alpha: torch.Tensor, g: int, layout: int = LAYOUT_TILED,
+         stream=None) -> PackedLayer:
+    """§8 a1 on the device: int8 sign planes [q][N][K] and fp32 scales [q][N][K/g] -> key
+    bytes + PoT exponents (shiftadd_pack)."""
+    if signs.dtype != torch.int8 or alpha.dtype != torch.float32:
+        raise TypeError("signs must be int8 and alpha float32")
+    if not (signs.is_cuda and alpha.is_cuda):
+        raise ValueError("pack runs on the GPU; pass CUDA tensors")
+    if signs.dim() != 3 or alpha.dim() != 3:
+        raise ValueError("signs [q][N][K], alpha [q][N][K/g]")
+    q, N, K = signs.shape
+    if tuple(alpha.shape) != (q, N, K // g if g else 0):
+        raise ValueError("alpha must be [q][N][K/g]")
+    signs = signs.contiguous()
+    alpha = alpha.contiguous()
+    pb, eb = packed_bytes(layout, q, N, K, g)
+    dev = signs.device
+    planes = torch.empty(pb, dtype=torch.uint8, device=dev)
+    exps = torch.empty(eb, dtype=torch.int8, device=dev)
+    counts = torch.zeros(2, dtype=torch.int32, device=dev)
+    with torch.cuda.device(dev):
+        st = lib().shiftadd_pack(_ptr(signs), _ptr(alpha), q, N, K, g, layout, _ptr(planes), _ptr(exps),
+                                 _ptr(counts), _stream_ptr(stream, dev))
+    _check(st, "shiftadd_pack")
+    return PackedLayer(planes, exps, q, N, K, g, layout, counts)
+
+
+def workspace_bytes(layer: PackedLayer, M: int) -> int:
+    return int(lib().shiftadd_workspace_bytes(layer.layout, M, layer.N, layer.K, layer.q, layer.g))
+
+
+class Workspace:
+    """A zero-initialised device scratch buffer that grows on demand.  Calls leave it zeroed
+    (the kernels reset their arrival counters), so it is reused without re-clearing.  Do not
+    share one Workspace between calls that may run concurrently on different streams."""
+
+    def __init__(self, device):
+        self.device = torch.device(device)
+        self.buf = None
+
+    def get(self, nbytes: int):
+        if nbytes == 0:
+            return None
+        if self.buf is None or self.buf.numel() < nbytes:
+            self.buf = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=self.device)
+        return self.buf
+
+
+_default_ws = {}
+
+
+def _workspace_for(device):
+    key = (device.index, torch.cuda.current_stream(device).cuda_stream)
+    ws = _default_ws.get(key)
+    if ws is None:
+        ws = _default_ws[key] = Workspace(device)
+    return ws
+
+
+def lut_gemm(x: torch.Tensor, layer: PackedLayer, out: torch.Tensor | None = None,
+             workspace: Workspace | None = None, pdl: bool = False, stream=None) -> torch.Tensor:
+    """§8 a2-a7: y[M][N] = x[M][K] (.) the packed layer, fp16 in/out (shiftadd_lut_gemm)."""
+    squeeze = x.dim() == 1
+    x2 = x.unsqueeze(0) if squeeze else x
+    if x2.dtype != torch.float16 or not x2.is_cuda or x2.device != layer.device:
+        raise ValueError("x must be fp16 on the layer's device")
+    if x2.stride(-1) != 1:
+        x2 = x2.contiguous()
+    M, K = x2.shape
+    if K != layer.K:
+        raise ValueError("x has K=%d, layer has K=%d" % (K, layer.K))
+    dev = layer.device
+    if out is None:
+        out = torch.empty((M, layer.N), dtype=torch.float16, device=dev)
+    if out.dtype != torch.float16 or out.dim() != 2 or out.shape[0] != M or out.stride(-1) != 1:
+        raise ValueError("out must be fp16 [M][>=N] with unit column stride")
+    need = workspace_bytes(layer, M)
+    ws = (workspace or _workspace_for(dev)).get(need)
+    with torch.cuda.device(dev):
+        st = lib().shiftadd_lut_gemm(_ptr(x2), x2.stride(0), _ptr(layer.planes), _ptr(layer.exps), layer.layout,
+                                     M, layer.N, layer.K, layer.q, layer.g, _ptr(out), out.stride(0),
+                                     _ptr(ws), ws.numel() if ws is not None else 0,
+                                     FLAG_PDL if pdl else 0, _stream_ptr(stream, dev))
+    _check(st, "shiftadd_lut_gemm")
+    return out[0] if squeeze else out
+
+
+def lut_gemv(x: torch.Tensor, layer: PackedLayer, **kw) -> torch.Tensor:
+    """Batch-1 form: x fp16 [K] -> y fp16 [N]."""
+    return lut_gemm(x.reshape(-1), layer, **kw)
+
+
+def gemm_plan(layer: PackedLayer, M: int):
+    """(grid, threads, dynamic smem bytes, kernel id) the call would launch with."""
+    out = (ctypes.c_int * 4)()
+    _check(lib().shiftadd_gemm_plan(layer.layout, M, layer.N, layer.K, layer.q, layer.g, ctypes.byref(out)),
+           "shiftadd_gemm_plan")
+    return tuple(out)

@@ -1,0 +1,216 @@
+// abi.cu -- the extern "C" boundary of libshiftadd (include/shiftadd.h, §8(b)).
+//
+// Synchronous argument validation (nothing is launched on failure), device checks, the
+// mixed-bit dispatch of §8 a6 (q -> template instance, host side, no device cost) and the
+// layout/batch dispatch between the kernels.  No exceptions cross the boundary.
+#include <cstdarg>
+#include <cstdio>
+#include <mutex>
+#include <string>
+
+#include "common.cuh"
+
+namespace shiftadd {
+namespace {
+
+thread_local std::string g_last_error;
+
+shiftadd_status fail(shiftadd_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return st;
+}
+
+shiftadd_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(SHIFTADD_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+struct DevInfo {
+  cudaError_t err;
+  int major, minor, sms;
+};
+
+// Immutable per-device facts, computed once per device.
+shiftadd_status device_info(DevInfo* out) {
+  static std::once_flag once[64];
+  static DevInfo info[64];
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  if (dev < 0 || dev >= 64) return fail(SHIFTADD_ERR_CUDA, "device ordinal %d out of range", dev);
+  std::call_once(once[dev], [dev] {
+    DevInfo d{cudaSuccess, 0, 0, 0};
+    d.err = cudaDeviceGetAttribute(&d.major, cudaDevAttrComputeCapabilityMajor, dev);
+    if (d.err == cudaSuccess) d.err = cudaDeviceGetAttribute(&d.minor, cudaDevAttrComputeCapabilityMinor, dev);
+    if (d.err == cudaSuccess) d.err = cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+    info[dev] = d;
+  });
+  *out = info[dev];
+  if (out->err != cudaSuccess) return cuda_fail(out->err, "cudaDeviceGetAttribute");
+  if (out->major != 10 || out->minor != 0)
+    return fail(SHIFTADD_ERR_CUDA, "device %d is sm_%d%d; this library is built for sm_100a only", dev,
+                out->major, out->minor);
+  return SHIFTADD_OK;
+}
+
+shiftadd_status check_shape(int q, int N, int K, int g, int max_q) {
+  if (q < 1 || q > max_q) return fail(SHIFTADD_ERR_INVALID, "q=%d outside [1, %d]", q, max_q);
+  if (N < 1 || K < 8) return fail(SHIFTADD_ERR_INVALID, "need N >= 1 and K >= 8 (N=%d, K=%d)", N, K);
+  if (N > kCounterSlots * kTileRows) return fail(SHIFTADD_ERR_INVALID, "N=%d above %d", N, kCounterSlots * kTileRows);
+  if (K % 8) return fail(SHIFTADD_ERR_INVALID, "K=%d is not a multiple of 8", K);
+  if (g < 8 || g % 8 || K % g) return fail(SHIFTADD_ERR_INVALID, "need 8 | g and g | K (g=%d, K=%d)", g, K);
+  return SHIFTADD_OK;
+}
+
+shiftadd_status check_layout(int layout, int K, int g) {
+  if (layout == SHIFTADD_LAYOUT_CANONICAL) return SHIFTADD_OK;
+  if (layout != SHIFTADD_LAYOUT_TILED) return fail(SHIFTADD_ERR_INVALID, "unknown layout %d", layout);
+  if (K % kTileK) return fail(SHIFTADD_ERR_INVALID, "tiled layout needs K %% 256 == 0 (K=%d)", K);
+  if (g % 128) return fail(SHIFTADD_ERR_INVALID, "tiled layout needs g %% 128 == 0 (g=%d)", g);
+  return SHIFTADD_OK;
+}
+
+size_t tiled_rows(int N) { return (size_t)((N + kTileRows - 1) / kTileRows); }
+
+LaunchPlan make_plan(int layout, int M, int N, int K, int q, int g, int sms) {
+  if (layout == SHIFTADD_LAYOUT_CANONICAL) return plan_generic(M, N, K, q, g, sms);
+  if (M == 1) return plan_gemv_tiled(N, K, q, sms);
+  return plan_gemm_tiled_mb(M, N, K, q, sms);
+}
+
+size_t workspace_for(int layout, int M, int N, int K) {
+  if (layout == SHIFTADD_LAYOUT_CANONICAL) return 0;
+  if (M == 1) return workspace_gemv_tiled(N, K);
+  return workspace_gemm_tiled_mb(M, N, K);
+}
+
+}  // namespace
+}  // namespace shiftadd
+
+using namespace shiftadd;
+
+extern "C" {
+
+int shiftadd_abi_version(void) { return SHIFTADD_ABI_VERSION; }
+
+const char* shiftadd_status_string(int status) {
+  switch (status) {
+    case SHIFTADD_OK: return "ok";
+    case SHIFTADD_ERR_INVALID: return "invalid argument";
+    case SHIFTADD_ERR_UNSUPPORTED: return "unsupported";
+    case SHIFTADD_ERR_CUDA: return "cuda error";
+    default: return "unknown status";
+  }
+}
+
+const char* shiftadd_last_error(void) { return g_last_error.c_str(); }
+
+size_t shiftadd_packed_bytes(int layout, int q, int N, int K, int g, size_t* exps_bytes) {
+  if (exps_bytes) *exps_bytes = 0;
+  if (check_shape(q, N, K, g, 8) != SHIFTADD_OK || check_layout(layout, K, g) != SHIFTADD_OK) return 0;
+  if (layout == SHIFTADD_LAYOUT_CANONICAL) {
+    if (exps_bytes) *exps_bytes = (size_t)q * N * (K / g);
+    return (size_t)q * N * (K / 8);
+  }
+  const size_t tiles = (size_t)(K / kTileK) * tiled_rows(N) * q;
+  if (exps_bytes) *exps_bytes = tiles * kTileExps;
+  return tiles * kTileBytes;
+}
+
+shiftadd_status shiftadd_pack(const int8_t* signs, const float* alpha, int q, int N, int K, int g,
+                              int layout, uint8_t* planes, int8_t* exps, int32_t* counts, void* stream) {
+  if (!signs || !alpha || !planes || !exps) return fail(SHIFTADD_ERR_INVALID, "null pointer argument");
+  shiftadd_status st = check_shape(q, N, K, g, 8);
+  if (st != SHIFTADD_OK) return st;
+  if ((st = check_layout(layout, K, g)) != SHIFTADD_OK) return st;
+  if (!aligned(signs, 8) || !aligned(alpha, 4) || !aligned(planes, 16) || (counts && !aligned(counts, 4)))
+    return fail(SHIFTADD_ERR_INVALID, "misaligned pointer (signs 8 B, alpha 4 B, planes 16 B)");
+  DevInfo di;
+  if ((st = device_info(&di)) != SHIFTADD_OK) return st;
+  cudaError_t e = launch_pack(signs, alpha, q, N, K, g, layout, planes, exps, counts,
+                              reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "pack launch");
+  return SHIFTADD_OK;
+}
+
+size_t shiftadd_workspace_bytes(int layout, int M, int N, int K, int q, int g) {
+  if (check_shape(q, N, K, g, 4) != SHIFTADD_OK || check_layout(layout, K, g) != SHIFTADD_OK) return 0;
+  if (M < 1 || M > 16) return 0;
+  return workspace_for(layout, M, N, K);
+}
+
+shiftadd_status shiftadd_gemm_plan(int layout, int M, int N, int K, int q, int g, int out[4]) {
+  if (!out) return fail(SHIFTADD_ERR_INVALID, "null out");
+  shiftadd_status st = check_shape(q, N, K, g, 4);
+  if (st != SHIFTADD_OK) return st;
+  if ((st = check_layout(layout, K, g)) != SHIFTADD_OK) return st;
+  if (M < 1 || M > 16) return fail(SHIFTADD_ERR_UNSUPPORTED, "M=%d outside [1, 16]", M);
+  DevInfo di;
+  if ((st = device_info(&di)) != SHIFTADD_OK) return st;
+  const LaunchPlan p = make_plan(layout, M, N, K, q, g, di.sms);
+  out[0] = p.grid;
+  out[1] = p.threads;
+  out[2] = p.smem;
+  out[3] = p.kernel;
+  return SHIFTADD_OK;
+}
+
+shiftadd_status shiftadd_lut_gemm(const uint16_t* x, int ldx, const uint8_t* planes, const int8_t* exps,
+                                  int layout, int M, int N, int K, int q, int g, uint16_t* y, int ldy,
+                                  void* workspace, size_t workspace_bytes, unsigned flags, void* stream) {
+  if (!x || !planes || !exps || !y) return fail(SHIFTADD_ERR_INVALID, "null pointer argument");
+  shiftadd_status st = check_shape(q, N, K, g, 4);
+  if (st != SHIFTADD_OK) return st;
+  if ((st = check_layout(layout, K, g)) != SHIFTADD_OK) return st;
+  if (M < 1) return fail(SHIFTADD_ERR_INVALID, "M=%d < 1", M);
+  if (M > 16) return fail(SHIFTADD_ERR_UNSUPPORTED, "M=%d > 16 (small-batch kernels cover M <= 16)", M);
+  if (ldx < K || ldy < N) return fail(SHIFTADD_ERR_INVALID, "ldx=%d < K=%d or ldy=%d < N=%d", ldx, K, ldy, N);
+  if (flags & ~SHIFTADD_FLAG_PDL) return fail(SHIFTADD_ERR_INVALID, "unknown flags 0x%x", flags);
+  if (!aligned(x, 16) || (M > 1 && (ldx % 8)) || !aligned(planes, 16) || !aligned(y, 2))
+    return fail(SHIFTADD_ERR_INVALID, "misaligned pointer (x rows and planes need 16 B)");
+  const size_t need = workspace_for(layout, M, N, K);
+  if (need > 0 && (!workspace || workspace_bytes < need || !aligned(workspace, 16)))
+    return fail(SHIFTADD_ERR_INVALID, "workspace needs %zu bytes, 16-B aligned (got %zu)", need, workspace_bytes);
+  DevInfo di;
+  if ((st = device_info(&di)) != SHIFTADD_OK) return st;
+
+  GemmArgs a;
+  a.x = reinterpret_cast<const __half*>(x);
+  a.ldx = ldx;
+  a.planes = planes;
+  a.exps = exps;
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.q = q;
+  a.g = g;
+  a.y = reinterpret_cast<__half*>(y);
+  a.ldy = ldy;
+  a.workspace = workspace;
+  a.workspace_bytes = workspace_bytes;
+  a.flags = flags;
+  a.stream = reinterpret_cast<cudaStream_t>(stream);
+  const LaunchPlan p = make_plan(layout, M, N, K, q, g, di.sms);
+  cudaError_t e;
+  if (layout == SHIFTADD_LAYOUT_CANONICAL) e = launch_gemm_generic(a, p);
+  else if (M == 1) e = launch_gemv_tiled(a, p);
+  else e = launch_gemm_tiled_mb(a, p);
+  if (e == cudaErrorNotSupported) return fail(SHIFTADD_ERR_UNSUPPORTED, "no kernel for this configuration");
+  if (e != cudaSuccess) return cuda_fail(e, "lut_gemm launch");
+  return SHIFTADD_OK;
+}
+
+shiftadd_status shiftadd_lut_gemv(const uint16_t* x, const uint8_t* planes, const int8_t* exps, int layout,
+                                  int N, int K, int q, int g, uint16_t* y, void* workspace,
+                                  size_t workspace_bytes, unsigned flags, void* stream) {
+  return shiftadd_lut_gemm(x, K, planes, exps, layout, 1, N, K, q, g, y, N, workspace, workspace_bytes, flags,
+                           stream);
+}
+
+}  // extern "C"

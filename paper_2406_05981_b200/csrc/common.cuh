@@ -1,0 +1,133 @@
+// common.cuh -- shared device helpers and internal launch interfaces of libshiftadd.
+// Product code only: nothing here is shared with oracle/ (which is test infrastructure).
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "shiftadd.h"
+
+namespace shiftadd {
+
+// Device-tiled layout geometry (include/shiftadd.h, SHIFTADD_LAYOUT_TILED).
+constexpr int kTileRows = 16;    // output rows per tile
+constexpr int kTileK = 256;      // reduction indices per tile (32 key bytes per row)
+constexpr int kTileBytes = 512;  // 16 rows x 32 key bytes
+constexpr int kTileExps = 32;    // 16 rows x 2 chunk exponents
+// Split-K workspace: a fixed region of per-row-group arrival counters at offset 0 (so a later
+// call of any shape finds its counters zeroed -- the last CTA of each row group resets its
+// counter), then the fp32 partials.  Bounds N at kCounterSlots * 16 rows.
+constexpr int kCounterSlots = 65536;
+constexpr size_t kCounterBytes = (size_t)kCounterSlots * sizeof(int);
+
+// LUT slab in shared memory for one 256-k slice: 256 keys x 64 words.  Word (key, col):
+// cols 0..31 hold the 32 groups of an even slice segment, cols 32..63 of an odd one, so a
+// CTA can build the next slice's LUT without waiting for the current one to drain.
+constexpr int kLutBytes = 256 * 256;
+// The LUT is pinned at shared-window address 64 KB (kLutBase): the byte address of entry
+// (key, col) is then 0x10000 | key << 8 | col*4, which one PRMT assembles from the key byte
+// and a per-lane constant -- no base-address add per lookup.  The kernels request enough
+// dynamic shared memory to cover [kLutBase, kLutBase + LUT size) and trap if the runtime
+// placed their dynamic region above kLutBase.
+constexpr uint32_t kLutBase = 0x10000u;
+
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float4 lds_f32x4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts_f32(uint32_t addr, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ void sts_f32x4(uint32_t addr, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+// Guard for the fixed LUT placement (see kLutBase).
+__device__ __forceinline__ void check_lut_window(const void* dyn_smem) {
+  if ((uint32_t)__cvta_generic_to_shared(dyn_smem) > kLutBase) __trap();
+}
+
+// a4 -- the "shift" (App. H :974; DenseShift): p * 2^e as an integer add
+// on the fp32 exponent field.  Guarded: +-0 stays 0 and Inf/NaN pass through; every other
+// p this kernel produces is a normal fp32 (sums of fp16 values are multiples of 2^-24, so
+// |p| >= 2^-24, and |p| <= 2^24 for one 128-k chunk) and e in [-100, 100] keeps p * 2^e
+// normal, so the add is bit-identical to the multiply.  e == EXP_ZERO contributes 0.
+__device__ __forceinline__ float shift_pow2(float p, int e) {
+  const uint32_t b = __float_as_uint(p);
+  const uint32_t ex = b & 0x7f800000u;
+  const uint32_t r = ((ex - 0x00800000u) < 0x7f000000u) ? b + ((uint32_t)e << 23) : b;
+  return (e == -128) ? 0.f : __uint_as_float(r);
+}
+
+// Programmatic dependent launch (sm_90+): wait for the upstream grid before touching
+// anything it may produce or consume (x, y, workspace); let dependents start early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" :::);
+}
+
+// Streaming 16-byte weight load: read-only path, no L1 allocation (each byte is used once).
+__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+// One unit (slice s, row group rg) of the tiled layout: Q plane tiles of 512 B (lane reads
+// its 16 B) and Q x 32 chunk exponents (lane reads its byte).
+template <int Q>
+__device__ __forceinline__ void load_unit(const uint4* __restrict__ planes, const int8_t* __restrict__ exps,
+                                          long long u, int lane, uint4 (&w)[Q], int (&e)[Q]) {
+#pragma unroll
+  for (int i = 0; i < Q; ++i) w[i] = ldg_stream(planes + (u * Q + i) * 32 + lane);
+#pragma unroll
+  for (int i = 0; i < Q; ++i) e[i] = __ldg(exps + (u * Q + i) * 32 + lane);
+}
+
+struct GemmArgs {
+  const __half* x;
+  int ldx;
+  const uint8_t* planes;
+  const int8_t* exps;
+  int M, N, K, q, g;
+  __half* y;
+  int ldy;
+  void* workspace;
+  size_t workspace_bytes;
+  unsigned flags;
+  cudaStream_t stream;
+};
+
+struct LaunchPlan {
+  int grid;
+  int threads;
+  int smem;
+  int kernel;  // 0 generic, 1 tiled M=1, 2 tiled small batch
+};
+
+// Implemented in the kernel translation units.
+cudaError_t launch_pack(const int8_t* signs, const float* alpha, int q, int N, int K, int g,
+                        int layout, uint8_t* planes, int8_t* exps, int32_t* counts,
+                        cudaStream_t stream);
+
+LaunchPlan plan_generic(int M, int N, int K, int q, int g, int sms);
+cudaError_t launch_gemm_generic(const GemmArgs& a, const LaunchPlan& p);
+
+LaunchPlan plan_gemv_tiled(int N, int K, int q, int sms);
+size_t workspace_gemv_tiled(int N, int K);
+cudaError_t launch_gemv_tiled(const GemmArgs& a, const LaunchPlan& p);
+
+LaunchPlan plan_gemm_tiled_mb(int M, int N, int K, int q, int sms);
+size_t workspace_gemm_tiled_mb(int M, int N, int K);
+cudaError_t launch_gemm_tiled_mb(const GemmArgs& a, const LaunchPlan& p);
+
+}  // namespace shiftadd

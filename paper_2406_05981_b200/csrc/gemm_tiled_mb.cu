@@ -1,0 +1,262 @@
+// gemm_tiled_mb.cu -- §8 a7: small-batch (2 <= M <= 16) LUT-GEMM on the tiled layout.
+//
+// Same work decomposition, lane mapping and split-K reduction as gemv_tiled.cu, but each
+// LUT entry carries the partial sums of MC = 4 batch rows (one float4), so one key byte
+// loaded from HBM and one 16-byte LDS serve 4 rows (App. D :804-817 evaluates
+// batch 1/2/4/8).  Rows are processed in ceil(M/4) chunks; the CTA re-walks its own units
+// for each chunk, which it just read, so chunks after the first stream from L2.
+//
+// LUT slab for one 256-k slice and one row chunk: 2 regions (h = chunk half of the tile) x
+// 256 keys x 16 columns x 16 B = 128 KB.  Entry (key, group t) lives at
+//     (t >> 4) * 64 KB + key * 256 + ((t & 15) ^ (4 * (t >> 4))) * 16
+// -- one PRMT builds it from the key byte.  The XOR swizzle makes the 8 lanes of every
+// LDS.128 phase (rows r..r+3, halves 0/1) hit 8 distinct 16-B bank quads: conflict free.
+// With M rows the smem traffic per weight byte is 4*M bytes, so for M >= 2 the shared-
+// memory bandwidth (128 B/clk/SM), not HBM, is the roof.
+#include <mutex>
+
+#include "common.cuh"
+
+namespace shiftadd {
+namespace {
+
+constexpr int kMC = 4;                       // batch rows per LUT entry
+constexpr int kLutMbBytes = 2 * 256 * 256;   // 128 KB
+constexpr int kDynSmemMb = (int)kLutBase + kLutMbBytes;  // covers [64 KB, 192 KB)
+
+template <int NW>
+__device__ __forceinline__ void build_lut4(const __half* __restrict__ x, int ldx, int m0, int M, int s,
+                                           int warp, int lane) {
+  // thread (warp w, lane t): group t of the slice, every hi nibble assigned to the warp.
+  float L[kMC][16];
+  float X4[kMC][4];  // x4..x7 of each row, for the hi-nibble half sums
+#pragma unroll
+  for (int mm = 0; mm < kMC; ++mm) {
+    float xv[8];
+    if (m0 + mm < M) {
+      const uint4 raw = *reinterpret_cast<const uint4*>(x + (size_t)(m0 + mm) * ldx + s * kTileK + 8 * lane);
+      const __half2* hp = reinterpret_cast<const __half2*>(&raw);
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const float2 f = __half22float2(hp[b]);
+        xv[2 * b] = f.x;
+        xv[2 * b + 1] = f.y;
+      }
+    } else {
+#pragma unroll
+      for (int b = 0; b < 8; ++b) xv[b] = 0.f;
+    }
+    const float A[4] = {-xv[0] - xv[1], xv[0] - xv[1], xv[1] - xv[0], xv[0] + xv[1]};
+    const float B[4] = {-xv[2] - xv[3], xv[2] - xv[3], xv[3] - xv[2], xv[2] + xv[3]};
+#pragma unroll
+    for (int lo = 0; lo < 16; ++lo) L[mm][lo] = A[lo & 3] + B[lo >> 2];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) X4[mm][b] = xv[4 + b];
+  }
+  const int t = lane;
+  const uint32_t col = kLutBase + (t >> 4) * 65536 + (((t & 15) ^ (4 * (t >> 4))) << 4);
+#pragma unroll
+  for (int hh = 0; hh < 16 / NW; ++hh) {
+    const int hi = warp + NW * hh;
+    float H[kMC];
+#pragma unroll
+    for (int mm = 0; mm < kMC; ++mm)
+      H[mm] = ((hi & 1 ? X4[mm][0] : -X4[mm][0]) + (hi & 2 ? X4[mm][1] : -X4[mm][1])) +
+              ((hi & 4 ? X4[mm][2] : -X4[mm][2]) + (hi & 8 ? X4[mm][3] : -X4[mm][3]));
+#pragma unroll
+    for (int lo = 0; lo < 16; ++lo) {
+      float4 v;
+      v.x = L[0][lo] + H[0];
+      v.y = L[1][lo] + H[1];
+      v.z = L[2][lo] + H[2];
+      v.w = L[3][lo] + H[3];
+      sts_f32x4(col + ((hi * 16 + lo) << 8), v);
+    }
+  }
+}
+
+template <int Q>
+__device__ __forceinline__ void unit_dot4(const uint4 (&w)[Q], const int (&e)[Q], const uint32_t (&cst)[16],
+                                          float (&acc)[kMC]) {
+#pragma unroll
+  for (int mm = 0; mm < kMC; ++mm) acc[mm] = 0.f;
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f), p1 = p0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const uint32_t word = (j < 4) ? w[i].x : (j < 8) ? w[i].y : (j < 12) ? w[i].z : w[i].w;
+      // byte0 <- swizzled col*16, byte1 <- key, byte2 <- 1 + region h, byte3 <- 0
+      const uint32_t addr = __byte_perm(word, cst[j], 0x7604u | ((uint32_t)(j & 3) << 4));
+      const float4 v = lds_f32x4(addr);
+      if (j & 1) { p1.x += v.x; p1.y += v.y; p1.z += v.z; p1.w += v.w; }
+      else { p0.x += v.x; p0.y += v.y; p0.z += v.z; p0.w += v.w; }
+    }
+    acc[0] += shift_pow2(p0.x + p1.x, e[i]);
+    acc[1] += shift_pow2(p0.y + p1.y, e[i]);
+    acc[2] += shift_pow2(p0.z + p1.z, e[i]);
+    acc[3] += shift_pow2(p0.w + p1.w, e[i]);
+  }
+}
+
+template <int Q, int NW>
+__global__ void __launch_bounds__(NW * 32, 1)
+gemm_tiled_mb_kernel(const __half* __restrict__ x, int ldx, const uint4* __restrict__ planes,
+                     const int8_t* __restrict__ exps, int M, int N, int S, int RG, long long U,
+                     __half* __restrict__ y, int ldy, float* __restrict__ partial, int* __restrict__ counters,
+                     int pdl) {
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
+  __shared__ int fin_list[NW * 32];
+  __shared__ int fin_count;
+  check_lut_window(dyn_smem);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int r = lane >> 1, h = lane & 1;
+  const long long G = gridDim.x;
+  const long long u0 = ((long long)blockIdx.x * U) / G;
+  const long long u1 = ((long long)(blockIdx.x + 1) * U) / G;
+  const size_t Npad = (size_t)RG * kTileRows;
+
+  uint32_t cst[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    cst[j] = kLutBase + ((uint32_t)((((j + r) & 15) ^ (4 * h)) << 4)) + ((uint32_t)h << 16);
+
+  uint4 wa[Q], wb[Q];
+  int ea[Q], eb[Q];
+  bool waited = false;
+  for (int m0 = 0; m0 < M; m0 += kMC) {
+    long long u = u0;
+    while (u < u1) {
+      const int s = (int)(u / RG);
+      const long long seg_end = min(u1, (long long)(s + 1) * RG);
+      long long uu = u + warp;
+      if (uu < seg_end) load_unit<Q>(planes, exps, uu, lane, wa, ea);
+      if (!waited) {
+        if (pdl) pdl_wait();
+        waited = true;
+      }
+      __syncthreads();  // previous LUT fully consumed
+      build_lut4<NW>(x, ldx, m0, M, s, warp, lane);
+      __syncthreads();
+      const long long rg_base = (long long)s * RG;
+      for (; uu < seg_end; uu += NW) {
+        const long long un = uu + NW;
+        if (un < seg_end) load_unit<Q>(planes, exps, un, lane, wb, eb);
+        float acc[kMC];
+        unit_dot4<Q>(wa, ea, cst, acc);
+#pragma unroll
+        for (int mm = 0; mm < kMC; ++mm) acc[mm] += __shfl_xor_sync(0xffffffffu, acc[mm], 1);
+        const int n = (int)(uu - rg_base) * kTileRows + r;
+        if (h == 0) {
+#pragma unroll
+          for (int mm = 0; mm < kMC; ++mm) {
+            const int m = m0 + mm;
+            if (m < M) {
+              if (S == 1) { if (n < N) y[(size_t)m * ldy + n] = __float2half_rn(acc[mm]); }
+              else partial[((size_t)m * S + s) * Npad + n] = acc[mm];
+            }
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < Q; ++i) { wa[i] = wb[i]; ea[i] = eb[i]; }
+      }
+      u = seg_end;
+    }
+  }
+  if (pdl) pdl_launch_dependents();
+  if (S == 1) return;
+
+  __threadfence();
+  __syncthreads();
+  for (long long ub = u0; ub < u1; ub += NW * 32) {
+    if (tid == 0) fin_count = 0;
+    __syncthreads();
+    const long long uq = ub + tid;
+    if (uq < u1) {
+      const int rg = (int)(uq % RG);
+      if (atomicAdd(&counters[rg], 1) == S - 1) fin_list[atomicAdd(&fin_count, 1)] = rg;
+    }
+    __syncthreads();
+    const int nf = fin_count;
+    if (nf > 0) {
+      __threadfence();
+      for (int f = warp; f < nf; f += NW) {
+        const int rg = fin_list[f];
+        const int rr = lane & 15, part = lane >> 4;
+        const int n = rg * kTileRows + rr;
+        for (int m = 0; m < M; ++m) {
+          float sum = 0.f;
+          for (int s = part; s < S; s += 2) sum += __ldcg(partial + ((size_t)m * S + s) * Npad + n);
+          sum += __shfl_xor_sync(0xffffffffu, sum, 16);
+          if (part == 0 && n < N) y[(size_t)m * ldy + n] = __float2half_rn(sum);
+        }
+        if (lane == 0) counters[rg] = 0;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+constexpr int kNW = 16;
+
+template <int Q>
+cudaError_t launch_q(const GemmArgs& a, const LaunchPlan& p) {
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(gemm_tiled_mb_kernel<Q, kNW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kDynSmemMb);
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  const int S = a.K / kTileK;
+  const int RG = (a.N + kTileRows - 1) / kTileRows;
+  const long long U = (long long)S * RG;
+  const size_t Npad = (size_t)RG * kTileRows;
+  int* counters = S > 1 ? reinterpret_cast<int*>(a.workspace) : nullptr;
+  float* partial = S > 1 ? reinterpret_cast<float*>(reinterpret_cast<char*>(a.workspace) + kCounterBytes) : nullptr;
+  (void)Npad;
+  const int pdl = (a.flags & SHIFTADD_FLAG_PDL) ? 1 : 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.grid);
+  cfg.blockDim = dim3(p.threads);
+  cfg.dynamicSmemBytes = p.smem;
+  cfg.stream = a.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, gemm_tiled_mb_kernel<Q, kNW>, a.x, a.ldx,
+                            reinterpret_cast<const uint4*>(a.planes), a.exps, a.M, a.N, S, RG, U, a.y, a.ldy,
+                            partial, counters, pdl);
+}
+
+}  // namespace
+
+LaunchPlan plan_gemm_tiled_mb(int M, int N, int K, int q, int sms) {
+  (void)M; (void)q;
+  const long long S = K / kTileK;
+  const long long RG = (N + kTileRows - 1) / kTileRows;
+  const long long U = S * RG;
+  const long long grid = U < sms ? U : sms;
+  return LaunchPlan{(int)grid, kNW * 32, kDynSmemMb, 2};
+}
+
+size_t workspace_gemm_tiled_mb(int M, int N, int K) {
+  const size_t S = K / kTileK;
+  if (S <= 1) return 0;
+  const size_t RG = (N + kTileRows - 1) / kTileRows;
+  return kCounterBytes + (size_t)M * S * RG * kTileRows * sizeof(float);
+}
+
+cudaError_t launch_gemm_tiled_mb(const GemmArgs& a, const LaunchPlan& p) {
+  switch (a.q) {
+    case 1: return launch_q<1>(a, p);
+    case 2: return launch_q<2>(a, p);
+    case 3: return launch_q<3>(a, p);
+    case 4: return launch_q<4>(a, p);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace shiftadd

@@ -1,0 +1,130 @@
+"""CPU checks of the C-ABI library: it loads, exports every symbol include/shiftadd.h declares,
+and its host-side logic (sizes, validation) behaves -- no compute calls (no GPU here)."""
+
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "shiftadd.h")
+LIBPATH = os.path.join(ROOT, "paper_2406_05981_b200", "libshiftadd.so")
+
+
+@pytest.fixture(scope="module")
+def L():
+    if not os.path.exists(LIBPATH):
+        import __graft_entry__
+        __graft_entry__.build()
+    import paper_2406_05981_b200 as sa
+    return sa.lib()
+
+
+def _declared():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(shiftadd_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_header_declares_the_section8b_entry_points():
+    names = _declared()
+    for must in ("shiftadd_pack", "shiftadd_lut_gemv", "shiftadd_lut_gemm", "shiftadd_workspace_bytes",
+                 "shiftadd_abi_version", "shiftadd_status_string", "shiftadd_last_error"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol(L):
+    out = subprocess.run(["nm", "-D", "--defined-only", LIBPATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (shiftadd_\w+)", out))
+    for name in _declared():
+        assert name in exported, name
+        assert hasattr(L, name)
+
+
+def test_library_is_sm100a_only():
+    out = subprocess.run(["cuobjdump", "--list-elf", LIBPATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(80|86|89|90)\b", out)
+
+
+def test_abi_version_and_status_strings(L):
+    assert L.shiftadd_abi_version() == 1
+    assert L.shiftadd_status_string(0) == b"ok"
+    assert L.shiftadd_status_string(2) == b"invalid argument"
+    assert L.shiftadd_status_string(6) == b"unsupported"
+    assert L.shiftadd_status_string(7) == b"cuda error"
+
+
+@pytest.mark.parametrize("q,N,K,g", [(3, 768, 768, 128), (2, 4096, 4096, 128), (3, 11008, 4096, 128),
+                                     (1, 33, 512, 256), (4, 17, 256, 256)])
+def test_packed_bytes_match_oracle_accounting(L, q, N, K, g):
+    e = ctypes.c_size_t()
+    assert L.shiftadd_packed_bytes(0, q, N, K, g, ctypes.byref(e)) == oracle.packed_bytes(q, N, K, g)[0]
+    assert e.value == oracle.packed_bytes(q, N, K, g)[1]
+    p = L.shiftadd_packed_bytes(1, q, N, K, g, ctypes.byref(e))
+    assert (p, e.value) == oracle.tiled_sizes(q, N, K)
+
+
+def test_packed_bytes_rejects_bad_shapes(L):
+    e = ctypes.c_size_t()
+    assert L.shiftadd_packed_bytes(0, 3, 768, 100, 128, ctypes.byref(e)) == 0   # K % 8
+    assert L.shiftadd_packed_bytes(1, 3, 768, 768, 64, ctypes.byref(e)) == 0    # tiled needs 128 | g
+    assert L.shiftadd_packed_bytes(1, 3, 768, 640, 128, ctypes.byref(e)) == 0   # tiled needs 256 | K
+    assert L.shiftadd_packed_bytes(0, 9, 768, 768, 128, ctypes.byref(e)) == 0   # q <= 8
+    assert b"q=9" in L.shiftadd_last_error()
+
+
+def test_workspace_bytes(L):
+    # tiled M=1: S*Npad fp32 partials + RG counters; S == 1 needs none
+    S, RG = 4096 // 256, 4096 // 16
+    C = 65536 * 4  # fixed counter region
+    assert L.shiftadd_workspace_bytes(1, 1, 4096, 4096, 3, 128) == C + S * RG * 16 * 4
+    assert L.shiftadd_workspace_bytes(1, 1, 4096, 256, 3, 128) == 0
+    assert L.shiftadd_workspace_bytes(1, 8, 4096, 4096, 3, 128) == C + 8 * S * RG * 16 * 4
+    assert L.shiftadd_workspace_bytes(0, 1, 4096, 4096, 3, 128) == 0
+    assert L.shiftadd_workspace_bytes(1, 17, 4096, 4096, 3, 128) == 0
+
+
+def _buf(n, align=256):
+    raw = ctypes.create_string_buffer(n + align)
+    addr = (ctypes.addressof(raw) + align - 1) // align * align
+    return raw, ctypes.c_void_p(addr)
+
+
+def test_gemm_validation_happens_before_any_launch(L):
+    _r1, p = _buf(1 << 16)
+    _r2, p_odd = _buf(1 << 16)
+    odd = ctypes.c_void_p(p_odd.value + 2)
+    # null pointers
+    assert L.shiftadd_lut_gemm(None, 768, p, p, 1, 1, 768, 768, 3, 128, p, 768, None, 0, 0, None) == 2
+    # q out of range, M too large, ld too small, bad layout, unknown flags, misaligned x
+    assert L.shiftadd_lut_gemm(p, 768, p, p, 1, 1, 768, 768, 5, 128, p, 768, None, 0, 0, None) == 2
+    assert L.shiftadd_lut_gemm(p, 768, p, p, 1, 17, 768, 768, 3, 128, p, 768, None, 0, 0, None) == 6
+    assert L.shiftadd_lut_gemm(p, 700, p, p, 1, 1, 768, 768, 3, 128, p, 768, None, 0, 0, None) == 2
+    assert L.shiftadd_lut_gemm(p, 768, p, p, 7, 1, 768, 768, 3, 128, p, 768, None, 0, 0, None) == 2
+    assert L.shiftadd_lut_gemm(p, 768, p, p, 1, 1, 768, 768, 3, 128, p, 768, None, 0, 8, None) == 2
+    assert L.shiftadd_lut_gemm(odd, 768, p, p, 1, 1, 768, 768, 3, 128, p, 768, None, 0, 0, None) == 2
+    # missing workspace for a split-K shape
+    assert L.shiftadd_lut_gemm(p, 4096, p, p, 1, 1, 4096, 4096, 3, 128, p, 4096, None, 0, 0, None) == 2
+    assert b"workspace" in L.shiftadd_last_error()
+    # pack: bad sign alignment / null
+    assert L.shiftadd_pack(None, p, 3, 16, 256, 128, 1, p, p, None, None) == 2
+    assert L.shiftadd_pack(odd, p, 3, 16, 256, 128, 1, p, p, None, None) == 2
+
+
+def test_valid_call_without_a_gpu_reports_cuda_error(L):
+    _r, p = _buf(1 << 20)
+    st = L.shiftadd_lut_gemm(p, 768, p, p, 0, 1, 768, 768, 3, 128, p, 768, None, 0, 0, None)
+    assert st == 7 and len(L.shiftadd_last_error()) > 0
+
+
+def test_python_binding_fails_loudly_without_gpu_tensors():
+    import torch
+    import paper_2406_05981_b200 as sa
+    with pytest.raises(ValueError):
+        sa.pack(torch.ones((1, 16, 256), dtype=torch.int8), torch.ones((1, 16, 2)), 128)
