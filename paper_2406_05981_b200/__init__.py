@@ -15,7 +15,7 @@ from __future__ import annotations
 import ctypes
 import os
 import threading
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import torch
 
@@ -115,6 +115,7 @@ class PackedLayer:
     g: int
     layout: int
     counts: torch.Tensor      # int32[2] on device: clamped exponents, invalid inputs
+    _ws_bytes: dict = field(default_factory=dict, repr=False)   # M -> workspace bytes
 
     @property
     def device(self):
@@ -200,14 +201,19 @@ def lut_gemm(x: torch.Tensor, layer: PackedLayer, out: torch.Tensor | None = Non
         out = torch.empty((M, layer.N), dtype=torch.float16, device=dev)
     if out.dtype != torch.float16 or out.dim() != 2 or out.shape[0] != M or out.stride(-1) != 1:
         raise ValueError("out must be fp16 [M][>=N] with unit column stride")
-    need = workspace_bytes(layer, M)
+    need = layer._ws_bytes.get(M)
+    if need is None:
+        need = layer._ws_bytes[M] = workspace_bytes(layer, M)
     ws = (workspace or _workspace_for(dev)).get(need)
-    with torch.cuda.device(dev):
-        st = lib().shiftadd_lut_gemm(_ptr(x2), x2.stride(0), _ptr(layer.planes), _ptr(layer.exps), layer.layout,
-                                     M, layer.N, layer.K, layer.q, layer.g, _ptr(out), out.stride(0),
-                                     _ptr(ws), ws.numel() if ws is not None else 0,
-                                     FLAG_PDL if pdl else 0, _stream_ptr(stream, dev))
-    _check(st, "shiftadd_lut_gemm")
+    if torch.cuda.current_device() != dev.index:
+        torch.cuda.set_device(dev)
+    sptr = (stream if stream is not None else torch.cuda.current_stream(dev)).cuda_stream
+    st = lib().shiftadd_lut_gemm(x2.data_ptr(), x2.stride(0), layer.planes.data_ptr(), layer.exps.data_ptr(),
+                                 layer.layout, M, layer.N, layer.K, layer.q, layer.g, out.data_ptr(),
+                                 out.stride(0), ws.data_ptr() if ws is not None else None,
+                                 ws.numel() if ws is not None else 0, FLAG_PDL if pdl else 0, sptr)
+    if st:
+        _check(st, "shiftadd_lut_gemm")
     return out[0] if squeeze else out
 
 

@@ -25,12 +25,31 @@ constexpr size_t kCounterBytes = (size_t)kCounterSlots * sizeof(int);
 // cols 0..31 hold the 32 groups of an even slice segment, cols 32..63 of an odd one, so a
 // CTA can build the next slice's LUT without waiting for the current one to drain.
 constexpr int kLutBytes = 256 * 256;
-// The LUT is pinned at shared-window address 64 KB (kLutBase): the byte address of entry
-// (key, col) is then 0x10000 | key << 8 | col*4, which one PRMT assembles from the key byte
-// and a per-lane constant -- no base-address add per lookup.  The kernels request enough
-// dynamic shared memory to cover [kLutBase, kLutBase + LUT size) and trap if the runtime
-// placed their dynamic region above kLutBase.
-constexpr uint32_t kLutBase = 0x10000u;
+}  // namespace shiftadd
+
+// Dynamic shared memory as a named PTX symbol.  The kernels that use it declare no static
+// shared memory, so their dynamic region starts right after the 1 KB the driver reserves at
+// the bottom of every CTA's shared window: kDynBase.  Using that constant as the LUT base
+// lets ptxas fold it into the LDS immediate -- LDS [R + 0x400] -- instead of spending an
+// IADD per lookup on a base register; the kernels check the assumption once (trap if not).
+extern "C" __shared__ __align__(16) unsigned char shiftadd_dyn_smem[];
+
+namespace shiftadd {
+
+constexpr uint32_t kDynBase = 0x400u;
+
+__device__ __forceinline__ uint32_t dyn_smem_base() {
+  asm volatile("" ::"l"(shiftadd_dyn_smem));  // reference the symbol so it is declared
+  uint32_t b;
+  asm("mov.u32 %0, shiftadd_dyn_smem;" : "=r"(b));
+  // Bits 24+ of a shared::cta address carry the CTA's rank in its cluster; the kernels are
+  // launched without clusters (rank 0), so the base is the constant window offset.
+  return b & 0x00ffffffu;
+}
+
+__device__ __forceinline__ void check_dyn_base() {
+  if (dyn_smem_base() != kDynBase) __trap();
+}
 
 __device__ __forceinline__ float lds_f32(uint32_t addr) {
   float v;
@@ -48,10 +67,6 @@ __device__ __forceinline__ void sts_f32(uint32_t addr, float v) {
 __device__ __forceinline__ void sts_f32x4(uint32_t addr, float4 v) {
   asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                : "memory");
-}
-// Guard for the fixed LUT placement (see kLutBase).
-__device__ __forceinline__ void check_lut_window(const void* dyn_smem) {
-  if ((uint32_t)__cvta_generic_to_shared(dyn_smem) > kLutBase) __trap();
 }
 
 // a4 -- the "shift" (App. H :974; DenseShift): p * 2^e as an integer add

@@ -7,9 +7,9 @@
 // for each chunk, which it just read, so chunks after the first stream from L2.
 //
 // LUT slab for one 256-k slice and one row chunk: 2 regions (h = chunk half of the tile) x
-// 256 keys x 16 columns x 16 B = 128 KB.  Entry (key, group t) lives at
+// 256 keys x 16 columns x 16 B = 128 KB.  Entry (key, group t) lives at byte offset
 //     (t >> 4) * 64 KB + key * 256 + ((t & 15) ^ (4 * (t >> 4))) * 16
-// -- one PRMT builds it from the key byte.  The XOR swizzle makes the 8 lanes of every
+// -- one PRMT builds it from the key byte; the LDS adds the (uniform) region base.  The XOR swizzle makes the 8 lanes of every
 // LDS.128 phase (rows r..r+3, halves 0/1) hit 8 distinct 16-B bank quads: conflict free.
 // With M rows the smem traffic per weight byte is 4*M bytes, so for M >= 2 the shared-
 // memory bandwidth (128 B/clk/SM), not HBM, is the roof.
@@ -22,11 +22,11 @@ namespace {
 
 constexpr int kMC = 4;                       // batch rows per LUT entry
 constexpr int kLutMbBytes = 2 * 256 * 256;   // 128 KB
-constexpr int kDynSmemMb = (int)kLutBase + kLutMbBytes;  // covers [64 KB, 192 KB)
+constexpr int kDynSmemMb = kLutMbBytes + 16 + 16 * 32 * 4;  // LUT + finalize list
 
 template <int NW>
 __device__ __forceinline__ void build_lut4(const __half* __restrict__ x, int ldx, int m0, int M, int s,
-                                           int warp, int lane) {
+                                           uint32_t lut, int warp, int lane) {
   // thread (warp w, lane t): group t of the slice, every hi nibble assigned to the warp.
   float L[kMC][16];
   float X4[kMC][4];  // x4..x7 of each row, for the hi-nibble half sums
@@ -54,7 +54,7 @@ __device__ __forceinline__ void build_lut4(const __half* __restrict__ x, int ldx
     for (int b = 0; b < 4; ++b) X4[mm][b] = xv[4 + b];
   }
   const int t = lane;
-  const uint32_t col = kLutBase + (t >> 4) * 65536 + (((t & 15) ^ (4 * (t >> 4))) << 4);
+  const uint32_t col = lut + (t >> 4) * 65536 + (((t & 15) ^ (4 * (t >> 4))) << 4);
 #pragma unroll
   for (int hh = 0; hh < 16 / NW; ++hh) {
     const int hi = warp + NW * hh;
@@ -76,8 +76,8 @@ __device__ __forceinline__ void build_lut4(const __half* __restrict__ x, int ldx
 }
 
 template <int Q>
-__device__ __forceinline__ void unit_dot4(const uint4 (&w)[Q], const int (&e)[Q], const uint32_t (&cst)[16],
-                                          float (&acc)[kMC]) {
+__device__ __forceinline__ void unit_dot4(const uint4 (&w)[Q], const int (&e)[Q], uint32_t lut,
+                                          const uint32_t (&cst)[16], float (&acc)[kMC]) {
 #pragma unroll
   for (int mm = 0; mm < kMC; ++mm) acc[mm] = 0.f;
 #pragma unroll
@@ -86,9 +86,9 @@ __device__ __forceinline__ void unit_dot4(const uint4 (&w)[Q], const int (&e)[Q]
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       const uint32_t word = (j < 4) ? w[i].x : (j < 8) ? w[i].y : (j < 12) ? w[i].z : w[i].w;
-      // byte0 <- swizzled col*16, byte1 <- key, byte2 <- 1 + region h, byte3 <- 0
-      const uint32_t addr = __byte_perm(word, cst[j], 0x7604u | ((uint32_t)(j & 3) << 4));
-      const float4 v = lds_f32x4(addr);
+      // byte0 <- swizzled col*16, byte1 <- key, byte2 <- region h, byte3 <- 0
+      const uint32_t off = __byte_perm(word, cst[j], 0x7604u | ((uint32_t)(j & 3) << 4));
+      const float4 v = lds_f32x4(lut + off);
       if (j & 1) { p1.x += v.x; p1.y += v.y; p1.z += v.z; p1.w += v.w; }
       else { p0.x += v.x; p0.y += v.y; p0.z += v.z; p0.w += v.w; }
     }
@@ -105,10 +105,11 @@ gemm_tiled_mb_kernel(const __half* __restrict__ x, int ldx, const uint4* __restr
                      const int8_t* __restrict__ exps, int M, int N, int S, int RG, long long U,
                      __half* __restrict__ y, int ldy, float* __restrict__ partial, int* __restrict__ counters,
                      int pdl) {
-  extern __shared__ __align__(16) unsigned char dyn_smem[];
-  __shared__ int fin_list[NW * 32];
-  __shared__ int fin_count;
-  check_lut_window(dyn_smem);
+  // dynamic smem: [LUT][fin_count][fin_list[NW*32]]; no static shared memory (kDynBase)
+  int& fin_count = *reinterpret_cast<int*>(shiftadd_dyn_smem + kLutMbBytes);
+  int* fin_list = reinterpret_cast<int*>(shiftadd_dyn_smem + kLutMbBytes + 16);
+  if (threadIdx.x == 0) check_dyn_base();
+  const uint32_t lut = kDynBase;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int r = lane >> 1, h = lane & 1;
   const long long G = gridDim.x;
@@ -119,7 +120,7 @@ gemm_tiled_mb_kernel(const __half* __restrict__ x, int ldx, const uint4* __restr
   uint32_t cst[16];
 #pragma unroll
   for (int j = 0; j < 16; ++j)
-    cst[j] = kLutBase + ((uint32_t)((((j + r) & 15) ^ (4 * h)) << 4)) + ((uint32_t)h << 16);
+    cst[j] = ((uint32_t)((((j + r) & 15) ^ (4 * h)) << 4)) | ((uint32_t)h << 16);
 
   uint4 wa[Q], wb[Q];
   int ea[Q], eb[Q];
@@ -136,14 +137,14 @@ gemm_tiled_mb_kernel(const __half* __restrict__ x, int ldx, const uint4* __restr
         waited = true;
       }
       __syncthreads();  // previous LUT fully consumed
-      build_lut4<NW>(x, ldx, m0, M, s, warp, lane);
+      build_lut4<NW>(x, ldx, m0, M, s, lut, warp, lane);
       __syncthreads();
       const long long rg_base = (long long)s * RG;
       for (; uu < seg_end; uu += NW) {
         const long long un = uu + NW;
         if (un < seg_end) load_unit<Q>(planes, exps, un, lane, wb, eb);
         float acc[kMC];
-        unit_dot4<Q>(wa, ea, cst, acc);
+        unit_dot4<Q>(wa, ea, lut, cst, acc);
 #pragma unroll
         for (int mm = 0; mm < kMC; ++mm) acc[mm] += __shfl_xor_sync(0xffffffffu, acc[mm], 1);
         const int n = (int)(uu - rg_base) * kTileRows + r;

@@ -129,7 +129,7 @@ def test_small_batch_parity(sa, M, layout):
 
 @pytest.mark.parametrize("g", [8, 32, 64])
 def test_canonical_small_scale_groups(sa, g):
-    q, N, K = 2, 70, 520
+    q, N, K = 2, 70, 576
     signs, alpha, planes, exps = _layer(q, N, K, g, synth.seed_for(3, g))
     layer = _gpu(sa, signs, alpha, g, sa.LAYOUT_CANONICAL)
     x = synth.gen_x(3, K, seed=synth.seed_for(3, g, 1))

@@ -1,0 +1,61 @@
+"""Device time per LUT-GEMV call (CUDA graph of back-to-back launches over rotating copies
+that exceed L2).  Development tool; bench.py is the contract.
+Usage: python tools/time_gemv.py [--pdl] [--m M] N:K:q [N:K:q ...]"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2406_05981_b200 as sa  # noqa: E402
+import synth  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("shapes", nargs="+")
+ap.add_argument("--pdl", action="store_true")
+ap.add_argument("--m", type=int, default=1)
+ap.add_argument("--reps", type=int, default=200)
+a = ap.parse_args()
+dev = torch.device("cuda:0")
+l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+peak = 6550.7
+for spec in a.shapes:
+    N, K, q = map(int, spec.split(":"))
+    lb = q * N * K // 8 + q * N * K // 128
+    R = max(2, -(-4 * l2 // lb))
+    copies = []
+    for r in range(R):
+        if r < 2:
+            signs, alpha = synth.gen_layer(q, N, K, 128, seed=synth.seed_for(1, 0, r), device=dev)
+            copies.append(sa.pack(signs, alpha, 128, layout=sa.LAYOUT_TILED))
+            del signs, alpha
+        else:
+            base = copies[r % 2]
+            copies.append(sa.PackedLayer(base.planes.clone(), base.exps.clone(), q, N, K, 128, base.layout, base.counts))
+    x = synth.gen_x(a.m, K, seed=1, device=dev)
+    y = torch.empty((a.m, N), dtype=torch.float16, device=dev)
+    ws = sa.Workspace(dev)
+    s = torch.cuda.Stream(dev)
+    with torch.cuda.stream(s):
+        for t in range(3):
+            sa.lut_gemm(x, copies[t % R], out=y, workspace=ws, pdl=a.pdl)
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for t in range(a.reps):
+            sa.lut_gemm(x, copies[t % R], out=y, workspace=ws, pdl=a.pdl)
+    with torch.cuda.stream(s):
+        g.replay()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        g.replay()
+        e1.record(s)
+    s.synchronize()
+    us = e0.elapsed_time(e1) / a.reps * 1e3
+    tot = lb + 2 * a.m * K + 2 * a.m * N
+    print("N=%6d K=%6d q=%d M=%2d  %8.2f us  %7.1f GB/s  frac %.3f  (R=%d, exp=%s)" % (
+        N, K, q, a.m, us, tot / us * 1e-3, tot / us * 1e-3 / peak, R, os.environ.get("SHIFTADD_EXP", "0")), flush=True)
+    del copies, g
+    torch.cuda.empty_cache()
