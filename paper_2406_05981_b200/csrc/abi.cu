@@ -62,7 +62,7 @@ shiftadd_status device_info(DevInfo* out) {
 shiftadd_status check_shape(int q, int N, int K, int g, int max_q) {
   if (q < 1 || q > max_q) return fail(SHIFTADD_ERR_INVALID, "q=%d outside [1, %d]", q, max_q);
   if (N < 1 || K < 8) return fail(SHIFTADD_ERR_INVALID, "need N >= 1 and K >= 8 (N=%d, K=%d)", N, K);
-  if (N > kCounterSlots * kTileRows) return fail(SHIFTADD_ERR_INVALID, "N=%d above %d", N, kCounterSlots * kTileRows);
+  if (N > kMaxRows) return fail(SHIFTADD_ERR_INVALID, "N=%d above %d", N, kMaxRows);
   if (K % 8) return fail(SHIFTADD_ERR_INVALID, "K=%d is not a multiple of 8", K);
   if (g < 8 || g % 8 || K % g) return fail(SHIFTADD_ERR_INVALID, "need 8 | g and g | K (g=%d, K=%d)", g, K);
   return SHIFTADD_OK;

@@ -15,11 +15,11 @@ constexpr int kTileRows = 16;    // output rows per tile
 constexpr int kTileK = 256;      // reduction indices per tile (32 key bytes per row)
 constexpr int kTileBytes = 512;  // 16 rows x 32 key bytes
 constexpr int kTileExps = 32;    // 16 rows x 2 chunk exponents
-// Split-K workspace: a fixed region of per-row-group arrival counters at offset 0 (so a later
-// call of any shape finds its counters zeroed -- the last CTA of each row group resets its
-// counter), then the fp32 partials.  Bounds N at kCounterSlots * 16 rows.
-constexpr int kCounterSlots = 65536;
-constexpr size_t kCounterBytes = (size_t)kCounterSlots * sizeof(int);
+// Split-K workspace: a fixed 256-byte region of grid-barrier words at offset 0 (arrivals,
+// departures; the last CTA out resets them, so a later call of any shape finds them zeroed),
+// then the fp32 partials [M][S][Npad].
+constexpr size_t kCounterBytes = 256;
+constexpr int kMaxRows = 1 << 20;
 
 // LUT slab in shared memory for one 256-k slice: 256 keys x 64 words.  Word (key, col):
 // cols 0..31 hold the 32 groups of an even slice segment, cols 32..63 of an odd one, so a
@@ -49,6 +49,14 @@ __device__ __forceinline__ uint32_t dyn_smem_base() {
 
 __device__ __forceinline__ void check_dyn_base() {
   if (dyn_smem_base() != kDynBase) __trap();
+}
+
+// PTX prmt.b32 (default mode).  Unlike __byte_perm, the selector's per-nibble msb is honoured:
+// it replicates the sign bit of the selected byte over the target byte.
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
 }
 
 __device__ __forceinline__ float lds_f32(uint32_t addr) {
@@ -88,12 +96,44 @@ __device__ __forceinline__ void pdl_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;" :::);
 }
 
-// Streaming 16-byte weight load: read-only path, no L1 allocation (each byte is used once).
-__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// L2 cache policies: streamed weights are read exactly once per call -> evict_first, so
+// they do not push x, the split-K partials or the next layer's activations out of L2.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// Streaming 16-byte weight load: read-only path, no L1 allocation, L2 evict-first.
+__device__ __forceinline__ uint4 ldg_stream(const uint4* p, uint64_t pol) {
   uint4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p));
+               : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int ldg_s8_stream(const int8_t* p, uint64_t pol) {
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s8 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+// 16-byte load of data other CTAs / the next call will re-read (activations): L2 evict-last.
+__device__ __forceinline__ uint4 ldg_keep(const void* p, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(pol));
   return v;
 }
 
@@ -101,11 +141,11 @@ __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
 // its 16 B) and Q x 32 chunk exponents (lane reads its byte).
 template <int Q>
 __device__ __forceinline__ void load_unit(const uint4* __restrict__ planes, const int8_t* __restrict__ exps,
-                                          long long u, int lane, uint4 (&w)[Q], int (&e)[Q]) {
+                                          long long u, int lane, uint64_t pol, uint4 (&w)[Q], int (&e)[Q]) {
 #pragma unroll
-  for (int i = 0; i < Q; ++i) w[i] = ldg_stream(planes + (u * Q + i) * 32 + lane);
+  for (int i = 0; i < Q; ++i) w[i] = ldg_stream(planes + (u * Q + i) * 32 + lane, pol);
 #pragma unroll
-  for (int i = 0; i < Q; ++i) e[i] = __ldg(exps + (u * Q + i) * 32 + lane);
+  for (int i = 0; i < Q; ++i) e[i] = ldg_s8_stream(exps + (u * Q + i) * 32 + lane, pol);
 }
 
 struct GemmArgs {

@@ -22,7 +22,7 @@ namespace {
 
 constexpr int kMC = 4;                       // batch rows per LUT entry
 constexpr int kLutMbBytes = 2 * 256 * 256;   // 128 KB
-constexpr int kDynSmemMb = kLutMbBytes + 16 + 16 * 32 * 4;  // LUT + finalize list
+constexpr int kDynSmemMb = kLutMbBytes;
 
 template <int NW>
 __device__ __forceinline__ void build_lut4(const __half* __restrict__ x, int ldx, int m0, int M, int s,
@@ -103,11 +103,8 @@ template <int Q, int NW>
 __global__ void __launch_bounds__(NW * 32, 1)
 gemm_tiled_mb_kernel(const __half* __restrict__ x, int ldx, const uint4* __restrict__ planes,
                      const int8_t* __restrict__ exps, int M, int N, int S, int RG, long long U,
-                     __half* __restrict__ y, int ldy, float* __restrict__ partial, int* __restrict__ counters,
+                     __half* __restrict__ y, int ldy, float* __restrict__ partial, unsigned* __restrict__ sync,
                      int pdl) {
-  // dynamic smem: [LUT][fin_count][fin_list[NW*32]]; no static shared memory (kDynBase)
-  int& fin_count = *reinterpret_cast<int*>(shiftadd_dyn_smem + kLutMbBytes);
-  int* fin_list = reinterpret_cast<int*>(shiftadd_dyn_smem + kLutMbBytes + 16);
   if (threadIdx.x == 0) check_dyn_base();
   const uint32_t lut = kDynBase;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -122,6 +119,8 @@ gemm_tiled_mb_kernel(const __half* __restrict__ x, int ldx, const uint4* __restr
   for (int j = 0; j < 16; ++j)
     cst[j] = ((uint32_t)((((j + r) & 15) ^ (4 * h)) << 4)) | ((uint32_t)h << 16);
 
+  if (pdl) pdl_launch_dependents();
+  const uint64_t pol = policy_evict_first();
   uint4 wa[Q], wb[Q];
   int ea[Q], eb[Q];
   bool waited = false;
@@ -131,7 +130,7 @@ gemm_tiled_mb_kernel(const __half* __restrict__ x, int ldx, const uint4* __restr
       const int s = (int)(u / RG);
       const long long seg_end = min(u1, (long long)(s + 1) * RG);
       long long uu = u + warp;
-      if (uu < seg_end) load_unit<Q>(planes, exps, uu, lane, wa, ea);
+      if (uu < seg_end) load_unit<Q>(planes, exps, uu, lane, pol, wa, ea);
       if (!waited) {
         if (pdl) pdl_wait();
         waited = true;
@@ -142,7 +141,7 @@ gemm_tiled_mb_kernel(const __half* __restrict__ x, int ldx, const uint4* __restr
       const long long rg_base = (long long)s * RG;
       for (; uu < seg_end; uu += NW) {
         const long long un = uu + NW;
-        if (un < seg_end) load_unit<Q>(planes, exps, un, lane, wb, eb);
+        if (un < seg_end) load_unit<Q>(planes, exps, un, lane, pol, wb, eb);
         float acc[kMC];
         unit_dot4<Q>(wa, ea, lut, cst, acc);
 #pragma unroll
@@ -164,37 +163,39 @@ gemm_tiled_mb_kernel(const __half* __restrict__ x, int ldx, const uint4* __restr
       u = seg_end;
     }
   }
-  if (pdl) pdl_launch_dependents();
   if (S == 1) return;
 
+  // Deterministic split-K reduction balanced over the grid (as in gemv_tiled.cu): grid
+  // barrier, then CTA c sums the S partials of its share of the rows for every batch row.
   __threadfence();
   __syncthreads();
-  for (long long ub = u0; ub < u1; ub += NW * 32) {
-    if (tid == 0) fin_count = 0;
-    __syncthreads();
-    const long long uq = ub + tid;
-    if (uq < u1) {
-      const int rg = (int)(uq % RG);
-      if (atomicAdd(&counters[rg], 1) == S - 1) fin_list[atomicAdd(&fin_count, 1)] = rg;
+  if (tid == 0) {
+    atomicAdd(&sync[0], 1u);
+    while (ld_acquire_gpu(&sync[0]) < (unsigned)G) __nanosleep(32);
+  }
+  __syncthreads();
+  const long long n0 = ((long long)blockIdx.x * (long long)Npad) / G;
+  const long long n1 = ((long long)(blockIdx.x + 1) * (long long)Npad) / G;
+  const long long rows = n1 - n0;
+  for (long long it = tid; it < rows * M; it += NW * 32) {
+    const int m = (int)(it / rows);
+    const long long n = n0 + (it - (long long)m * rows);
+    const float* p = partial + (size_t)m * S * Npad + n;
+    float sum = 0.f;
+    int s = 0;
+    for (; s + 8 <= S; s += 8) {
+      float v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = __ldcg(p + (size_t)(s + k) * Npad);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) sum += v[k];
     }
-    __syncthreads();
-    const int nf = fin_count;
-    if (nf > 0) {
-      __threadfence();
-      for (int f = warp; f < nf; f += NW) {
-        const int rg = fin_list[f];
-        const int rr = lane & 15, part = lane >> 4;
-        const int n = rg * kTileRows + rr;
-        for (int m = 0; m < M; ++m) {
-          float sum = 0.f;
-          for (int s = part; s < S; s += 2) sum += __ldcg(partial + ((size_t)m * S + s) * Npad + n);
-          sum += __shfl_xor_sync(0xffffffffu, sum, 16);
-          if (part == 0 && n < N) y[(size_t)m * ldy + n] = __float2half_rn(sum);
-        }
-        if (lane == 0) counters[rg] = 0;
-      }
-    }
-    __syncthreads();
+    for (; s < S; ++s) sum += __ldcg(p + (size_t)s * Npad);
+    if (n < N) y[(size_t)m * ldy + n] = __float2half_rn(sum);
+  }
+  if (tid == 0 && atomicAdd(&sync[1], 1u) == (unsigned)G - 1) {
+    sync[0] = 0u;
+    sync[1] = 0u;
   }
 }
 
@@ -213,7 +214,7 @@ cudaError_t launch_q(const GemmArgs& a, const LaunchPlan& p) {
   const int RG = (a.N + kTileRows - 1) / kTileRows;
   const long long U = (long long)S * RG;
   const size_t Npad = (size_t)RG * kTileRows;
-  int* counters = S > 1 ? reinterpret_cast<int*>(a.workspace) : nullptr;
+  unsigned* sync = S > 1 ? reinterpret_cast<unsigned*>(a.workspace) : nullptr;
   float* partial = S > 1 ? reinterpret_cast<float*>(reinterpret_cast<char*>(a.workspace) + kCounterBytes) : nullptr;
   (void)Npad;
   const int pdl = (a.flags & SHIFTADD_FLAG_PDL) ? 1 : 0;
@@ -229,7 +230,7 @@ cudaError_t launch_q(const GemmArgs& a, const LaunchPlan& p) {
   cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, gemm_tiled_mb_kernel<Q, kNW>, a.x, a.ldx,
                             reinterpret_cast<const uint4*>(a.planes), a.exps, a.M, a.N, S, RG, U, a.y, a.ldy,
-                            partial, counters, pdl);
+                            partial, sync, pdl);
 }
 
 }  // namespace

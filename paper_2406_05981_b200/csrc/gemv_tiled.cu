@@ -18,15 +18,19 @@
 // a3 query: lane (r = lane/2, h = lane&1) holds the 16 key bytes of row r, chunk h of a
 //    plane tile.  The tiled layout stores them rotated by r, so at unrolled step j every
 //    lane reads its byte j and the 32 lanes look up 32 different LUTs (cols 16h+(j+r)&15):
-//    bank-conflict free for any keys.  One PRMT forms key*256 + col*4, one LDS [R + UR_base],
-//    one FADD per key byte.
+//    bank-conflict free for any keys.  One PRMT forms key*256 + col*4 -- the per-lane column
+//    bytes of 4 steps share one register, and the two zero high bytes come from PRMT's
+//    sign-replicate selector -- then one LDS [R + imm] (LUT base and column half are
+//    compile-time immediates) and one FADD per key byte.
 // a4 shift: the chunk sum (16 lookups, inside one scale group since 128 | g) is scaled by
 //    2^e with an exponent-field integer add.
 // a5 reduce: lanes h=0,1 combine with one shuffle; split-K partials (one fp32 per slice and
-//    row) go to the workspace; the last CTA to finish a row group (per-group arrival
-//    counter) sums its S partials in fixed slice order and stores fp16 (RNE).  The final
-//    sums are spread over all threads of that CTA with independent (unrolled) loads.  The
-//    counters are reset by that CTA, leaving the counter region zeroed for the next call.
+//    row) go to the workspace; after a grid barrier (all CTAs are co-resident) every CTA
+//    sums the S partials of an equal share of the rows in fixed slice order (several threads
+//    per row, one round trip) and stores fp16 (RNE) -- balanced and deterministic; the
+//    barrier words are reset by the last CTA out.
+// PDL: dependents are released at kernel start; the first unit's weights are requested
+//    before griddepcontrol.wait, x after it.
 #include <cstdlib>
 #include <mutex>
 
@@ -35,11 +39,20 @@
 namespace shiftadd {
 namespace {
 
-// a2: build the 32 LUTs of one 256-k slice into column half `hoff` (0 or 128 bytes).
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// a2: build the 32 LUTs of one 256-k slice into column half `hoff` (0 or 128 bytes) from the
+// 8 activations of group `lane` (xv = x[256 s + 8 lane .. +7]).
 template <int NW>
-__device__ __forceinline__ void build_lut(const __half* __restrict__ xs, uint32_t lut, uint32_t hoff,
-                                          int warp, int lane) {
-  const uint4 xv = *reinterpret_cast<const uint4*>(xs + 8 * lane);  // activations 8*lane .. +7
+__device__ __forceinline__ void build_lut(const uint4 xv, uint32_t hoff, int warp, int lane) {
   const float2 f01 = __half22float2(*reinterpret_cast<const __half2*>(&xv.x));
   const float2 f23 = __half22float2(*reinterpret_cast<const __half2*>(&xv.y));
   const float2 f45 = __half22float2(*reinterpret_cast<const __half2*>(&xv.z));
@@ -50,10 +63,11 @@ __device__ __forceinline__ void build_lut(const __half* __restrict__ xs, uint32_
   float L[16];
 #pragma unroll
   for (int lo = 0; lo < 16; ++lo) L[lo] = A[lo & 3] + B[lo >> 2];
-  const uint32_t col = lut + hoff + 4 * lane;
+  const uint32_t col = kDynBase + hoff + 4 * lane;
 #pragma unroll
-  for (int hh = 0; hh < 16 / NW; ++hh) {
+  for (int hh = 0; hh < (16 + NW - 1) / NW; ++hh) {
     const int hi = warp + NW * hh;
+    if (NW > 16 && hi >= 16) break;
     // hi is warp-dependent: select the signs instead of indexing (keeps it in registers)
     const float H = ((hi & 1 ? f45.x : -f45.x) + (hi & 2 ? f45.y : -f45.y)) +
                     ((hi & 4 ? f67.x : -f67.x) + (hi & 8 ? f67.y : -f67.y));
@@ -62,10 +76,17 @@ __device__ __forceinline__ void build_lut(const __half* __restrict__ xs, uint32_
   }
 }
 
-// a3 + a4 for one unit: sum over planes of 2^e * (16 LUT lookups).
-template <int Q, int MODE>
-__device__ __forceinline__ float unit_dot(const uint4 (&w)[Q], const int (&e)[Q], uint32_t lut,
-                                          const uint32_t (&cst)[16]) {
+// PRMT selector for step j: byte0 <- column byte (j&3) of cst[j>>2], byte1 <- key byte (j&3)
+// of the weight word, bytes 2,3 <- sign of the column byte (< 0x80, so 0x00).
+__host__ __device__ constexpr uint32_t step_sel(int j) {
+  return ((8u | (4u + (j & 3))) << 12) | ((8u | (4u + (j & 3))) << 8) | ((uint32_t)(j & 3) << 4) |
+         (4u + (j & 3));
+}
+
+// a3 + a4 for one unit: sum over planes of 2^e * (16 LUT lookups).  LUT byte address of a
+// lookup = kDynBase + HOFF + (key << 8 | col*4); the constant part is the LDS immediate.
+template <int Q, int MODE, uint32_t HOFF>
+__device__ __forceinline__ float unit_dot(const uint4 (&w)[Q], const int (&e)[Q], const uint32_t (&cst)[4]) {
   float acc = 0.f;
 #pragma unroll
   for (int i = 0; i < Q; ++i) {
@@ -73,11 +94,8 @@ __device__ __forceinline__ float unit_dot(const uint4 (&w)[Q], const int (&e)[Q]
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       const uint32_t word = (j < 4) ? w[i].x : (j < 8) ? w[i].y : (j < 12) ? w[i].z : w[i].w;
-      // byte0 <- cst (col*4 + half), byte1 <- key byte (j&3) of word, bytes 2,3 <- 0
-      const uint32_t off = __byte_perm(word, cst[j], 0x7604u | ((uint32_t)(j & 3) << 4));
-      float v;
-      if (MODE == 2) v = __uint_as_float(off);   // experiment: no LUT lookup
-      else v = lds_f32(lut + off);
+      const uint32_t off = prmt(word, cst[j >> 2], step_sel(j));
+      const float v = lds_f32(kDynBase + HOFF + off);
       if (j & 1) p1 += v; else p0 += v;
     }
     acc += shift_pow2(p0 + p1, e[i]);
@@ -93,130 +111,198 @@ __device__ __forceinline__ float unit_xor(const uint4 (&w)[Q], const int (&e)[Q]
   return __uint_as_float(a & 0x3fffffffu);
 }
 
-// MODE: 0 = product; 1 = no split-K finalize; 2 = no LUT lookups; 3 = loads only.
-// Modes 1-3 are internal bottleneck experiments (SHIFTADD_EXP), never the product path.
-template <int Q, int NW, int MODE>
-__global__ void __launch_bounds__(NW * 32, NW == 8 ? 2 : 1)
+struct SegCtx {
+  const uint4* planes;
+  const int8_t* exps;
+  int N, S, Npad;
+  long long rg_base;   // first unit of the slice
+  __half* y;
+  float* partial;
+};
+
+template <int Q, int MODE>
+__device__ __forceinline__ void emit(float acc, const SegCtx& c, int s, long long u, int r, int h) {
+  acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+  const int n = (int)(u - c.rg_base) * kTileRows + r;
+  if (h == 0) {
+    if (c.S == 1) { if (n < c.N) c.y[n] = __float2half_rn(acc); }
+    else c.partial[(size_t)s * c.Npad + n] = acc;
+  }
+}
+
+// Register budget and pipeline depth.  A unit in flight costs Q x (4 + 1) registers; the
+// rest of the loop needs ~36.  D units per warp are kept in flight (a ring of D register
+// buffers), which is what hides the HBM latency at ~1-2 us under load.
+__host__ __device__ constexpr int ring_depth(int Q, int REGS) {
+  return (REGS - 36) / (5 * Q) < 1 ? 1 : ((REGS - 36) / (5 * Q) > 8 ? 8 : (REGS - 36) / (5 * Q));
+}
+
+// Process the units [uu, seg_end) (warp stride NW) of one slice; ring slot k holds unit
+// uu + k*NW on entry (loaded by the caller before the LUT build).
+template <int Q, int NW, int MODE, uint32_t HOFF, int D>
+__device__ __forceinline__ void run_segment(const SegCtx& c, int s, long long uu, long long seg_end,
+                                            int lane, uint64_t pol, uint4 (&w)[D][Q], int (&e)[D][Q]) {
+  const int r = lane >> 1, h = lane & 1;
+  uint32_t cst[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    uint32_t v = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) v |= (4u * (uint32_t)(16 * h + ((4 * k + b + r) & 15))) << (8 * b);
+    cst[k] = v;
+  }
+  for (long long base = uu; base < seg_end; base += (long long)D * NW) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const long long cur = base + (long long)k * NW;
+      if (cur < seg_end) {
+        const float acc = (MODE == 3) ? unit_xor<Q>(w[k], e[k]) : unit_dot<Q, MODE, HOFF>(w[k], e[k], cst);
+        const long long nxt = cur + (long long)D * NW;
+        if (nxt < seg_end) load_unit<Q>(c.planes, c.exps, nxt, lane, pol, w[k], e[k]);
+        emit<Q, MODE>(acc, c, s, cur, r, h);
+      }
+    }
+  }
+}
+
+// MODE: 0 = product; 3 = loads only; 4 = product + per-CTA phase timestamps written after the
+// partials in the workspace.  Modes 3-4 are internal experiments (SHIFTADD_EXP).
+template <int Q, int NW, int REGS, int MODE>
+__global__ void __launch_bounds__(NW * 32) __maxnreg__(REGS)
 gemv_tiled_kernel(const __half* __restrict__ x, const uint4* __restrict__ planes,
                   const int8_t* __restrict__ exps, int N, int S, int RG, long long U,
-                  __half* __restrict__ y, float* __restrict__ partial, int* __restrict__ counters,
+                  __half* __restrict__ y, float* __restrict__ partial, unsigned* __restrict__ sync,
                   int pdl) {
-  // dynamic smem: [LUT][fin_count][fin_list[NW*32]]; no static shared memory (kDynBase)
-  int& fin_count = *reinterpret_cast<int*>(shiftadd_dyn_smem + kLutBytes);
-  int* fin_list = reinterpret_cast<int*>(shiftadd_dyn_smem + kLutBytes + 16);
+  constexpr int D = ring_depth(Q, REGS);
   if (threadIdx.x == 0) check_dyn_base();
-  const uint32_t lut = kDynBase;
+  unsigned long long* trace = (MODE == 4) ? reinterpret_cast<unsigned long long*>(
+      partial + (size_t)S * RG * kTileRows) + (size_t)blockIdx.x * 8 : nullptr;
+  if (MODE == 4 && threadIdx.x == 0) trace[0] = gtimer();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int r = lane >> 1, h = lane & 1;
   const long long G = gridDim.x;
   const long long u0 = ((long long)blockIdx.x * U) / G;
   const long long u1 = ((long long)(blockIdx.x + 1) * U) / G;
   const int Npad = RG * kTileRows;
+  const uint64_t pol_stream = policy_evict_first();
+  const uint64_t pol_keep = policy_evict_last();
+  // All CTAs of this grid are resident once each has passed this point, so the dependent
+  // grid may launch now and start fetching its own weights while this one works.
+  if (pdl) pdl_launch_dependents();
 
-  uint4 wa[Q], wb[Q];
-  int ea[Q], eb[Q];
+  SegCtx c{planes, exps, N, S, Npad, 0, y, partial};
+  uint4 w[D][Q];
+  int e[D][Q];
   long long u = u0;
   int seg = 0;
-  bool waited = false;
   while (u < u1) {
     const int s = (int)(u / RG);
     const long long seg_end = min(u1, (long long)(s + 1) * RG);
-    long long uu = u + warp;
-    if (uu < seg_end) load_unit<Q>(planes, exps, uu, lane, wa, ea);  // weights never depend on
-    if (!waited) {                                                    // the upstream kernel
-      if (pdl) pdl_wait();
-      waited = true;
-    }
-    const uint32_t hoff = (seg & 1) ? 128u : 0u;
-    if (MODE != 3) build_lut<NW>(x + (size_t)s * kTileK, lut, hoff, warp, lane);
-    __syncthreads();
-    uint32_t cst[16];
+    const long long uu = u + warp;
+    uint4 xv;
+    const __half* xs = x + (size_t)s * kTileK + 8 * lane;
+    if (seg == 0 && pdl) {
+      // weights never depend on the upstream kernel; x may (it is its output)
 #pragma unroll
-    for (int j = 0; j < 16; ++j) cst[j] = 4u * (uint32_t)(16 * h + ((j + r) & 15)) + hoff;
-    const long long rg_base = (long long)s * RG;
-    for (; uu < seg_end; uu += 2 * NW) {
-      const long long un = uu + NW;
-      if (un < seg_end) load_unit<Q>(planes, exps, un, lane, wb, eb);
-      {
-        float acc = (MODE == 3) ? unit_xor<Q>(wa, ea) : unit_dot<Q, MODE>(wa, ea, lut, cst);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-        const int n = (int)(uu - rg_base) * kTileRows + r;
-        if (h == 0) {
-          if (S == 1) { if (n < N) y[n] = __float2half_rn(acc); }
-          else partial[(size_t)s * Npad + n] = acc;
-        }
-      }
-      if (un >= seg_end) break;
-      const long long unn = un + NW;
-      if (unn < seg_end) load_unit<Q>(planes, exps, unn, lane, wa, ea);
-      {
-        float acc = (MODE == 3) ? unit_xor<Q>(wb, eb) : unit_dot<Q, MODE>(wb, eb, lut, cst);
-        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-        const int n = (int)(un - rg_base) * kTileRows + r;
-        if (h == 0) {
-          if (S == 1) { if (n < N) y[n] = __float2half_rn(acc); }
-          else partial[(size_t)s * Npad + n] = acc;
-        }
-      }
+      for (int k = 0; k < D; ++k)
+        if (uu + (long long)k * NW < seg_end) load_unit<Q>(planes, exps, uu + (long long)k * NW, lane, pol_stream, w[k], e[k]);
+      pdl_wait();
+      xv = ldg_keep(xs, pol_keep);
+    } else {
+      // x first: the LUT build is on the critical path; the ring fills while it is built
+      xv = ldg_keep(xs, pol_keep);
+#pragma unroll
+      for (int k = 0; k < D; ++k)
+        if (uu + (long long)k * NW < seg_end) load_unit<Q>(planes, exps, uu + (long long)k * NW, lane, pol_stream, w[k], e[k]);
     }
+    if (MODE != 3) build_lut<NW>(xv, (seg & 1) ? 128u : 0u, warp, lane);
+    __syncthreads();
+    if (MODE == 4 && tid == 0 && seg == 0) trace[1] = gtimer();
+    c.rg_base = (long long)s * RG;
+    if (seg & 1) run_segment<Q, NW, MODE, 128u, D>(c, s, uu, seg_end, lane, pol_stream, w, e);
+    else run_segment<Q, NW, MODE, 0u, D>(c, s, uu, seg_end, lane, pol_stream, w, e);
     u = seg_end;
     ++seg;
   }
-  if (pdl) pdl_launch_dependents();
-  if (S == 1 || MODE != 0) return;
+  if (MODE == 4) {
+    __syncthreads();
+    if (tid == 0) trace[2] = gtimer();
+  }
+  if (S == 1 || MODE == 3) return;
 
-  // a5: deterministic split-K reduction by the last-arriving CTA of each row group.
-  __threadfence();
+  // a5: deterministic split-K reduction, balanced over the grid.  Grid barrier (all CTAs are
+  // co-resident: gridDim <= #SMs x CTAs-per-SM the kernel fits); arrival is a release by one
+  // thread after the CTA barrier (cumulative over the CTA's partial stores), departure polls
+  // with acquire loads.  Then CTA c sums the S partials of rows [c*Npad/G, (c+1)*Npad/G) in a
+  // fixed order and stores fp16.  sync[0] counts arrivals, sync[1] departures; the last CTA
+  // to depart resets both to zero.
   __syncthreads();
-  for (long long ub = u0; ub < u1; ub += NW * 32) {
-    if (tid == 0) fin_count = 0;
-    __syncthreads();
-    const long long uq = ub + tid;
-    if (uq < u1) {
-      const int rg = (int)(uq % RG);
-      if (atomicAdd(&counters[rg], 1) == S - 1) fin_list[atomicAdd(&fin_count, 1)] = rg;
+  if (tid == 0) {
+    red_release_add(&sync[0], 1u);
+    while (ld_acquire_gpu(&sync[0]) < (unsigned)G) {
     }
-    __syncthreads();
-    const int nf = fin_count;
-    if (nf > 0) {
-      __threadfence();
-      // (row group, row) items spread over all threads; 16 consecutive threads read the 16
-      // consecutive rows of one group (64 B per slice).  Loads are issued 8 at a time,
-      // independent of each other; the sum order is always s = 0, 1, ..., S-1.
-      for (int item = tid; item < nf * kTileRows; item += NW * 32) {
-        const int rg = fin_list[item >> 4];
-        const int n = rg * kTileRows + (item & 15);
-        const float* p = partial + n;
-        float sum = 0.f;
-        int s = 0;
-        for (; s + 8 <= S; s += 8) {
-          float v[8];
+  }
+  __syncthreads();
+  if (MODE == 4 && tid == 0) trace[3] = gtimer();
+  const int n0 = (int)(((long long)blockIdx.x * Npad) / G);
+  const int n1 = (int)(((long long)(blockIdx.x + 1) * Npad) / G);
+  const int R = n1 - n0;
+  // T threads per row (power of two <= 32, <= S): each sums its strided share of the S
+  // partials (up to 16 loads in flight per thread), then a fixed butterfly combines them.
+  int T = 1;
+  while (T < 32 && 2 * T <= S && (R * 2 * T <= NW * 32 || S > 16 * T)) T *= 2;
+  const int items = R * T;
+  const int items_pad = (items + 31) & ~31;
+  for (int it = tid; it < items_pad; it += NW * 32) {
+    const bool live = it < items;
+    const int n = n0 + it / T;
+    const int part = it & (T - 1);
+    float sum = 0.f;
+    if (live) {
+      const float* p = partial + n;
+      int s = part;
+      for (; s + 15 * T < S; s += 16 * T) {
+        float v[16];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) v[k] = __ldcg(p + (size_t)(s + k) * Npad);
+        for (int k = 0; k < 16; ++k) v[k] = __ldcg(p + (size_t)(s + k * T) * Npad);
 #pragma unroll
-          for (int k = 0; k < 8; ++k) sum += v[k];
-        }
-        for (; s < S; ++s) sum += __ldcg(p + (size_t)s * Npad);
-        if (n < N) y[n] = __float2half_rn(sum);
-        if ((item & 15) == 0) counters[rg] = 0;
+        for (int k = 0; k < 16; ++k) sum += v[k];
       }
+      for (; s < S; s += T) sum += __ldcg(p + (size_t)s * Npad);
     }
+    for (int off = T >> 1; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+    if (live && part == 0 && n < N) y[n] = __float2half_rn(sum);
+  }
+  if (MODE == 4) {
     __syncthreads();
+    if (tid == 0) trace[4] = gtimer();
+  }
+  if (tid == 0 && atomicAdd(&sync[1], 1u) == (unsigned)G - 1) {
+    sync[0] = 0u;
+    sync[1] = 0u;
   }
 }
 
+// Launch configurations (warps per CTA, register cap).  Variant 0 is the product default;
+// the others exist for measurement (SHIFTADD_VARIANT) and are documented in DESIGN.md.
+struct Variant {
+  int nw, regs;
+};
+constexpr Variant kVariants[] = {{16, 128}, {8, 128}, {16, 64}, {24, 80}};
+constexpr int kNumVariants = 4;
+
 struct Cfg {
-  int nw;          // warps per CTA
+  int variant;     // index into kVariants
   int per_sm;      // CTAs per SM
   int mode;        // experiment mode (0 = product)
 };
 
 Cfg config_from_env() {
-  Cfg c{8, 1, 0};
+  Cfg c{0, 1, 0};
   if (const char* e = std::getenv("SHIFTADD_EXP")) c.mode = std::atoi(e);
-  if (const char* e = std::getenv("SHIFTADD_NW")) c.nw = std::atoi(e) == 16 ? 16 : 8;
+  if (const char* e = std::getenv("SHIFTADD_VARIANT")) c.variant = std::atoi(e);
   if (const char* e = std::getenv("SHIFTADD_PER_SM")) c.per_sm = std::atoi(e) < 1 ? 1 : std::atoi(e);
-  if (c.mode < 0 || c.mode > 3) c.mode = 0;
+  if (c.mode != 3 && c.mode != 4) c.mode = 0;
+  if (c.variant < 0 || c.variant >= kNumVariants) c.variant = 0;
   return c;
 }
 
@@ -225,21 +311,21 @@ const Cfg& cfg() {
   return c;
 }
 
-constexpr int kDynSmem = kLutBytes + 16 + 16 * 32 * 4;  // 64 KB LUT + finalize list
+constexpr int kDynSmem = kLutBytes;  // 64 KB LUT
 
-template <int Q, int NW, int MODE>
-cudaError_t launch_qnm(const GemmArgs& a, const LaunchPlan& p) {
+template <int Q, int NW, int REGS, int MODE>
+cudaError_t launch_k(const GemmArgs& a, const LaunchPlan& p) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(gemv_tiled_kernel<Q, NW, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    kDynSmem);
+    attr_err = cudaFuncSetAttribute(gemv_tiled_kernel<Q, NW, REGS, MODE>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
   });
   if (attr_err != cudaSuccess) return attr_err;
   const int S = a.K / kTileK;
   const int RG = (a.N + kTileRows - 1) / kTileRows;
   const long long U = (long long)S * RG;
-  int* counters = S > 1 ? reinterpret_cast<int*>(a.workspace) : nullptr;
+  unsigned* sync = S > 1 ? reinterpret_cast<unsigned*>(a.workspace) : nullptr;
   float* partial = S > 1 ? reinterpret_cast<float*>(reinterpret_cast<char*>(a.workspace) + kCounterBytes) : nullptr;
   const int pdl = (a.flags & SHIFTADD_FLAG_PDL) ? 1 : 0;
 
@@ -253,23 +339,29 @@ cudaError_t launch_qnm(const GemmArgs& a, const LaunchPlan& p) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   c.attrs = attr;
   c.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&c, gemv_tiled_kernel<Q, NW, MODE>, a.x, reinterpret_cast<const uint4*>(a.planes),
-                            a.exps, a.N, S, RG, U, a.y, partial, counters, pdl);
+  return cudaLaunchKernelEx(&c, gemv_tiled_kernel<Q, NW, REGS, MODE>, a.x,
+                            reinterpret_cast<const uint4*>(a.planes), a.exps, a.N, S, RG, U, a.y, partial, sync,
+                            pdl);
 }
 
-template <int Q, int NW>
-cudaError_t launch_qn(const GemmArgs& a, const LaunchPlan& p) {
+template <int Q, int V>
+cudaError_t launch_v(const GemmArgs& a, const LaunchPlan& p) {
+  constexpr int NW = kVariants[V].nw, REGS = kVariants[V].regs;
   switch (cfg().mode) {
-    case 1: return launch_qnm<Q, NW, 1>(a, p);
-    case 2: return launch_qnm<Q, NW, 2>(a, p);
-    case 3: return launch_qnm<Q, NW, 3>(a, p);
-    default: return launch_qnm<Q, NW, 0>(a, p);
+    case 3: return launch_k<Q, NW, REGS, 3>(a, p);
+    case 4: return launch_k<Q, NW, REGS, 4>(a, p);
+    default: return launch_k<Q, NW, REGS, 0>(a, p);
   }
 }
 
 template <int Q>
 cudaError_t launch_q(const GemmArgs& a, const LaunchPlan& p) {
-  return p.threads == 512 ? launch_qn<Q, 16>(a, p) : launch_qn<Q, 8>(a, p);
+  switch (cfg().variant) {
+    case 1: return launch_v<Q, 1>(a, p);
+    case 2: return launch_v<Q, 2>(a, p);
+    case 3: return launch_v<Q, 3>(a, p);
+    default: return launch_v<Q, 0>(a, p);
+  }
 }
 
 }  // namespace
@@ -281,7 +373,7 @@ LaunchPlan plan_gemv_tiled(int N, int K, int q, int sms) {
   const long long U = S * RG;
   const long long want = (long long)sms * cfg().per_sm;
   const long long grid = U < want ? U : want;
-  return LaunchPlan{(int)grid, cfg().nw * 32, kDynSmem, 1};
+  return LaunchPlan{(int)grid, kVariants[cfg().variant].nw * 32, kDynSmem, 1};
 }
 
 size_t workspace_gemv_tiled(int N, int K) {
