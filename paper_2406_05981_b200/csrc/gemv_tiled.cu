@@ -292,15 +292,15 @@ constexpr int kNumVariants = 4;
 
 struct Cfg {
   int variant;     // index into kVariants
-  int per_sm;      // CTAs per SM
+  int per_sm;      // CTAs per SM; 0 = choose by problem size
   int mode;        // experiment mode (0 = product)
 };
 
 Cfg config_from_env() {
-  Cfg c{0, 1, 0};
+  Cfg c{2, 0, 0};
   if (const char* e = std::getenv("SHIFTADD_EXP")) c.mode = std::atoi(e);
   if (const char* e = std::getenv("SHIFTADD_VARIANT")) c.variant = std::atoi(e);
-  if (const char* e = std::getenv("SHIFTADD_PER_SM")) c.per_sm = std::atoi(e) < 1 ? 1 : std::atoi(e);
+  if (const char* e = std::getenv("SHIFTADD_PER_SM")) c.per_sm = std::atoi(e) < 0 ? 0 : std::atoi(e);
   if (c.mode != 3 && c.mode != 4) c.mode = 0;
   if (c.variant < 0 || c.variant >= kNumVariants) c.variant = 0;
   return c;
@@ -371,7 +371,12 @@ LaunchPlan plan_gemv_tiled(int N, int K, int q, int sms) {
   const long long S = K / kTileK;
   const long long RG = (N + kTileRows - 1) / kTileRows;
   const long long U = S * RG;
-  const long long want = (long long)sms * cfg().per_sm;
+  // Default (measured): 16-warp CTAs capped at 64 registers.  Small problems
+  // run one CTA per SM, leaving room for the next call's CTAs under PDL; problems with >= 64
+  // units per SM run two (32 warps per SM keep more loads in flight).
+  int per_sm = cfg().per_sm;
+  if (per_sm == 0) per_sm = (U >= 64LL * sms && kVariants[cfg().variant].nw * 32 * kVariants[cfg().variant].regs <= 32768) ? 2 : 1;
+  const long long want = (long long)sms * per_sm;
   const long long grid = U < want ? U : want;
   return LaunchPlan{(int)grid, kVariants[cfg().variant].nw * 32, kDynSmem, 1};
 }
