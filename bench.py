@@ -284,22 +284,31 @@ def main():
             if group is not None:
                 torch.distributed.all_gather_into_tensor(yfull[li], ys[li], group=group)
 
-    # One CUDA graph per rotating copy: a step is one graph replay (4 GEMV launches, PDL
-    # edges between them), so the host launch rate never limits the device.
-    graphs = []
+    # CUDA graphs: one graph holds a full rotation (R steps = 4R GEMV launches with PDL edges
+    # between consecutive kernels), plus one single-step graph per copy for a remainder, so
+    # neither the host launch rate nor per-graph launch gaps limit the device.
     with torch.cuda.stream(stream):
         for t in range(3):
             step(t)
     stream.synchronize()
+    g_round = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_round, stream=stream):
+        for r in range(R):
+            step(r)
+    singles = []
     for r in range(R):
         gr = torch.cuda.CUDAGraph()
         with torch.cuda.graph(gr, stream=stream):
             step(r)
-        graphs.append(gr)
+        singles.append(gr)
     stream.synchronize()
 
-    def step_graph(t):
-        graphs[t % R].replay()
+    def run_steps(k):
+        """Exactly k steps: k // R full rotations, then k % R single steps."""
+        for _ in range(k // R):
+            g_round.replay()
+        for t in range(k % R):
+            singles[t].replay()
 
     # ---- timed region: barrier + sync, K steps with CUDA events on the launch stream
     def barrier():
@@ -309,16 +318,14 @@ def main():
 
     with ClockSampler(local) as clk:
         with torch.cuda.stream(stream):
-            for t in range(args.warmup):
-                step_graph(t)
+            run_steps(args.warmup)
         barrier()
         m0 = clk.mark()
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(stream):
             ev0.record(stream)
-            for t in range(args.steps):
-                step_graph(t)
+            run_steps(args.steps)
             ev1.record(stream)
         barrier()
         m1 = clk.mark()

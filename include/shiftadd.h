@@ -90,11 +90,12 @@ shiftadd_status shiftadd_pack(const int8_t* signs, const float* alpha, int q, in
                               int32_t* counts, void* stream);
 
 /* Workspace bytes a shiftadd_lut_gemm call with these arguments needs (0 if none).  The
- * caller zeroes a fresh workspace once (cudaMemsetAsync).  Layout: 256 bytes of split-K
- * grid-barrier words at offset 0, then fp32 partials [M][K/256][N padded to 16]; every call
- * leaves the barrier words zeroed again, so one workspace can be reused by calls of any
- * shape without re-clearing.  One workspace must not be used by two calls that can run
- * concurrently.  N <= 1,048,576. */
+ * caller zeroes a fresh workspace once (cudaMemsetAsync).  Layout: 256 KB of split-K
+ * per-row-group arrival counters at offset 0, then fp32 partials [M][K/256][N padded to 16];
+ * every call leaves the counters zeroed again, so one workspace can be reused by calls of
+ * any shape without clearing.  One workspace must not be used by two calls that can run
+ * concurrently.  N <= 1,048,576.  The tiled kernels size their grid to the SM count and need
+ * all their CTAs co-resident; do not co-schedule kernels that pin SMs for the whole call. */
 size_t shiftadd_workspace_bytes(int layout, int M, int N, int K, int q, int g);
 
 /* a2-a7 -- shift-and-add LUT-GEMM, M in [1, 16] (App. D :804-817):

@@ -15,11 +15,12 @@ constexpr int kTileRows = 16;    // output rows per tile
 constexpr int kTileK = 256;      // reduction indices per tile (32 key bytes per row)
 constexpr int kTileBytes = 512;  // 16 rows x 32 key bytes
 constexpr int kTileExps = 32;    // 16 rows x 2 chunk exponents
-// Split-K workspace: a fixed 256-byte region of grid-barrier words at offset 0 (arrivals,
-// departures; the last CTA out resets them, so a later call of any shape finds them zeroed),
+// Split-K workspace: a 256 KB region of per-row-group arrival counters at offset 0 (every
+// call leaves the counters it used zeroed, so a later call of any shape finds them zero),
 // then the fp32 partials [M][S][Npad].
-constexpr size_t kCounterBytes = 256;
-constexpr int kMaxRows = 1 << 20;
+constexpr int kMaxRowGroups = 65536;
+constexpr size_t kCounterBytes = (size_t)kMaxRowGroups * sizeof(unsigned);
+constexpr int kMaxRows = kMaxRowGroups * kTileRows;
 
 // LUT slab in shared memory for one 256-k slice: 256 keys x 64 words.  Word (key, col):
 // cols 0..31 hold the 32 groups of an even slice segment, cols 32..63 of an odd one, so a
@@ -94,6 +95,15 @@ __device__ __forceinline__ float shift_pow2(float p, int e) {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;" :::);
+}
+
+__device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_gpu(unsigned* p, unsigned v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {

@@ -103,7 +103,7 @@ template <int Q, int NW>
 __global__ void __launch_bounds__(NW * 32, 1)
 gemm_tiled_mb_kernel(const __half* __restrict__ x, int ldx, const uint4* __restrict__ planes,
                      const int8_t* __restrict__ exps, int M, int N, int S, int RG, long long U,
-                     __half* __restrict__ y, int ldy, float* __restrict__ partial, unsigned* __restrict__ sync,
+                     __half* __restrict__ y, int ldy, float* __restrict__ partial, unsigned* __restrict__ cnt,
                      int pdl) {
   if (threadIdx.x == 0) check_dyn_base();
   const uint32_t lut = kDynBase;
@@ -165,38 +165,39 @@ gemm_tiled_mb_kernel(const __half* __restrict__ x, int ldx, const uint4* __restr
   }
   if (S == 1) return;
 
-  // Deterministic split-K reduction balanced over the grid (as in gemv_tiled.cu): grid
-  // barrier, then CTA c sums the S partials of its share of the rows for every batch row.
-  __threadfence();
+  // Deterministic split-K reduction, balanced over the grid, with per-row-group arrival
+  // counters exactly as in gemv_tiled.cu (each counter counts the (slice, rg) units of all
+  // row chunks, so the owner waits for S * ceil(M/4) arrivals).
+  const long long own0 = ((long long)blockIdx.x * RG) / G;
+  const long long own1 = ((long long)(blockIdx.x + 1) * RG) / G;
+  const long long n0 = own0 * kTileRows;
+  const long long rows = (own1 - own0) * kTileRows;
+  const unsigned expect = (unsigned)S * (unsigned)((M + kMC - 1) / kMC);
   __syncthreads();
-  if (tid == 0) {
-    atomicAdd(&sync[0], 1u);
-    while (ld_acquire_gpu(&sync[0]) < (unsigned)G) __nanosleep(32);
-  }
+  if (tid == 0) __threadfence();
   __syncthreads();
-  const long long n0 = ((long long)blockIdx.x * (long long)Npad) / G;
-  const long long n1 = ((long long)(blockIdx.x + 1) * (long long)Npad) / G;
-  const long long rows = n1 - n0;
+  for (int m0 = 0; m0 < M; m0 += kMC)
+    for (long long uq = u0 + tid; uq < u1; uq += NW * 32)
+      asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(cnt + (uq % RG)) : "memory");
+  for (long long rg = own0 + tid; rg < own1; rg += NW * 32)
+    while (ld_acquire_gpu(cnt + rg) < expect) {
+    }
+  __syncthreads();
   for (long long it = tid; it < rows * M; it += NW * 32) {
     const int m = (int)(it / rows);
     const long long n = n0 + (it - (long long)m * rows);
     const float* p = partial + (size_t)m * S * Npad + n;
     float sum = 0.f;
-    int s = 0;
-    for (; s + 8 <= S; s += 8) {
-      float v[8];
+    for (int s = 0; s < S; s += 16) {
+      float v[16];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] = __ldcg(p + (size_t)(s + k) * Npad);
+      for (int k = 0; k < 16; ++k) v[k] = (s + k < S) ? __ldcg(p + (size_t)(s + k) * Npad) : 0.f;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) sum += v[k];
+      for (int k = 0; k < 16; ++k) sum += v[k];
     }
-    for (; s < S; ++s) sum += __ldcg(p + (size_t)s * Npad);
     if (n < N) y[(size_t)m * ldy + n] = __float2half_rn(sum);
   }
-  if (tid == 0 && atomicAdd(&sync[1], 1u) == (unsigned)G - 1) {
-    sync[0] = 0u;
-    sync[1] = 0u;
-  }
+  for (long long rg = own0 + tid; rg < own1; rg += NW * 32) cnt[rg] = 0u;   // for the next call
 }
 
 constexpr int kNW = 16;

@@ -25,10 +25,10 @@
 // a4 shift: the chunk sum (16 lookups, inside one scale group since 128 | g) is scaled by
 //    2^e with an exponent-field integer add.
 // a5 reduce: lanes h=0,1 combine with one shuffle; split-K partials (one fp32 per slice and
-//    row) go to the workspace; after a grid barrier (all CTAs are co-resident) every CTA
-//    sums the S partials of an equal share of the rows in fixed slice order (several threads
-//    per row, one round trip) and stores fp16 (RNE) -- balanced and deterministic; the
-//    barrier words are reset by the last CTA out.
+//    row) go to the workspace; per row group an arrival counter (one fence per CTA, then
+//    relaxed reds) tells the group's owner CTA -- every CTA owns an equal share of the row
+//    groups -- when its S partials are stored; the owner sums them in fixed slice order
+//    (several threads per row, one round trip), stores fp16 (RNE) and zeroes the counter.
 // PDL: dependents are released at kernel start; the first unit's weights are requested
 //    before griddepcontrol.wait, x after it.
 #include <cstdlib>
@@ -43,10 +43,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
-}
-
-__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 // a2: build the 32 LUTs of one 256-k slice into column half `hoff` (0 or 128 bytes) from the
@@ -171,13 +167,13 @@ template <int Q, int NW, int REGS, int MODE>
 __global__ void __launch_bounds__(NW * 32) __maxnreg__(REGS)
 gemv_tiled_kernel(const __half* __restrict__ x, const uint4* __restrict__ planes,
                   const int8_t* __restrict__ exps, int N, int S, int RG, long long U,
-                  __half* __restrict__ y, float* __restrict__ partial, unsigned* __restrict__ sync,
-                  int pdl) {
+                  __half* __restrict__ y, float* __restrict__ partial, unsigned* __restrict__ cnt,
+                  int pdl, int pre_wait, int pre_build) {
   constexpr int D = ring_depth(Q, REGS);
   if (threadIdx.x == 0) check_dyn_base();
-  unsigned long long* trace = (MODE == 4) ? reinterpret_cast<unsigned long long*>(
-      partial + (size_t)S * RG * kTileRows) + (size_t)blockIdx.x * 8 : nullptr;
-  if (MODE == 4 && threadIdx.x == 0) trace[0] = gtimer();
+  unsigned long long* trace = (MODE >= 4) ? reinterpret_cast<unsigned long long*>(
+      partial + (size_t)S * RG * kTileRows) + (size_t)blockIdx.x * 16 : nullptr;
+  if (MODE >= 4 && threadIdx.x == 0) trace[0] = gtimer();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long G = gridDim.x;
   const long long u0 = ((long long)blockIdx.x * U) / G;
@@ -200,52 +196,77 @@ gemv_tiled_kernel(const __half* __restrict__ x, const uint4* __restrict__ planes
     const long long uu = u + warp;
     uint4 xv;
     const __half* xs = x + (size_t)s * kTileK + 8 * lane;
+    // Ring slots k < early are requested before the LUT build, the rest right after this
+    // warp's share of it: LDG traffic in flight delays the build's shared-memory stores, and
+    // the build is on the critical path.  Weights never depend on the upstream kernel, x may
+    // (it is its output), so under PDL the early slots go out before griddepcontrol.wait.
+    const int early = (seg == 0 && pdl) ? pre_wait : pre_build;
     if (seg == 0 && pdl) {
-      // weights never depend on the upstream kernel; x may (it is its output)
 #pragma unroll
       for (int k = 0; k < D; ++k)
-        if (uu + (long long)k * NW < seg_end) load_unit<Q>(planes, exps, uu + (long long)k * NW, lane, pol_stream, w[k], e[k]);
+        if (k < early && uu + (long long)k * NW < seg_end)
+          load_unit<Q>(planes, exps, uu + (long long)k * NW, lane, pol_stream, w[k], e[k]);
       pdl_wait();
       xv = ldg_keep(xs, pol_keep);
     } else {
-      // x first: the LUT build is on the critical path; the ring fills while it is built
       xv = ldg_keep(xs, pol_keep);
 #pragma unroll
       for (int k = 0; k < D; ++k)
-        if (uu + (long long)k * NW < seg_end) load_unit<Q>(planes, exps, uu + (long long)k * NW, lane, pol_stream, w[k], e[k]);
+        if (k < early && uu + (long long)k * NW < seg_end)
+          load_unit<Q>(planes, exps, uu + (long long)k * NW, lane, pol_stream, w[k], e[k]);
     }
+    if (MODE >= 4 && tid == 0 && seg == 0) trace[8] = gtimer() + (xv.x & 0u);   // x arrived
     if (MODE != 3) build_lut<NW>(xv, (seg & 1) ? 128u : 0u, warp, lane);
+    if (MODE >= 4 && tid == 0 && seg == 0) trace[9] = gtimer();                 // own part built
+#pragma unroll
+    for (int k = 0; k < D; ++k)
+      if (k >= early && uu + (long long)k * NW < seg_end)
+        load_unit<Q>(planes, exps, uu + (long long)k * NW, lane, pol_stream, w[k], e[k]);
     __syncthreads();
-    if (MODE == 4 && tid == 0 && seg == 0) trace[1] = gtimer();
+    if (MODE >= 4 && tid == 0 && seg == 0) trace[1] = gtimer();
     c.rg_base = (long long)s * RG;
     if (seg & 1) run_segment<Q, NW, MODE, 128u, D>(c, s, uu, seg_end, lane, pol_stream, w, e);
     else run_segment<Q, NW, MODE, 0u, D>(c, s, uu, seg_end, lane, pol_stream, w, e);
     u = seg_end;
     ++seg;
   }
-  if (MODE == 4) {
+  if (MODE >= 4) {
     __syncthreads();
-    if (tid == 0) trace[2] = gtimer();
+    if (tid == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      trace[2] = gtimer();
+      trace[5] = smid;
+      trace[6] = (unsigned long long)seg;
+      trace[7] = (unsigned long long)u0;
+    }
   }
   if (S == 1 || MODE == 3) return;
 
-  // a5: deterministic split-K reduction, balanced over the grid.  Grid barrier (all CTAs are
-  // co-resident: gridDim <= #SMs x CTAs-per-SM the kernel fits); arrival is a release by one
-  // thread after the CTA barrier (cumulative over the CTA's partial stores), departure polls
-  // with acquire loads.  Then CTA c sums the S partials of rows [c*Npad/G, (c+1)*Npad/G) in a
-  // fixed order and stores fp16.  sync[0] counts arrivals, sync[1] departures; the last CTA
-  // to depart resets both to zero.
+  // a5: deterministic split-K reduction, balanced over the grid.  CTA c owns the final sums
+  // of row groups [c*RG/G, (c+1)*RG/G) (whole groups, so every counter has one owner).  Per
+  // row group an arrival counter cnt[rg] counts the (slice, rg) units whose partials are
+  // stored: each CTA fences once after its main loop (cumulative over its threads' stores,
+  // after bar.sync) and then adds 1 per unit with a relaxed red -- no grid-wide barrier, no
+  // single hot address.  An owner waits (one acquire poller per row group) only for its own
+  // counters, sums the S partials of each row in a fixed order, stores fp16 and zeroes the
+  // counters.  All CTAs are co-resident (gridDim <= #SMs x CTAs-per-SM the kernel fits), so
+  // the wait always completes.  (Measured alternatives: a red/acquire grid
+  // barrier, and polling self-validating partial words, were both slower on B200.)
+  const int own0 = (int)(((long long)blockIdx.x * RG) / G);
+  const int own1 = (int)(((long long)(blockIdx.x + 1) * RG) / G);
+  const int n0 = own0 * kTileRows;
+  const int R = (own1 - own0) * kTileRows;
   __syncthreads();
-  if (tid == 0) {
-    red_release_add(&sync[0], 1u);
-    while (ld_acquire_gpu(&sync[0]) < (unsigned)G) {
+  if (tid == 0) __threadfence();
+  __syncthreads();
+  for (long long uq = u0 + tid; uq < u1; uq += NW * 32)
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(cnt + (uq % RG)) : "memory");
+  for (int rg = own0 + tid; rg < own1; rg += NW * 32)
+    while (ld_acquire_gpu(cnt + rg) < (unsigned)S) {
     }
-  }
   __syncthreads();
-  if (MODE == 4 && tid == 0) trace[3] = gtimer();
-  const int n0 = (int)(((long long)blockIdx.x * Npad) / G);
-  const int n1 = (int)(((long long)(blockIdx.x + 1) * Npad) / G);
-  const int R = n1 - n0;
+  if (MODE >= 4 && tid == 0) trace[3] = gtimer();
   // T threads per row (power of two <= 32, <= S): each sums its strided share of the S
   // partials (up to 16 loads in flight per thread), then a fixed butterfly combines them.
   int T = 1;
@@ -259,27 +280,23 @@ gemv_tiled_kernel(const __half* __restrict__ x, const uint4* __restrict__ planes
     float sum = 0.f;
     if (live) {
       const float* p = partial + n;
-      int s = part;
-      for (; s + 15 * T < S; s += 16 * T) {
+      for (int s = part; s < S; s += 16 * T) {
         float v[16];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) v[k] = __ldcg(p + (size_t)(s + k * T) * Npad);
+        for (int k = 0; k < 16; ++k)
+          v[k] = (MODE != 5 && s + k * T < S) ? __ldcg(p + (size_t)(s + k * T) * Npad) : 0.f;
 #pragma unroll
         for (int k = 0; k < 16; ++k) sum += v[k];
       }
-      for (; s < S; s += T) sum += __ldcg(p + (size_t)s * Npad);
     }
     for (int off = T >> 1; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
     if (live && part == 0 && n < N) y[n] = __float2half_rn(sum);
   }
-  if (MODE == 4) {
+  if (MODE >= 4) {
     __syncthreads();
     if (tid == 0) trace[4] = gtimer();
   }
-  if (tid == 0 && atomicAdd(&sync[1], 1u) == (unsigned)G - 1) {
-    sync[0] = 0u;
-    sync[1] = 0u;
-  }
+  for (int rg = own0 + tid; rg < own1; rg += NW * 32) cnt[rg] = 0u;   // for the next call
 }
 
 // Launch configurations (warps per CTA, register cap).  Variant 0 is the product default;
@@ -294,14 +311,22 @@ struct Cfg {
   int variant;     // index into kVariants
   int per_sm;      // CTAs per SM; 0 = choose by problem size
   int mode;        // experiment mode (0 = product)
+  int no_align;    // 1 = plain linear split (experiment)
+  int pre_wait;    // ring slots requested before griddepcontrol.wait (PDL)
+  int pre_build;   // ring slots requested before the LUT build (no PDL)
+  int align_min;   // min % of CTA slots a slice-aligned grid must keep
 };
 
 Cfg config_from_env() {
-  Cfg c{2, 0, 0};
+  Cfg c{2, 0, 0, 0, 0, 0, 85};
+  if (const char* e = std::getenv("SHIFTADD_ALIGN_MIN")) c.align_min = std::atoi(e);
+  if (const char* e = std::getenv("SHIFTADD_PREBUILD")) c.pre_build = std::atoi(e);
+  if (const char* e = std::getenv("SHIFTADD_PREWAIT")) c.pre_wait = std::atoi(e);
+  if (const char* e = std::getenv("SHIFTADD_NO_ALIGN")) c.no_align = std::atoi(e) != 0;
   if (const char* e = std::getenv("SHIFTADD_EXP")) c.mode = std::atoi(e);
   if (const char* e = std::getenv("SHIFTADD_VARIANT")) c.variant = std::atoi(e);
   if (const char* e = std::getenv("SHIFTADD_PER_SM")) c.per_sm = std::atoi(e) < 0 ? 0 : std::atoi(e);
-  if (c.mode != 3 && c.mode != 4) c.mode = 0;
+  if (c.mode != 3 && c.mode != 4 && c.mode != 5) c.mode = 0;
   if (c.variant < 0 || c.variant >= kNumVariants) c.variant = 0;
   return c;
 }
@@ -341,7 +366,7 @@ cudaError_t launch_k(const GemmArgs& a, const LaunchPlan& p) {
   c.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&c, gemv_tiled_kernel<Q, NW, REGS, MODE>, a.x,
                             reinterpret_cast<const uint4*>(a.planes), a.exps, a.N, S, RG, U, a.y, partial, sync,
-                            pdl);
+                            pdl, cfg().pre_wait, cfg().pre_build);
 }
 
 template <int Q, int V>
@@ -350,6 +375,7 @@ cudaError_t launch_v(const GemmArgs& a, const LaunchPlan& p) {
   switch (cfg().mode) {
     case 3: return launch_k<Q, NW, REGS, 3>(a, p);
     case 4: return launch_k<Q, NW, REGS, 4>(a, p);
+    case 5: return launch_k<Q, NW, REGS, 5>(a, p);
     default: return launch_k<Q, NW, REGS, 0>(a, p);
   }
 }
@@ -377,7 +403,13 @@ LaunchPlan plan_gemv_tiled(int N, int K, int q, int sms) {
   int per_sm = cfg().per_sm;
   if (per_sm == 0) per_sm = (U >= 64LL * sms && kVariants[cfg().variant].nw * 32 * kVariants[cfg().variant].regs <= 32768) ? 2 : 1;
   const long long want = (long long)sms * per_sm;
-  const long long grid = U < want ? U : want;
+  long long grid = U < want ? U : want;
+  // Slice-aligned split: with gridDim a multiple of S every CTA's chunk lies in one slice
+  // (one LUT build, no mid-chunk barrier).  Taken when it idles <= 15% of the CTA slots.
+  if (grid == want && S > 1 && !cfg().no_align) {
+    const long long k = want / S;
+    if (k >= 1 && S * k * 100 >= want * cfg().align_min) grid = S * k;
+  }
   return LaunchPlan{(int)grid, kVariants[cfg().variant].nw * 32, kDynSmem, 1};
 }
 

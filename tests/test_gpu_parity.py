@@ -256,7 +256,7 @@ def test_deterministic_and_workspace_left_zeroed(sa):
     torch.cuda.synchronize()
     for y in ys[1:]:
         assert torch.equal(y, ys[0])
-    assert int(ws.buf[:256].count_nonzero()) == 0   # the grid-barrier words
+    assert int(ws.buf[:65536 * 4].count_nonzero()) == 0   # the per-row-group counters
 
 
 def test_workspace_reuse_across_shapes(sa):
