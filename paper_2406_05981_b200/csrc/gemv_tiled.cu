@@ -114,15 +114,24 @@ struct SegCtx {
   long long rg_base;   // first unit of the slice
   __half* y;
   float* partial;
+  unsigned* cnt;       // per-row-group arrival counters
+  int unit_release;    // 1: each warp releases its unit's arrival right after storing it
 };
 
 template <int Q, int MODE>
 __device__ __forceinline__ void emit(float acc, const SegCtx& c, int s, long long u, int r, int h) {
   acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-  const int n = (int)(u - c.rg_base) * kTileRows + r;
+  const int rg = (int)(u - c.rg_base);
+  const int n = rg * kTileRows + r;
   if (h == 0) {
     if (c.S == 1) { if (n < c.N) c.y[n] = __float2half_rn(acc); }
     else c.partial[(size_t)s * c.Npad + n] = acc;
+  }
+  if (c.unit_release && c.S > 1 && MODE != 3) {
+    // the warp's 16 stores, then one release-add by lane 0 (cumulative after __syncwarp)
+    __syncwarp();
+    if (r == 0 && h == 0)
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(c.cnt + rg) : "memory");
   }
 }
 
@@ -168,7 +177,7 @@ __global__ void __launch_bounds__(NW * 32) __maxnreg__(REGS)
 gemv_tiled_kernel(const __half* __restrict__ x, const uint4* __restrict__ planes,
                   const int8_t* __restrict__ exps, int N, int S, int RG, long long U,
                   __half* __restrict__ y, float* __restrict__ partial, unsigned* __restrict__ cnt,
-                  int pdl, int pre_wait, int pre_build) {
+                  int pdl, int pre_wait, int pre_build, int unit_release) {
   constexpr int D = ring_depth(Q, REGS);
   if (threadIdx.x == 0) check_dyn_base();
   unsigned long long* trace = (MODE >= 4) ? reinterpret_cast<unsigned long long*>(
@@ -176,8 +185,10 @@ gemv_tiled_kernel(const __half* __restrict__ x, const uint4* __restrict__ planes
   if (MODE >= 4 && threadIdx.x == 0) trace[0] = gtimer();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long G = gridDim.x;
-  const long long u0 = ((long long)blockIdx.x * U) / G;
-  const long long u1 = ((long long)(blockIdx.x + 1) * U) / G;
+  // u0 = floor(c*U/G) in 32-bit arithmetic (c*U = c*(U/G)*G + c*(U%G), c*(U%G) < G*G)
+  const unsigned Uu = (unsigned)U, Gu = (unsigned)G, qq = Uu / Gu, rr = Uu % Gu, cb = blockIdx.x;
+  const long long u0 = (long long)(cb * qq + (cb * rr) / Gu);
+  const long long u1 = (long long)((cb + 1) * qq + ((cb + 1) * rr) / Gu);
   const int Npad = RG * kTileRows;
   const uint64_t pol_stream = policy_evict_first();
   const uint64_t pol_keep = policy_evict_last();
@@ -185,13 +196,13 @@ gemv_tiled_kernel(const __half* __restrict__ x, const uint4* __restrict__ planes
   // grid may launch now and start fetching its own weights while this one works.
   if (pdl) pdl_launch_dependents();
 
-  SegCtx c{planes, exps, N, S, Npad, 0, y, partial};
+  SegCtx c{planes, exps, N, S, Npad, 0, y, partial, cnt, unit_release};
   uint4 w[D][Q];
   int e[D][Q];
   long long u = u0;
   int seg = 0;
   while (u < u1) {
-    const int s = (int)(u / RG);
+    const int s = (int)((unsigned)u / (unsigned)RG);
     const long long seg_end = min(u1, (long long)(s + 1) * RG);
     const long long uu = u + warp;
     uint4 xv;
@@ -257,11 +268,13 @@ gemv_tiled_kernel(const __half* __restrict__ x, const uint4* __restrict__ planes
   const int own1 = (int)(((long long)(blockIdx.x + 1) * RG) / G);
   const int n0 = own0 * kTileRows;
   const int R = (own1 - own0) * kTileRows;
-  __syncthreads();
-  if (tid == 0) __threadfence();
-  __syncthreads();
-  for (long long uq = u0 + tid; uq < u1; uq += NW * 32)
-    asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(cnt + (uq % RG)) : "memory");
+  if (!unit_release) {
+    __syncthreads();
+    if (tid == 0) __threadfence();
+    __syncthreads();
+    for (long long uq = u0 + tid; uq < u1; uq += NW * 32)
+      asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(cnt + ((unsigned)uq % (unsigned)RG)) : "memory");
+  }
   for (int rg = own0 + tid; rg < own1; rg += NW * 32)
     while (ld_acquire_gpu(cnt + rg) < (unsigned)S) {
     }
@@ -315,10 +328,12 @@ struct Cfg {
   int pre_wait;    // ring slots requested before griddepcontrol.wait (PDL)
   int pre_build;   // ring slots requested before the LUT build (no PDL)
   int align_min;   // min % of CTA slots a slice-aligned grid must keep
+  int unit_release;  // split-K arrival: 1 = per unit by each warp, 0 = once per CTA at the end
 };
 
 Cfg config_from_env() {
-  Cfg c{2, 0, 0, 0, 0, 0, 85};
+  Cfg c{2, 0, 0, 0, 0, 0, 85, 0};
+  if (const char* e = std::getenv("SHIFTADD_UNIT_RELEASE")) c.unit_release = std::atoi(e) != 0;
   if (const char* e = std::getenv("SHIFTADD_ALIGN_MIN")) c.align_min = std::atoi(e);
   if (const char* e = std::getenv("SHIFTADD_PREBUILD")) c.pre_build = std::atoi(e);
   if (const char* e = std::getenv("SHIFTADD_PREWAIT")) c.pre_wait = std::atoi(e);
@@ -366,7 +381,7 @@ cudaError_t launch_k(const GemmArgs& a, const LaunchPlan& p) {
   c.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&c, gemv_tiled_kernel<Q, NW, REGS, MODE>, a.x,
                             reinterpret_cast<const uint4*>(a.planes), a.exps, a.N, S, RG, U, a.y, partial, sync,
-                            pdl, cfg().pre_wait, cfg().pre_build);
+                            pdl, cfg().pre_wait, cfg().pre_build, cfg().unit_release);
 }
 
 template <int Q, int V>

@@ -101,17 +101,17 @@ if __name__ == "__main__":
     tag = sys.argv[1]
     os.makedirs(PROF, exist_ok=True)
     launches(sys.argv[2], tag)
-    traffic = {}
+    traffic = []
     for rep in sys.argv[3:]:
         ms = report(rep, tag)
         for m in ms:
             if "dram__bytes_read.sum" in m:
                 t = to_bytes(*m["dram__bytes_read.sum"]) + to_bytes(*m.get("dram__bytes_write.sum", ("0", "byte")))
-                traffic[os.path.basename(rep)] = t
+                traffic.append(t)
     if traffic:
         with open(os.path.join(PROF, "ncu_traffic.json"), "w") as f:
-            json.dump({"round": tag, "per_report_bytes": traffic,
-                       "traffic_bytes_per_launch_avg": sum(traffic.values()) / len(traffic),
-                       "note": "dram__bytes_read.sum + dram__bytes_write.sum of one launch per full capture"}, f,
-                      indent=1)
+            json.dump({"round": tag, "per_launch_bytes": traffic,
+                       "traffic_bytes_per_launch_avg": sum(traffic) / len(traffic),
+                       "note": "dram__bytes_read.sum + dram__bytes_write.sum per launch of the full capture(s); "
+                               "the bench step's 4 layers (attn q2, attn q3, fc1 q2, fc1 q3) in order"}, f, indent=1)
     print("ok", tag, traffic)
