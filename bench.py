@@ -50,6 +50,17 @@ def alg_bytes(M, q, N, K, g=G):
     return q * N * K // 8 + q * N * (K // g) + 2 * M * K + 2 * M * N
 
 
+KERNEL_NAMES = {0: "gemm_generic_kernel", 1: "gemv_tiled_kernel (grid split-K)", 2: "gemm_tiled_mb_kernel",
+                3: "gemv_cluster_kernel (cluster split-K)"}
+
+
+def kernel_names(layers):
+    """The kernel(s) the bench layers launch (shiftadd_gemm_plan kernel ids)."""
+    import paper_2406_05981_b200 as sa
+    ids = sorted({sa.gemm_plan(L, 1)[3] for L in layers})
+    return " + ".join(KERNEL_NAMES[i] for i in ids)
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -376,7 +387,7 @@ def main():
             traffic = json.load(f).get("traffic_bytes_per_launch_avg")
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
-                "kernel": "gemv_tiled_kernel<Q,16>",
+                "kernel": kernel_names(copies[0]),
                 "algorithmic_bytes_per_launch_avg": kern_bytes // len(shard),
                 "how": "per layer: CUDA events around one replay of a graph of %d back-to-back launches "
                        "(rotating copies) on the launch stream; achieved = sum bytes / sum times" % reps}

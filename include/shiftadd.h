@@ -64,6 +64,12 @@ typedef enum { SHIFTADD_LAYOUT_CANONICAL = 0, SHIFTADD_LAYOUT_TILED = 1 } shifta
 #define SHIFTADD_FLAG_PDL 1u /* launch with programmatic dependent launch: the kernel's weight
                                 prefetch may overlap the previous kernel on the stream; x,
                                 y and the workspace are touched only after it completes. */
+#define SHIFTADD_FLAG_SPLITK 2u /* M = 1, tiled layout: always use the grid-wide split-K
+                                   decomposition (one K-slice per CTA, partials in the
+                                   workspace) instead of the cluster kernel chosen for
+                                   K <= 4096 (K-split reduced over distributed shared memory).
+                                   For testing and measurement; results agree within
+                                   rounding order. */
 
 int shiftadd_abi_version(void);
 const char* shiftadd_status_string(int status);
@@ -105,7 +111,7 @@ size_t shiftadd_workspace_bytes(int layout, int M, int N, int K, int q, int g);
  *   y    : fp16 [M][ldy], ldy >= N (a shard may write into a wider buffer)
  *   workspace: shiftadd_workspace_bytes(...) bytes, 16-byte aligned (NULL if 0)
  *   q    : 1..4 bits per weight of THIS layer (mixed-bit dispatch)
- *   flags: 0 or SHIFTADD_FLAG_PDL
+ *   flags: 0 or a combination of SHIFTADD_FLAG_PDL, SHIFTADD_FLAG_SPLITK
  * Accumulation is fp32 in a fixed order per launch shape: results are bit-identical run to
  * run on one device.  Exponents outside [EXP_MIN, EXP_MAX] (other than EXP_ZERO) are
  * undefined behaviour (pack never emits them).  NaN/Inf in x propagate to the outputs
@@ -123,7 +129,8 @@ shiftadd_status shiftadd_lut_gemv(const uint16_t* x, const uint8_t* planes, cons
 
 /* Launch geometry the gemm call would use (for measurement/reporting; host only):
  * out[0] = grid CTAs, out[1] = threads per CTA, out[2] = dynamic smem bytes,
- * out[3] = kernel id (0 generic, 1 tiled M=1, 2 tiled small-batch).  Needs a device. */
+ * out[3] = kernel id (0 generic, 1 tiled M=1 split-K, 2 tiled small-batch, 3 tiled M=1
+ * cluster split-K), for flags = 0.  Needs a device. */
 shiftadd_status shiftadd_gemm_plan(int layout, int M, int N, int K, int q, int g, int out[4]);
 
 #ifdef __cplusplus

@@ -20,7 +20,7 @@ from dataclasses import dataclass, field
 import torch
 
 __all__ = [
-    "LAYOUT_CANONICAL", "LAYOUT_TILED", "FLAG_PDL", "EXP_ZERO", "ShiftAddError", "lib",
+    "LAYOUT_CANONICAL", "LAYOUT_TILED", "FLAG_PDL", "FLAG_SPLITK", "EXP_ZERO", "ShiftAddError", "lib",
     "PackedLayer", "packed_bytes", "pack", "lut_gemm", "lut_gemv", "workspace_bytes",
     "gemm_plan", "Workspace",
 ]
@@ -28,6 +28,7 @@ __all__ = [
 LAYOUT_CANONICAL = 0
 LAYOUT_TILED = 1
 FLAG_PDL = 1
+FLAG_SPLITK = 2
 EXP_ZERO = -128
 _ABI_VERSION = 1
 _LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libshiftadd.so")
@@ -185,8 +186,11 @@ def _workspace_for(device):
 
 
 def lut_gemm(x: torch.Tensor, layer: PackedLayer, out: torch.Tensor | None = None,
-             workspace: Workspace | None = None, pdl: bool = False, stream=None) -> torch.Tensor:
-    """§8 a2-a7: y[M][N] = x[M][K] (.) the packed layer, fp16 in/out (shiftadd_lut_gemm)."""
+             workspace: Workspace | None = None, pdl: bool = False, stream=None,
+             splitk: bool = False) -> torch.Tensor:
+    """§8 a2-a7: y[M][N] = x[M][K] (.) the packed layer, fp16 in/out (shiftadd_lut_gemm).
+
+    splitk forces the split-K decomposition for M = 1 (SHIFTADD_FLAG_SPLITK)."""
     squeeze = x.dim() == 1
     x2 = x.unsqueeze(0) if squeeze else x
     if x2.dtype != torch.float16 or not x2.is_cuda or x2.device != layer.device:
@@ -211,7 +215,8 @@ def lut_gemm(x: torch.Tensor, layer: PackedLayer, out: torch.Tensor | None = Non
     st = lib().shiftadd_lut_gemm(x2.data_ptr(), x2.stride(0), layer.planes.data_ptr(), layer.exps.data_ptr(),
                                  layer.layout, M, layer.N, layer.K, layer.q, layer.g, out.data_ptr(),
                                  out.stride(0), ws.data_ptr() if ws is not None else None,
-                                 ws.numel() if ws is not None else 0, FLAG_PDL if pdl else 0, sptr)
+                                 ws.numel() if ws is not None else 0,
+                                 (FLAG_PDL if pdl else 0) | (FLAG_SPLITK if splitk else 0), sptr)
     if st:
         _check(st, "shiftadd_lut_gemm")
     return out[0] if squeeze else out

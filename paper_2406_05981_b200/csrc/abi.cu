@@ -78,9 +78,9 @@ shiftadd_status check_layout(int layout, int K, int g) {
 
 size_t tiled_rows(int N) { return (size_t)((N + kTileRows - 1) / kTileRows); }
 
-LaunchPlan make_plan(int layout, int M, int N, int K, int q, int g, int sms) {
+LaunchPlan make_plan(int layout, int M, int N, int K, int q, int g, int sms, unsigned flags) {
   if (layout == SHIFTADD_LAYOUT_CANONICAL) return plan_generic(M, N, K, q, g, sms);
-  if (M == 1) return plan_gemv_tiled(N, K, q, sms);
+  if (M == 1) return !(flags & SHIFTADD_FLAG_SPLITK) && cluster_applicable(N, K, q, sms) ? plan_gemv_cluster(N, K, q, sms) : plan_gemv_tiled(N, K, q, sms);
   return plan_gemm_tiled_mb(M, N, K, q, sms);
 }
 
@@ -153,7 +153,7 @@ shiftadd_status shiftadd_gemm_plan(int layout, int M, int N, int K, int q, int g
   if (M < 1 || M > 16) return fail(SHIFTADD_ERR_UNSUPPORTED, "M=%d outside [1, 16]", M);
   DevInfo di;
   if ((st = device_info(&di)) != SHIFTADD_OK) return st;
-  const LaunchPlan p = make_plan(layout, M, N, K, q, g, di.sms);
+  const LaunchPlan p = make_plan(layout, M, N, K, q, g, di.sms, 0u);
   out[0] = p.grid;
   out[1] = p.threads;
   out[2] = p.smem;
@@ -171,7 +171,7 @@ shiftadd_status shiftadd_lut_gemm(const uint16_t* x, int ldx, const uint8_t* pla
   if (M < 1) return fail(SHIFTADD_ERR_INVALID, "M=%d < 1", M);
   if (M > 16) return fail(SHIFTADD_ERR_UNSUPPORTED, "M=%d > 16 (small-batch kernels cover M <= 16)", M);
   if (ldx < K || ldy < N) return fail(SHIFTADD_ERR_INVALID, "ldx=%d < K=%d or ldy=%d < N=%d", ldx, K, ldy, N);
-  if (flags & ~SHIFTADD_FLAG_PDL) return fail(SHIFTADD_ERR_INVALID, "unknown flags 0x%x", flags);
+  if (flags & ~(SHIFTADD_FLAG_PDL | SHIFTADD_FLAG_SPLITK)) return fail(SHIFTADD_ERR_INVALID, "unknown flags 0x%x", flags);
   if (!aligned(x, 16) || (M > 1 && (ldx % 8)) || !aligned(planes, 16) || !aligned(y, 2))
     return fail(SHIFTADD_ERR_INVALID, "misaligned pointer (x rows and planes need 16 B)");
   const size_t need = workspace_for(layout, M, N, K);
@@ -196,9 +196,10 @@ shiftadd_status shiftadd_lut_gemm(const uint16_t* x, int ldx, const uint8_t* pla
   a.workspace_bytes = workspace_bytes;
   a.flags = flags;
   a.stream = reinterpret_cast<cudaStream_t>(stream);
-  const LaunchPlan p = make_plan(layout, M, N, K, q, g, di.sms);
+  const LaunchPlan p = make_plan(layout, M, N, K, q, g, di.sms, flags);
   cudaError_t e;
   if (layout == SHIFTADD_LAYOUT_CANONICAL) e = launch_gemm_generic(a, p);
+  else if (p.kernel == 3) e = launch_gemv_cluster(a, p);
   else if (M == 1) e = launch_gemv_tiled(a, p);
   else e = launch_gemm_tiled_mb(a, p);
   if (e == cudaErrorNotSupported) return fail(SHIFTADD_ERR_UNSUPPORTED, "no kernel for this configuration");

@@ -176,7 +176,7 @@ struct LaunchPlan {
   int grid;
   int threads;
   int smem;
-  int kernel;  // 0 generic, 1 tiled M=1, 2 tiled small batch
+  int kernel;  // 0 generic, 1 tiled M=1 split-K, 2 tiled small batch, 3 tiled M=1 cluster split-K
 };
 
 // Implemented in the kernel translation units.
@@ -190,6 +190,10 @@ cudaError_t launch_gemm_generic(const GemmArgs& a, const LaunchPlan& p);
 LaunchPlan plan_gemv_tiled(int N, int K, int q, int sms);
 size_t workspace_gemv_tiled(int N, int K);
 cudaError_t launch_gemv_tiled(const GemmArgs& a, const LaunchPlan& p);
+
+bool cluster_applicable(int N, int K, int q, int sms);
+LaunchPlan plan_gemv_cluster(int N, int K, int q, int sms);
+cudaError_t launch_gemv_cluster(const GemmArgs& a, const LaunchPlan& p);
 
 LaunchPlan plan_gemm_tiled_mb(int M, int N, int K, int q, int sms);
 size_t workspace_gemm_tiled_mb(int M, int N, int K);

@@ -170,6 +170,58 @@ __device__ __forceinline__ void run_segment(const SegCtx& c, int s, long long uu
   }
 }
 
+// Dynamic variant of run_segment for slice-aligned grids (kc CTAs per slice): the slice's RG
+// units are a queue.  Ring slot k of warp gw = p*NW + w starts on local unit gw + k*kc*NW
+// (static prefix of kc*NW*D units); afterwards each refill takes the next unit from the
+// slice's claim counter.  Every slot's claim is issued one ring cycle before its result is
+// needed (lane 0 holds it; it is broadcast when the slot is refilled), so the atomic's
+// latency hides behind D units of work.  SM-to-SM speed differences then even out inside the
+// slice group.  Returns the number of units this warp processed.
+template <int Q, int NW, int MODE, int D>
+__device__ __forceinline__ int run_dynamic(const SegCtx& c, int s, int RG, int kc, int gw, int lane,
+                                           uint64_t pol, unsigned* claim, uint4 (&w)[D][Q], int (&e)[D][Q]) {
+  const int r = lane >> 1, h = lane & 1;
+  uint32_t cst[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    uint32_t v = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) v |= (4u * (uint32_t)(16 * h + ((4 * k + b + r) & 15))) << (8 * b);
+    cst[k] = v;
+  }
+  const int base_dyn = kc * NW * D;
+  int cur[D];
+  unsigned pend[D];   // lane 0: pending claim for the slot's next refill
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    cur[k] = gw + k * kc * NW;
+    pend[k] = 0u;
+    if (lane == 0 && cur[k] < RG) pend[k] = atomicAdd(claim, 1u);
+  }
+  int done = 0;
+  bool any = true;
+  while (any) {
+    any = false;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      if (cur[k] < RG) {
+        const float acc = (MODE == 3) ? unit_xor<Q>(w[k], e[k]) : unit_dot<Q, MODE, 0u>(w[k], e[k], cst);
+        const int unit = cur[k];
+        const int nxt = base_dyn + (int)__shfl_sync(0xffffffffu, pend[k], 0);
+        cur[k] = nxt;
+        if (nxt < RG) {
+          load_unit<Q>(c.planes, c.exps, c.rg_base + nxt, lane, pol, w[k], e[k]);
+          if (lane == 0) pend[k] = atomicAdd(claim, 1u);
+          any = true;
+        }
+        emit<Q, MODE>(acc, c, s, c.rg_base + unit, r, h);
+        ++done;
+      }
+    }
+  }
+  return done;
+}
+
 // MODE: 0 = product; 3 = loads only; 4 = product + per-CTA phase timestamps written after the
 // partials in the workspace.  Modes 3-4 are internal experiments (SHIFTADD_EXP).
 template <int Q, int NW, int REGS, int MODE>
@@ -177,7 +229,7 @@ __global__ void __launch_bounds__(NW * 32) __maxnreg__(REGS)
 gemv_tiled_kernel(const __half* __restrict__ x, const uint4* __restrict__ planes,
                   const int8_t* __restrict__ exps, int N, int S, int RG, long long U,
                   __half* __restrict__ y, float* __restrict__ partial, unsigned* __restrict__ cnt,
-                  int pdl, int pre_wait, int pre_build, int unit_release) {
+                  int pdl, int pre_wait, int pre_build, int unit_release, int dyn_kc) {
   constexpr int D = ring_depth(Q, REGS);
   if (threadIdx.x == 0) check_dyn_base();
   unsigned long long* trace = (MODE >= 4) ? reinterpret_cast<unsigned long long*>(
@@ -201,6 +253,31 @@ gemv_tiled_kernel(const __half* __restrict__ x, const uint4* __restrict__ planes
   int e[D][Q];
   long long u = u0;
   int seg = 0;
+  // Dynamic mode (slice-aligned grid, dyn_kc CTAs per slice): one segment, units claimed.
+  int* dyn_total = reinterpret_cast<int*>(shiftadd_dyn_smem + kLutBytes);
+  const int dyn_s = dyn_kc > 0 ? (int)(cb / (unsigned)dyn_kc) : 0;
+  if (dyn_kc > 0) {
+    const int gw = (int)(cb % (unsigned)dyn_kc) * NW + warp;
+    if (tid == 0) *dyn_total = 0;
+    c.rg_base = (long long)dyn_s * RG;
+    const __half* xs = x + (size_t)dyn_s * kTileK + 8 * lane;
+    if (pdl) pdl_wait();
+    const uint4 xv = ldg_keep(xs, pol_keep);
+    if (MODE >= 4 && tid == 0) trace[8] = gtimer() + (xv.x & 0u);
+    if (MODE != 3) build_lut<NW>(xv, 0u, warp, lane);
+    if (MODE >= 4 && tid == 0) trace[9] = gtimer();
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const int lu = gw + k * dyn_kc * NW;
+      if (lu < RG) load_unit<Q>(planes, exps, c.rg_base + lu, lane, pol_stream, w[k], e[k]);
+    }
+    __syncthreads();
+    if (MODE >= 4 && tid == 0) trace[1] = gtimer();
+    const int done = run_dynamic<Q, NW, MODE, D>(c, dyn_s, RG, dyn_kc, gw, lane, pol_stream, cnt + dyn_s, w, e);
+    if (lane == 0) atomicAdd(dyn_total, done);
+    u = u1;
+    seg = 1;
+  }
   while (u < u1) {
     const int s = (int)((unsigned)u / (unsigned)RG);
     const long long seg_end = min(u1, (long long)(s + 1) * RG);
@@ -254,6 +331,25 @@ gemv_tiled_kernel(const __half* __restrict__ x, const uint4* __restrict__ planes
   }
   if (S == 1 || MODE == 3) return;
 
+  // Dynamic mode: one arrival per CTA on its slice's done word (units processed + 2^20, so
+  // the word also counts the CTAs that finished claiming); every owner waits until each
+  // slice shows RG units from all dyn_kc CTAs, then finalizes as below.  The last CTA to
+  // depart resets the claim / done / departure words.
+  unsigned* const dyn_done = cnt + 1024;
+  unsigned* const dyn_dep = cnt + 2048;
+  if (dyn_kc > 0) {
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(dyn_done + dyn_s),
+                   "r"((unsigned)*dyn_total + (1u << 20)) : "memory");
+    }
+    const unsigned target = (unsigned)RG + ((unsigned)dyn_kc << 20);
+    for (int t = tid; t < S; t += NW * 32)
+      while (ld_acquire_gpu(dyn_done + t) != target) {
+      }
+    __syncthreads();
+  }
   // a5: deterministic split-K reduction, balanced over the grid.  CTA c owns the final sums
   // of row groups [c*RG/G, (c+1)*RG/G) (whole groups, so every counter has one owner).  Per
   // row group an arrival counter cnt[rg] counts the (slice, rg) units whose partials are
@@ -268,17 +364,19 @@ gemv_tiled_kernel(const __half* __restrict__ x, const uint4* __restrict__ planes
   const int own1 = (int)(((long long)(blockIdx.x + 1) * RG) / G);
   const int n0 = own0 * kTileRows;
   const int R = (own1 - own0) * kTileRows;
-  if (!unit_release) {
-    __syncthreads();
-    if (tid == 0) __threadfence();
-    __syncthreads();
-    for (long long uq = u0 + tid; uq < u1; uq += NW * 32)
-      asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(cnt + ((unsigned)uq % (unsigned)RG)) : "memory");
-  }
-  for (int rg = own0 + tid; rg < own1; rg += NW * 32)
-    while (ld_acquire_gpu(cnt + rg) < (unsigned)S) {
+  if (dyn_kc == 0) {
+    if (!unit_release) {
+      __syncthreads();
+      if (tid == 0) __threadfence();
+      __syncthreads();
+      for (long long uq = u0 + tid; uq < u1; uq += NW * 32)
+        asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(cnt + ((unsigned)uq % (unsigned)RG)) : "memory");
     }
-  __syncthreads();
+    for (int rg = own0 + tid; rg < own1; rg += NW * 32)
+      while (ld_acquire_gpu(cnt + rg) < (unsigned)S) {
+      }
+    __syncthreads();
+  }
   if (MODE >= 4 && tid == 0) trace[3] = gtimer();
   // T threads per row (power of two <= 32, <= S): each sums its strided share of the S
   // partials (up to 16 loads in flight per thread), then a fixed butterfly combines them.
@@ -309,7 +407,18 @@ gemv_tiled_kernel(const __half* __restrict__ x, const uint4* __restrict__ planes
     __syncthreads();
     if (tid == 0) trace[4] = gtimer();
   }
-  for (int rg = own0 + tid; rg < own1; rg += NW * 32) cnt[rg] = 0u;   // for the next call
+  if (dyn_kc == 0) {
+    for (int rg = own0 + tid; rg < own1; rg += NW * 32) cnt[rg] = 0u;   // for the next call
+  } else {
+    __syncthreads();
+    if (tid == 0 && atomicAdd(dyn_dep, 1u) == (unsigned)G - 1) {
+      for (int t = 0; t < S; ++t) {
+        cnt[t] = 0u;
+        dyn_done[t] = 0u;
+      }
+      *dyn_dep = 0u;
+    }
+  }
 }
 
 // Launch configurations (warps per CTA, register cap).  Variant 0 is the product default;
@@ -329,10 +438,12 @@ struct Cfg {
   int pre_build;   // ring slots requested before the LUT build (no PDL)
   int align_min;   // min % of CTA slots a slice-aligned grid must keep
   int unit_release;  // split-K arrival: 1 = per unit by each warp, 0 = once per CTA at the end
+  int dyn;           // 1 = dynamic unit claiming inside slice groups (slice-aligned grids)
 };
 
 Cfg config_from_env() {
-  Cfg c{2, 0, 0, 0, 0, 0, 85, 0};
+  Cfg c{2, 0, 0, 0, 0, 0, 85, 0, 0};
+  if (const char* e = std::getenv("SHIFTADD_DYN")) c.dyn = std::atoi(e) != 0;
   if (const char* e = std::getenv("SHIFTADD_UNIT_RELEASE")) c.unit_release = std::atoi(e) != 0;
   if (const char* e = std::getenv("SHIFTADD_ALIGN_MIN")) c.align_min = std::atoi(e);
   if (const char* e = std::getenv("SHIFTADD_PREBUILD")) c.pre_build = std::atoi(e);
@@ -351,7 +462,7 @@ const Cfg& cfg() {
   return c;
 }
 
-constexpr int kDynSmem = kLutBytes;  // 64 KB LUT
+constexpr int kDynSmem = kLutBytes + 16;  // 64 KB LUT + the dynamic mode's unit count
 
 template <int Q, int NW, int REGS, int MODE>
 cudaError_t launch_k(const GemmArgs& a, const LaunchPlan& p) {
@@ -368,6 +479,7 @@ cudaError_t launch_k(const GemmArgs& a, const LaunchPlan& p) {
   unsigned* sync = S > 1 ? reinterpret_cast<unsigned*>(a.workspace) : nullptr;
   float* partial = S > 1 ? reinterpret_cast<float*>(reinterpret_cast<char*>(a.workspace) + kCounterBytes) : nullptr;
   const int pdl = (a.flags & SHIFTADD_FLAG_PDL) ? 1 : 0;
+  const int dyn_kc = (cfg().dyn && S > 1 && S <= 1024 && p.grid % S == 0 && p.grid / S >= 2) ? p.grid / S : 0;
 
   cudaLaunchConfig_t c = {};
   c.gridDim = dim3(p.grid);
@@ -381,7 +493,7 @@ cudaError_t launch_k(const GemmArgs& a, const LaunchPlan& p) {
   c.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&c, gemv_tiled_kernel<Q, NW, REGS, MODE>, a.x,
                             reinterpret_cast<const uint4*>(a.planes), a.exps, a.N, S, RG, U, a.y, partial, sync,
-                            pdl, cfg().pre_wait, cfg().pre_build, cfg().unit_release);
+                            pdl, cfg().pre_wait, cfg().pre_build, cfg().unit_release, dyn_kc);
 }
 
 template <int Q, int V>

@@ -98,16 +98,21 @@ SHAPES = [
     (4, 256, 256, 256),    # single slice (no split-K), q = 4
     (3, 64, 2048, 2048),   # row-wise scales (g = K)
     (2, 4096, 4096, 128),  # OPT-6.7B / LLaMA-2-7B attention at 2 bits
+    (2, 23700, 512, 128),  # cluster kernel, C = 1, ragged band of ~10 row groups
+    (1, 4000, 3072, 128),  # cluster kernel, C = 3 (12 slices)
+    (1, 12000, 4096, 128), # cluster kernel, C = 4, 23 row groups per band
 ]
+# (layout, force split-K): the tiled M = 1 path has two decompositions
+KERNELS = [(1, False), (1, True), (0, False)]
 
 
 @pytest.mark.parametrize("q,N,K,g", SHAPES)
-@pytest.mark.parametrize("layout", [1, 0])
-def test_gemv_parity(sa, q, N, K, g, layout):
+@pytest.mark.parametrize("layout,splitk", KERNELS)
+def test_gemv_parity(sa, q, N, K, g, layout, splitk):
     signs, alpha, planes, exps = _layer(q, N, K, g, synth.seed_for(1, q, N % 7))
     layer = _gpu(sa, signs, alpha, g, layout)
     x = synth.gen_x(1, K, seed=synth.seed_for(1, 99))
-    y = _run(sa, x, layer)
+    y = _run(sa, x, layer, splitk=splitk)
     y_ref = oracle.gemm(x.numpy(), planes, exps, g)
     assert y.shape == (1, N)
     err = oracle.err_floor(y.float().cpu().numpy(), y_ref)
@@ -156,28 +161,42 @@ def test_mixed_bit_dispatch_interleaved(sa):
 
 
 # ------------------------------------------------------------ full-size config parity
+def test_m1_kernel_choice(sa):
+    """Cluster split-K for K <= 4096 (and K <= 8192 up to 12 MB of planes) with <= 128 row
+    groups per band; grid split-K otherwise."""
+    def kid(N, K, M=1, q=1):
+        signs, alpha = synth.gen_layer(q, N, K, 128, seed=1, device=DEV)
+        return sa.gemm_plan(sa.pack(signs, alpha, 128, layout=sa.LAYOUT_TILED), M)[3]
+    assert kid(4096, 4096) == 3 and kid(16384, 4096) == 3 and kid(256, 256) == 3 and kid(768, 768) == 3
+    assert kid(2048, 8192) == 3 and kid(28672, 8192, q=3) == 1
+    assert kid(4096, 11008) == 1 and kid(80000, 4096) == 1
+    assert kid(4096, 4096, M=2) == 2
+
+
+@pytest.mark.parametrize("splitk", [False, True])
 @pytest.mark.parametrize("name,N,K,q", [("fc1", 16384, 4096, 3), ("attn", 4096, 4096, 3),
                                         ("llama7b_down", 4096, 11008, 2)])
-def test_config_size_parity_full(sa, name, N, K, q):
+def test_config_size_parity_full(sa, name, N, K, q, splitk):
     """Configs 1-2 at full size, in the launch configuration bench.py times (tiled, PDL)."""
     g = 128
     signs, alpha = synth.gen_layer(q, N, K, g, seed=synth.seed_for(1, 7))
     layer = _gpu(sa, signs, alpha, g, sa.LAYOUT_TILED)
     planes, exps, _ = oracle.pack_canonical(signs.numpy(), alpha.numpy(), g)
     x = synth.gen_x(1, K, seed=synth.seed_for(1, 8))
-    y = _run(sa, x, layer, pdl=True)
+    y = _run(sa, x, layer, pdl=True, splitk=splitk)
     err = oracle.err_floor(y.float().cpu().numpy(), oracle.gemm(x.numpy(), planes, exps, g))
     assert err <= TOL, err
 
 
-def test_llama70b_mlp_sampled_rows(sa):
+@pytest.mark.parametrize("splitk", [False, True])
+def test_llama70b_mlp_sampled_rows(sa, splitk):
     """Config 3 shape (28672 x 8192, 3-bit) on the device; the oracle computes a sample of
     rows one by one from the canonical bytes of just those rows."""
     q, N, K, g = 3, 28672, 8192, 128
     signs, alpha = synth.gen_layer(q, N, K, g, seed=synth.seed_for(3, 0), device=DEV)
     layer = sa.pack(signs, alpha, g, layout=sa.LAYOUT_TILED)
     x = synth.gen_x(1, K, seed=synth.seed_for(3, 1))
-    y = _run(sa, x, layer, pdl=True).float().cpu().numpy()
+    y = _run(sa, x, layer, pdl=True, splitk=splitk).float().cpu().numpy()
     rows = np.random.default_rng(3).choice(N, 96, replace=False)
     rows = np.concatenate([rows, [0, 15, 16, N - 1]])
     s_rows = signs[:, rows].cpu().numpy()
@@ -196,13 +215,13 @@ def _exact_layer(sa, layout, q=3, N=80, K=512, g=128, seed=5):
     return _gpu(sa, signs, alpha, g, layout), planes, exps, (q, N, K, g)
 
 
-@pytest.mark.parametrize("layout", [1, 0])
-def test_basis_vector_gives_rounded_column_exactly(sa, layout):
+@pytest.mark.parametrize("layout,splitk", KERNELS)
+def test_basis_vector_gives_rounded_column_exactly(sa, layout, splitk):
     layer, planes, exps, (q, N, K, g) = _exact_layer(sa, layout)
     W = oracle.dequant(planes, exps, g, K)
     for j in (0, 7, 8, 255, 256, 300, K - 1):
         x = synth.gen_special_x("basis", 1, K, j=j)
-        y = _run(sa, x, layer).cpu().numpy()
+        y = _run(sa, x, layer, splitk=splitk).cpu().numpy()
         assert np.array_equal(y[0], oracle.to_fp16(W[:, j]))
 
 
@@ -246,13 +265,14 @@ def test_nan_input_propagates(sa):
     assert torch.isnan(y).all()
 
 
-def test_deterministic_and_workspace_left_zeroed(sa):
+@pytest.mark.parametrize("splitk", [False, True])
+def test_deterministic_and_workspace_left_zeroed(sa, splitk):
     q, N, K, g = 3, 2000, 4096, 128
     signs, alpha = synth.gen_layer(q, N, K, g, seed=synth.seed_for(6, 0))
     layer = _gpu(sa, signs, alpha, g, sa.LAYOUT_TILED)
     ws = sa.Workspace(DEV)
     x = synth.gen_x(1, K, seed=3).to(DEV)
-    ys = [sa.lut_gemm(x, layer, workspace=ws, pdl=bool(i & 1)).clone() for i in range(4)]
+    ys = [sa.lut_gemm(x, layer, workspace=ws, pdl=bool(i & 1), splitk=splitk).clone() for i in range(4)]
     torch.cuda.synchronize()
     for y in ys[1:]:
         assert torch.equal(y, ys[0])

@@ -14,6 +14,7 @@ import synth  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("shapes", nargs="+")
 ap.add_argument("--pdl", action="store_true")
+ap.add_argument("--splitk", action="store_true")
 ap.add_argument("--m", type=int, default=1)
 ap.add_argument("--reps", type=int, default=200)
 a = ap.parse_args()
@@ -39,12 +40,12 @@ for spec in a.shapes:
     s = torch.cuda.Stream(dev)
     with torch.cuda.stream(s):
         for t in range(3):
-            sa.lut_gemm(x, copies[t % R], out=y, workspace=ws, pdl=a.pdl)
+            sa.lut_gemm(x, copies[t % R], out=y, workspace=ws, pdl=a.pdl, splitk=a.splitk)
     s.synchronize()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=s):
         for t in range(a.reps):
-            sa.lut_gemm(x, copies[t % R], out=y, workspace=ws, pdl=a.pdl)
+            sa.lut_gemm(x, copies[t % R], out=y, workspace=ws, pdl=a.pdl, splitk=a.splitk)
     with torch.cuda.stream(s):
         g.replay()
         e0 = torch.cuda.Event(enable_timing=True)
