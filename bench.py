@@ -396,6 +396,7 @@ def main():
     xh = [x.cpu().pin_memory() for x in xs]
     yh = [torch.empty((1, N), dtype=torch.float16).pin_memory() for (_, N, _, _) in LAYERS]
     xd = [torch.empty_like(x) for x in xs]
+    torch.cuda.synchronize(dev)   # xd was allocated on the default stream; used on `stream`
     e2e_steps = max(10, min(args.steps, 500))
 
     def e2e_step(t):

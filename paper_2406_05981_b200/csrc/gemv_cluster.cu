@@ -16,8 +16,10 @@
 //    land in shared memory, part[t][row]; the CTA sums them over t in order.
 //  * The C partial sums meet over distributed shared memory (a5): every CTA pushes its row
 //    sums into the owning rank's receive buffer (rank c owns rows [c*chunk, (c+1)*chunk) of
-//    the band) with DSMEM stores; after one cluster barrier each owner sums ranks 0..C-1 in
-//    that order and stores fp16 (RNE).  Deterministic; no workspace, no global atomics.
+//    the band) with st.async stores that complete transaction bytes on the owner's
+//    mbarrier; each owner waits for exactly its bytes, sums ranks 0..C-1 in that order and
+//    stores fp16 (RNE).  Deterministic; no workspace, no global atomics, no cluster-wide
+//    barrier at the end.
 //  * The grid is (max co-resident clusters) x C, from cudaOccupancyMaxActiveClusters, so it
 //    never needs a second wave.
 // In a cluster a CTA's shared addresses carry its rank in bits 24+ (a rank-0 address used by
@@ -31,15 +33,22 @@
 namespace shiftadd {
 namespace {
 
-constexpr int kNW = 16;                   // warps per CTA (16 hi nibbles of the LUT build)
 constexpr int kMaxSc = 4;                 // resident LUT slots (slices per CTA)
 constexpr int kMaxC = 8;                  // portable cluster size
 constexpr int kMaxRGb = 128;              // row groups per band
-constexpr int kLutRegion = 2 * kLutBytes; // 128 KB: slots 0-3
-constexpr int kXStage = kMaxSc * kTileK * 2;                      // 2 KB
-constexpr int kPart = kMaxSc * kMaxRGb * kTileRows * 4;           // 32 KB
-constexpr int kRecv = (kMaxRGb * kTileRows + kMaxC) * 4;          // 8 KB + 32 B
-constexpr int kDynSmemCl = kLutRegion + kXStage + kPart + kRecv;  // 170 KB
+
+// Shared-memory map of a variant with SCM LUT slots: LUT slabs, staged x, per-item row sums
+// part[t][row], receive buffer recv[rank][row of the owner's chunk].
+template <int SCM>
+struct Smem {
+  static constexpr int lut = SCM <= 2 ? kLutBytes : 2 * kLutBytes;
+  static constexpr int xstage = SCM * kTileK * 2;
+  static constexpr int part = SCM * kMaxRGb * kTileRows * 4;
+  static constexpr int recv = (kMaxRGb * kTileRows + kMaxC) * 4;
+  static constexpr int mbar = 16;   // the owner's receive mbarrier (8-byte aligned)
+  static constexpr int total = lut + xstage + part + recv + mbar;
+};
+static_assert(Smem<2>::total <= 113 * 1024, "two half-SM CTAs must fit one SM");
 
 __device__ __forceinline__ unsigned long long gtimer_ns() {
   unsigned long long t;
@@ -58,7 +67,15 @@ __device__ __forceinline__ uint32_t cluster_rank() {
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
   return r;
 }
-__device__ __forceinline__ void cluster_sync() {
+// Split cluster barrier: arrive early (relaxed; a preceding fence supplies the release),
+// wait (acquire) right before the first DSMEM access.
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_sync_full() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void st_dsmem_f32(uint32_t local_addr, uint32_t rank, float v) {
@@ -66,9 +83,34 @@ __device__ __forceinline__ void st_dsmem_f32(uint32_t local_addr, uint32_t rank,
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_addr), "r"(rank));
   asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(remote), "f"(v) : "memory");
 }
+// Owner-side receive barrier: one arrival (the owner's own expect_tx) + the bytes its peers
+// push with st.async ... complete_tx.
+__device__ __forceinline__ void mbar_init_expect(uint32_t bar, uint32_t tx_bytes) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tx_bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity0(uint32_t bar) {
+  uint32_t done = 0;
+  do {
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(done) : "r"(bar) : "memory");
+  } while (!done);
+}
+// Asynchronous 4-byte store into CTA `rank`'s shared memory that completes 4 transaction
+// bytes on that CTA's mbarrier (both addresses given in this CTA's window, mapped here).
+__device__ __forceinline__ void st_async_f32(uint32_t local_addr, uint32_t local_bar, uint32_t rank, float v) {
+  uint32_t ra, rb;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local_addr), "r"(rank));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(local_bar), "r"(rank));
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(ra),
+               "r"(__float_as_uint(v)), "r"(rb) : "memory");
+}
+
 
 // a2 from staged x: LUT slot at `slot_base` (slab base + 0 / 128 B half) from the 256
 // activations at shared address xaddr; warp = hi nibble, lane = 8-k group (column).
+template <int NW>
 __device__ __forceinline__ void build_lut_slot(uint32_t slot_base, uint32_t xaddr, int warp, int lane) {
   uint4 xv;
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(xv.x), "=r"(xv.y), "=r"(xv.z), "=r"(xv.w)
@@ -79,12 +121,18 @@ __device__ __forceinline__ void build_lut_slot(uint32_t slot_base, uint32_t xadd
   const float2 f67 = __half22float2(*reinterpret_cast<const __half2*>(&xv.w));
   const float A[4] = {-f01.x - f01.y, f01.x - f01.y, f01.y - f01.x, f01.x + f01.y};
   const float B[4] = {-f23.x - f23.y, f23.x - f23.y, f23.y - f23.x, f23.x + f23.y};
-  const int hi = warp;
-  const float H = ((hi & 1 ? f45.x : -f45.x) + (hi & 2 ? f45.y : -f45.y)) +
-                  ((hi & 4 ? f67.x : -f67.x) + (hi & 8 ? f67.y : -f67.y));
+  float L[16];
+#pragma unroll
+  for (int lo = 0; lo < 16; ++lo) L[lo] = A[lo & 3] + B[lo >> 2];
   const uint32_t col = slot_base + 4 * lane;
 #pragma unroll
-  for (int lo = 0; lo < 16; ++lo) sts_f32(col + ((hi * 16 + lo) << 8), (A[lo & 3] + B[lo >> 2]) + H);
+  for (int k = 0; k < 16 / NW; ++k) {   // hi nibbles warp, warp + NW, ...
+    const int hi = warp + k * NW;
+    const float H = ((hi & 1 ? f45.x : -f45.x) + (hi & 2 ? f45.y : -f45.y)) +
+                    ((hi & 4 ? f67.x : -f67.x) + (hi & 8 ? f67.y : -f67.y));
+#pragma unroll
+    for (int lo = 0; lo < 16; ++lo) sts_f32(col + ((hi * 16 + lo) << 8), L[lo] + H);
+  }
 }
 
 // Lookup address of step j: byte 0 = column byte (cst byte j&1), byte 1 = key byte (word
@@ -119,16 +167,17 @@ __host__ __device__ constexpr int cl_ring(int Q, int REGS) {
 // warp walks its items with (t, rgl) cursors (no division per item).
 struct Cursor {
   int t, rgl;
+  template <int NW>
   __device__ __forceinline__ void advance(int RGb) {
-    rgl += kNW;
+    rgl += NW;
     while (rgl >= RGb) { rgl -= RGb; ++t; }
   }
 };
 
-constexpr int kFlagPdl = 1, kFlagXFirst = 2;
+constexpr int kFlagPdl = 1, kFlagXFirst = 2, kFlagBarrierTail = 4;
 
-template <int Q, int SCM, int REGS>
-__global__ void __launch_bounds__(kNW * 32) __maxnreg__(REGS)
+template <int Q, int SCM, int NW, int REGS>
+__global__ void __launch_bounds__(NW * 32) __maxnreg__(REGS)
 gemv_cluster_kernel(const __half* __restrict__ x, const uint4* __restrict__ planes,
                     const int8_t* __restrict__ exps, int N, int S, int RG, int C, __half* __restrict__ y,
                     int flags, unsigned long long* __restrict__ trace) {
@@ -147,15 +196,27 @@ gemv_cluster_kernel(const __half* __restrict__ x, const uint4* __restrict__ plan
   const int s0 = (int)((rank * (unsigned)S) / Cu);
   const int Sc = (int)(((rank + 1) * (unsigned)S) / Cu) - s0;
   const int Mc = Sc * RGb;
-  const int Mw = Mc > warp ? (Mc - warp + kNW - 1) / kNW : 0;
+  const int Mw = Mc > warp ? (Mc - warp + NW - 1) / NW : 0;
   const uint64_t pol_stream = policy_evict_first();
   const uint64_t pol_keep = policy_evict_last();
   if (pdl) pdl_launch_dependents();
 
   const uint32_t base = dyn_smem_base_cluster();   // kDynBase | rank << 24
-  const uint32_t xs = base + kLutRegion;
-  const uint32_t part = xs + kXStage;
+  const uint32_t xs = base + Smem<SCM>::lut;
+  const uint32_t part = xs + Smem<SCM>::xstage;
+  const uint32_t recv = part + Smem<SCM>::part;
+  const uint32_t bar = recv + Smem<SCM>::recv;
+  // a5 set-up: this CTA owns rows [rank*chunk, rank*chunk + cnt) of the band and expects
+  // (C - 1) * cnt fp32 sums from its peers.
+  const int rows = RGb * kTileRows;
+  const int chunk = (rows + C - 1) / C;
+  const int own_lo = (int)rank * chunk;
+  const int cnt = rows - own_lo < chunk ? (rows - own_lo > 0 ? rows - own_lo : 0) : chunk;
+  const bool btail = flags & kFlagBarrierTail;
+  if (tid == 0 && !btail) mbar_init_expect(bar, (uint32_t)((C - 1) * cnt * 4));
+  cluster_arrive_relaxed();
   const bool xthread = tid < Sc * (kTileK / 8);    // one 16-B chunk of x per thread
+  static_assert(NW * 32 >= SCM * (kTileK / 8), "x staging: one chunk per thread");
   const uint4* xsrc = reinterpret_cast<const uint4*>(x + (size_t)s0 * kTileK) + tid;
   Cursor ld{warp / RGb, warp % RGb};
   Cursor pc = ld;
@@ -174,7 +235,7 @@ gemv_cluster_kernel(const __half* __restrict__ x, const uint4* __restrict__ plan
     for (int k = 0; k < D; ++k)
       if (k < Mw) {
         load_unit<Q>(planes, exps, (long long)(s0 + ld.t) * RG + rg0 + ld.rgl, lane, pol_stream, w[k], e[k]);
-        ld.advance(RGb);
+        ld.advance<NW>(RGb);
       }
   };
   // Weights do not depend on the upstream kernel: under PDL they are requested before
@@ -189,7 +250,7 @@ gemv_cluster_kernel(const __half* __restrict__ x, const uint4* __restrict__ plan
 #pragma unroll
   for (int t = 0; t < SCM; ++t)
     if (t < Sc)
-      build_lut_slot(base + (uint32_t)(t >> 1) * kLutBytes + (uint32_t)(t & 1) * 128u, xs + t * (kTileK * 2), warp,
+      build_lut_slot<NW>(base + (uint32_t)(t >> 1) * kLutBytes + (uint32_t)(t & 1) * 128u, xs + t * (kTileK * 2), warp,
                      lane);
   __syncthreads();
   if (tr && threadIdx.x == 0) tr[2] = gtimer_ns();
@@ -221,10 +282,10 @@ gemv_cluster_kernel(const __half* __restrict__ x, const uint4* __restrict__ plan
       }
       v += __shfl_xor_sync(0xffffffffu, v, 1);
       if (h == 0) sts_f32(part + 4u * (uint32_t)((pc.t * RGb + pc.rgl) * kTileRows + r), v);
-      pc.advance(RGb);
+      pc.advance<NW>(RGb);
       if (m + D < Mw) {
         load_unit<Q>(planes, exps, (long long)(s0 + ld.t) * RG + rg0 + ld.rgl, lane, pol_stream, w[k], e[k]);
-        ld.advance(RGb);
+        ld.advance<NW>(RGb);
       }
     }
   }
@@ -232,25 +293,31 @@ gemv_cluster_kernel(const __half* __restrict__ x, const uint4* __restrict__ plan
   if (tr && threadIdx.x == 0) tr[3] = gtimer_ns();
 
   // a5: each CTA sums its slices (t in order) per row and pushes the sum into the owner
-  // rank's receive buffer, recv[rank][row - owner*chunk], with a DSMEM store; one cluster
-  // barrier (release/acquire) publishes them; the owner sums over ranks 0..C-1 in order.
-  const int rows = RGb * kTileRows;
-  const int chunk = (rows + C - 1) / C;
-  const uint32_t recv = part + kPart;
-  for (int i = tid; i < rows; i += kNW * 32) {
+  // rank's receive buffer recv[rank][row - owner*chunk] with st.async, which completes 4
+  // bytes on the owner's mbarrier; the owner waits for exactly its (C-1)*cnt pushed sums --
+  // no cluster-wide barrier at the end, so finished CTAs leave (their slots go to the next
+  // kernel) while others still stream.  The owner then sums ranks 0..C-1 in order.
+  cluster_wait();   // every peer's mbarrier is initialised (arrived at kernel start)
+  for (int i = tid; i < rows; i += NW * 32) {
     float v = 0.f;
     for (int t = 0; t < Sc; ++t) v += lds_f32(part + 4u * (uint32_t)(t * rows + i));
     const int o = i / chunk;
-    st_dsmem_f32(recv + 4u * (uint32_t)(rank * chunk + (i - o * chunk)), (uint32_t)o, v);
+    const uint32_t dst = recv + 4u * (uint32_t)(rank * chunk + (i - o * chunk));
+    if (o == (int)rank) sts_f32(dst, v);
+    else if (btail) st_dsmem_f32(dst, (uint32_t)o, v);
+    else st_async_f32(dst, bar, (uint32_t)o, v);
   }
-  cluster_sync();
+  if (btail) {
+    cluster_sync_full();     // measured alternative: one full cluster barrier
+  } else {
+    __syncthreads();         // the CTA's own sums
+    mbar_wait_parity0(bar);  // the peers' sums
+  }
   if (tr && threadIdx.x == 0) tr[4] = gtimer_ns();
-  const int lo = (int)rank * chunk;
-  const int cnt = rows - lo < chunk ? rows - lo : chunk;
-  for (int j = tid; j < cnt; j += kNW * 32) {
+  for (int j = tid; j < cnt; j += NW * 32) {
     float v = lds_f32(recv + 4u * (uint32_t)j);
     for (int c = 1; c < C; ++c) v += lds_f32(recv + 4u * (uint32_t)(c * chunk + j));
-    const int n = rg0 * kTileRows + lo + j;
+    const int n = rg0 * kTileRows + own_lo + j;
     if (n < N) y[n] = __float2half_rn(v);
   }
   if (tr && threadIdx.x == 0) {
@@ -275,46 +342,49 @@ int cluster_trace() {
   return v;
 }
 
-// Slices per CTA (LUT slots).  Fewer slots mean fewer serial LUT builds per CTA and a larger
-// cluster (more ranks to combine, and clusters of > 4 pack fewer SMs).  Measured on B200
-// (tools/sweep_r1t.sh, 4096x4096): 2 slots win below ~5 MB of planes (4096^2 q=2: 4.93 vs
-// 5.2 us), 4 above; SHIFTADD_CLUSTER_SC overrides.
+// Variants (warps, LUT slots).  HALF: 8 warps x 128 registers and 2 slots (~90 KB of shared
+// memory), so two CTAs share an SM -- when one finishes, a CTA of the next kernel on the
+// stream takes its place and, under PDL, prefetches its weights while this kernel's tail
+// (cluster barrier, reduction) runs.  FULL4: 16 warps, 4 slots (170 KB, one CTA per SM),
+// for K up to 8192 with clusters of <= 8.
+enum Variant { kHalf = 0, kFull2 = 1, kFull4 = 2 };
 struct ClusterShape {
-  int sc;   // max slices per CTA (2 or 4)
+  int variant;
+  int sc;   // max slices per CTA
   int C;    // cluster size
 };
-constexpr double kSmallLayer = 5.0 * (1 << 20);
 
 ClusterShape cluster_shape(int N, int K, int q) {
-  static const int forced = env_int("SHIFTADD_CLUSTER_SC", 0);
+  (void)N; (void)q;
+  static const int forced_sc = env_int("SHIFTADD_CLUSTER_SC", 0);
+  static const int half = env_int("SHIFTADD_CLUSTER_HALF", 1);
   const int S = K / kTileK;
-  int sc = forced > 0 ? (forced > kMaxSc ? kMaxSc : forced)
-                      : (((double)q * N * K / 8 <= kSmallLayer && (S + 1) / 2 <= kMaxC) ? 2 : kMaxSc);
-  return ClusterShape{sc, (S + sc - 1) / sc};
+  const int sc = forced_sc > 0 ? (forced_sc > kMaxSc ? kMaxSc : forced_sc) : ((S + 1) / 2 <= kMaxC ? 2 : kMaxSc);
+  const int variant = sc > 2 ? kFull4 : (half ? kHalf : kFull2);
+  return ClusterShape{variant, sc, (S + sc - 1) / sc};
 }
 
-template <int Q, int SCM, int REGS>
+int variant_threads(int v) { return v == kHalf ? 8 * 32 : 16 * 32; }
+int variant_smem(int v) { return v == kFull4 ? Smem<4>::total : Smem<2>::total; }
+
+template <int Q, int SCM, int NW, int REGS>
 cudaError_t set_attrs() {
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
   std::call_once(once, [] {
-    err = cudaFuncSetAttribute(gemv_cluster_kernel<Q, SCM, REGS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               kDynSmemCl);
+    err = cudaFuncSetAttribute(gemv_cluster_kernel<Q, SCM, NW, REGS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               Smem<SCM>::total);
   });
   return err;
 }
 
-// Max co-resident clusters of size C (cached per C; the kernels share one resource shape).
-int max_clusters(int C) {
-  static int cache[kMaxC + 1] = {0};
-  static std::mutex mu;
-  std::lock_guard<std::mutex> g(mu);
-  if (cache[C]) return cache[C];
-  if (set_attrs<2, 4, 128>() != cudaSuccess) return 0;
+template <int SCM, int NW>
+int occupancy_clusters(int C) {
+  if (set_attrs<2, SCM, NW, 128>() != cudaSuccess) return 0;
   cudaLaunchConfig_t c = {};
   c.gridDim = dim3(C * 64);
-  c.blockDim = dim3(kNW * 32);
-  c.dynamicSmemBytes = kDynSmemCl;
+  c.blockDim = dim3(NW * 32);
+  c.dynamicSmemBytes = Smem<SCM>::total;
   cudaLaunchAttribute attr;
   attr.id = cudaLaunchAttributeClusterDimension;
   attr.val.clusterDim.x = C;
@@ -323,22 +393,38 @@ int max_clusters(int C) {
   c.attrs = &attr;
   c.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, gemv_cluster_kernel<2, 4, 128>, &c) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&n, gemv_cluster_kernel<2, SCM, NW, 128>, &c) != cudaSuccess) {
     cudaGetLastError();
     n = 0;
   }
-  cache[C] = n > 0 ? n : -1;
-  return cache[C];
+  return n;
+}
+
+// Max co-resident clusters of size C for a variant (cached).
+int max_clusters(int variant, int C) {
+  static int cache[3][kMaxC + 1] = {};
+  static std::mutex mu;
+  std::lock_guard<std::mutex> g(mu);
+  int& slot = cache[variant][C];
+  if (slot) return slot;
+  const int n = variant == kHalf ? occupancy_clusters<2, 8>(C)
+                                 : (variant == kFull2 ? occupancy_clusters<2, 16>(C) : occupancy_clusters<4, 16>(C));
+  slot = n > 0 ? n : -1;
+  return slot;
 }
 
 int x_first() {
   static int v = env_int("SHIFTADD_CLUSTER_XFIRST", 0);
   return v;
 }
+int barrier_tail() {
+  static int v = env_int("SHIFTADD_CLUSTER_BTAIL", 0);
+  return v;
+}
 
-template <int Q, int SCM, int REGS>
+template <int Q, int SCM, int NW, int REGS>
 cudaError_t launch_cluster_q(const GemmArgs& a, const LaunchPlan& p, int C) {
-  const cudaError_t ae = set_attrs<Q, SCM, REGS>();
+  const cudaError_t ae = set_attrs<Q, SCM, NW, REGS>();
   if (ae != cudaSuccess) return ae;
   const int S = a.K / kTileK;
   const int RG = (a.N + kTileRows - 1) / kTileRows;
@@ -360,18 +446,18 @@ cudaError_t launch_cluster_q(const GemmArgs& a, const LaunchPlan& p, int C) {
   unsigned long long* trace = nullptr;
   if (cluster_trace() && a.workspace && a.workspace_bytes >= kCounterBytes + (size_t)p.grid * 256)
     trace = reinterpret_cast<unsigned long long*>(static_cast<char*>(a.workspace) + kCounterBytes);
-  const int flags = (pdl ? kFlagPdl : 0) | (x_first() ? kFlagXFirst : 0);
-  return cudaLaunchKernelEx(&c, gemv_cluster_kernel<Q, SCM, REGS>, a.x, reinterpret_cast<const uint4*>(a.planes),
-                            a.exps, a.N, S, RG, C, a.y, flags, trace);
+  const int flags = (pdl ? kFlagPdl : 0) | (x_first() ? kFlagXFirst : 0) | (barrier_tail() ? kFlagBarrierTail : 0);
+  return cudaLaunchKernelEx(&c, gemv_cluster_kernel<Q, SCM, NW, REGS>, a.x,
+                            reinterpret_cast<const uint4*>(a.planes), a.exps, a.N, S, RG, C, a.y, flags, trace);
 }
 
-template <int SCM>
-cudaError_t launch_cluster_sc(const GemmArgs& a, const LaunchPlan& p, int C) {
+template <int SCM, int NW>
+cudaError_t launch_cluster_v(const GemmArgs& a, const LaunchPlan& p, int C) {
   switch (a.q) {
-    case 1: return launch_cluster_q<1, SCM, 128>(a, p, C);
-    case 2: return launch_cluster_q<2, SCM, 128>(a, p, C);
-    case 3: return launch_cluster_q<3, SCM, 128>(a, p, C);
-    case 4: return launch_cluster_q<4, SCM, 128>(a, p, C);
+    case 1: return launch_cluster_q<1, SCM, NW, 128>(a, p, C);
+    case 2: return launch_cluster_q<2, SCM, NW, 128>(a, p, C);
+    case 3: return launch_cluster_q<3, SCM, NW, 128>(a, p, C);
+    case 4: return launch_cluster_q<4, SCM, NW, 128>(a, p, C);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -391,8 +477,8 @@ bool cluster_applicable(int N, int K, int q, int sms) {
   if (S < 1) return false;
   const ClusterShape cs = cluster_shape(N, K, q);
   if (cs.C > kMaxC) return false;
-  if (cs.C > 4 && (double)q * N * K / 8 > kBigC) return false;
-  const int ncl = max_clusters(cs.C);
+  if (cs.variant == kFull4 && cs.C > 4 && (double)q * N * K / 8 > kBigC) return false;
+  const int ncl = max_clusters(cs.variant, cs.C);
   if (ncl <= 0) return false;
   const int RG = (N + kTileRows - 1) / kTileRows;
   const int bands = ncl < RG ? ncl : RG;
@@ -403,14 +489,18 @@ LaunchPlan plan_gemv_cluster(int N, int K, int q, int sms) {
   (void)sms;
   const ClusterShape cs = cluster_shape(N, K, q);
   const int RG = (N + kTileRows - 1) / kTileRows;
-  const int ncl = max_clusters(cs.C);
+  const int ncl = max_clusters(cs.variant, cs.C);
   const int bands = ncl < RG ? ncl : RG;
-  return LaunchPlan{bands * cs.C, kNW * 32, kDynSmemCl, 3};
+  return LaunchPlan{bands * cs.C, variant_threads(cs.variant), variant_smem(cs.variant), 3};
 }
 
 cudaError_t launch_gemv_cluster(const GemmArgs& a, const LaunchPlan& p) {
   const ClusterShape cs = cluster_shape(a.N, a.K, a.q);
-  return cs.sc <= 2 ? launch_cluster_sc<2>(a, p, cs.C) : launch_cluster_sc<4>(a, p, cs.C);
+  switch (cs.variant) {
+    case kHalf: return launch_cluster_v<2, 8>(a, p, cs.C);
+    case kFull2: return launch_cluster_v<2, 16>(a, p, cs.C);
+    default: return launch_cluster_v<4, 16>(a, p, cs.C);
+  }
 }
 
 }  // namespace shiftadd

@@ -41,6 +41,7 @@ def pack_layer(q, N, K, seed, dev):
 
 
 def time_graph(fn, reps=5):
+    torch.cuda.synchronize()   # inputs were made on the default stream; fn runs on s
     s = torch.cuda.Stream()
     with torch.cuda.stream(s):
         fn()

@@ -37,6 +37,10 @@ for spec in a.shapes:
     x = synth.gen_x(a.m, K, seed=1, device=dev)
     y = torch.empty((a.m, N), dtype=torch.float16, device=dev)
     ws = sa.Workspace(dev)
+    # Everything above was enqueued on the default stream: without this sync the caching
+    # allocator may hand y the memory of a just-freed temporary whose kernels have not run,
+    # and the GEMV on stream s would overwrite it.
+    torch.cuda.synchronize(dev)
     s = torch.cuda.Stream(dev)
     with torch.cuda.stream(s):
         for t in range(3):

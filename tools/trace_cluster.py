@@ -37,3 +37,14 @@ le = (tr[:, 3] - t0) / 1000.0
 o = np.argsort(-le)
 print("  slowest loop_end:", ", ".join("cta %d %.2f sm %d Mw %d" % (i, le[i], tr[i, 6], tr[i, 7]) for i in o[:6]))
 print("  Mw values:", sorted(set(tr[:, 7].tolist())))
+sm = tr[:, 6]
+cnt = {}
+for s_ in sm.tolist():
+    cnt[s_] = cnt.get(s_, 0) + 1
+hist = {}
+for v in cnt.values():
+    hist[v] = hist.get(v, 0) + 1
+print("  CTAs per SM histogram:", dict(sorted(hist.items())), " SMs used:", len(cnt))
+for k in sorted(hist):
+    sel = np.array([cnt[s_] == k for s_ in sm.tolist()])
+    print("    SMs with %d CTA(s): loop_end median %.2f us (n=%d)" % (k, np.median(le[sel]), sel.sum()))
