@@ -18,6 +18,11 @@ Parity status per function (see DESIGN.md §"Oracle pins"):
   lut_direct / lut_incremental  pinned (exhaustive 256-key agreement, one-hot / zero cases)
   lut_gemm          pinned  (agrees exactly with gemm on brute-force cases)
   gemm_scalar       pinned  (agrees exactly with gemm on config-1 and tiny shapes)
+  pack_colwise / dequant_colwise / gemm_colwise / lut_gemm_colwise  (NEXT-f1)
+                    pinned  (S9: exact powers of two reproduce sum_i alpha_i s_i; constant
+                    exponents per plane reduce to the pinned row-wise gemm with g = K;
+                    all-ones closed form; x-column scaling == exponent shift of that column
+                    on N != K; LUT route == definition)
 """
 
 from .ref import *  # noqa: F401,F403

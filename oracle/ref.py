@@ -43,7 +43,8 @@ __all__ = [
     "pot_exponent", "pack_canonical", "unpack_signs", "to_tiled", "from_tiled",
     "tiled_sizes", "dequant", "gemm", "gemm_scalar", "lut_direct", "lut_incremental",
     "lut_gemm", "to_fp16", "err_floor", "err_normwise", "packed_bytes",
-    "algorithmic_bytes",
+    "algorithmic_bytes", "tile_planes", "pack_colwise", "dequant_colwise", "gemm_colwise",
+    "lut_gemm_colwise", "algorithmic_bytes_colwise",
 ]
 
 
@@ -313,6 +314,106 @@ def lut_gemm(x, planes, exps, g):
             scale = np.where(ei == EXP_ZERO, 0.0, np.ldexp(1.0, np.where(ei == EXP_ZERO, 0, ei)))
             y[m] += (grp * scale).sum(axis=1)
     return y
+
+
+# ------------------------------------- NEXT-f1: column-wise scales ("Ours (Acc.)", §4.2)
+# PAPER.md:223-228 (Fig. 3(c)): "column-wise scaling factors ... Each scaling factor
+# corresponds to a constant activation value": plane i has one scale alpha_i[k] per input
+# column k, shared by every output row.  The LUT realisation is SPEC.md:375
+# (ColumnWisePerPlane): "for each plane i, activations are pre-shifted per column by that
+# plane's column PotScale, one LUT bank per plane built from shifted x; queries then
+# accumulate unscaled".  Readings R17-R18.
+def tile_planes(planes):
+    """The device-tiled permutation of plane bytes alone (same tiles as ``to_tiled``)."""
+    p = np.asarray(planes, dtype=np.uint8)
+    q, n, kb = p.shape
+    zeros = np.zeros((q, n, 1), dtype=np.int8)
+    return to_tiled(p, zeros, kb * 8)[0]
+
+
+def pack_colwise(signs, alpha_col):
+    """signs int8 [q][N][K] (+-1), alpha_col float32 [q][K] -> planes, exps_col, n_clamped.
+
+      1. sign fold per column (R3 applied to a column group, R17): alpha_i[k] < 0 negates
+         s_i[n][k] for every row n and keeps |alpha_i[k]|;
+      2. exponent: P = round(log2|alpha_i[k]|) (pot_exponent: same zero/clamp rules);
+      3. bits exactly as pack_canonical step 3 (R1, R2).
+    Returns planes uint8 [q][N][K/8], exps_col int8 [q][K], n_clamped.
+    """
+    s = np.asarray(signs)
+    a = np.asarray(alpha_col, dtype=np.float32)
+    if s.ndim != 3:
+        raise ValueError("signs must be [q][N][K]")
+    q, n, k = s.shape
+    if k % 8:
+        raise ValueError("need 8 | K")
+    if a.shape != (q, k):
+        raise ValueError("alpha_col must be [q][K]")
+    if not np.all((s == 1) | (s == -1)):
+        raise ValueError("signs must be -1 or +1")
+    exps, n_clamped = pot_exponent(a)
+    flip = (a < 0)[:, None, :]
+    folded = np.where(flip, -s.astype(np.int16), s.astype(np.int16))
+    bits = (folded == 1).astype(np.uint8).reshape(q, n, k // 8, 8)
+    weights = (1 << np.arange(8, dtype=np.uint16)).astype(np.uint16)
+    planes = (bits.astype(np.uint16) * weights).sum(axis=3).astype(np.uint8)
+    return planes, exps, n_clamped
+
+
+def _pow2(e):
+    e = np.asarray(e, dtype=np.int64)
+    return np.where(e == EXP_ZERO, 0.0, np.ldexp(1.0, np.where(e == EXP_ZERO, 0, e)))
+
+
+def dequant_colwise(planes, exps_col, K):
+    """W_hat[n][k] = sum_i 2^{e_i[k]} s_i[n][k] (column-wise PoT scales), fp64."""
+    p = np.asarray(planes, dtype=np.uint8)
+    s = unpack_signs(p, K).astype(np.float64)                  # [q][N][K]
+    scale = _pow2(exps_col)[:, None, :]                         # [q][1][K]
+    return (s * scale).sum(axis=0)
+
+
+def gemm_colwise(x, planes, exps_col, row_chunk=2048):
+    """y = x W_hat^T in fp64 with column-wise scales (the plain definition)."""
+    xf = np.atleast_2d(np.asarray(x, dtype=np.float64))
+    p = np.asarray(planes, dtype=np.uint8)
+    q, n, kb = p.shape
+    K = kb * 8
+    if xf.shape[1] != K or np.asarray(exps_col).shape != (q, K):
+        raise ValueError("x must be [M][K] and exps_col [q][K]")
+    y = np.empty((xf.shape[0], n), dtype=np.float64)
+    for n0 in range(0, n, row_chunk):
+        n1 = min(n, n0 + row_chunk)
+        y[:, n0:n1] = xf @ dequant_colwise(p[:, n0:n1], exps_col, K).T
+    return y
+
+
+def lut_gemm_colwise(x, planes, exps_col):
+    """SPEC.md:375 ColumnWisePerPlane, step by step, fp64:
+
+      1. pre-shift: x_i[k] = 2^{e_i[k]} * x[k]  (EXP_ZERO -> 0)     (the paper's step (1),
+         "bitwise shifts between activations and scaling factors", PAPER.md:182-183);
+      2. one LUT bank per plane: lut_direct on each 8-group of x_i  (PAPER.md:184-185);
+      3. query: plane i's key byte planes[i][n][t] selects bank_i T_t[key];
+      4. add all queried partial sums (no per-group shift).
+    """
+    xf = np.atleast_2d(np.asarray(x, dtype=np.float64))
+    p = np.asarray(planes, dtype=np.uint8)
+    q, n, kb = p.shape
+    sc = _pow2(exps_col)
+    y = np.zeros((xf.shape[0], n), dtype=np.float64)
+    t_idx = np.arange(kb)[None, :]
+    for m in range(xf.shape[0]):
+        for i in range(q):
+            xi = xf[m] * sc[i]
+            bank = np.stack([lut_direct(xi[8 * t:8 * t + 8]) for t in range(kb)])   # [K/8][256]
+            y[m] += bank[t_idx, p[i].astype(np.int64)].sum(axis=1)
+    return y
+
+
+def algorithmic_bytes_colwise(M, q, N, K):
+    """HBM bytes of one column-wise GEMV call: planes + int8 exps [q][K] + fp16 x + fp16 y."""
+    return q * N * K // 8 + q * K + 2 * M * K + 2 * M * N
 
 
 # ----------------------------------------------------------------------- output + metrics

@@ -357,7 +357,7 @@ struct ClusterShape {
 ClusterShape cluster_shape(int N, int K, int q) {
   (void)N; (void)q;
   static const int forced_sc = env_int("SHIFTADD_CLUSTER_SC", 0);
-  static const int half = env_int("SHIFTADD_CLUSTER_HALF", 1);
+  static const int half = env_int("SHIFTADD_CLUSTER_HALF", 0);
   const int S = K / kTileK;
   const int sc = forced_sc > 0 ? (forced_sc > kMaxSc ? kMaxSc : forced_sc) : ((S + 1) / 2 <= kMaxC ? 2 : kMaxSc);
   const int variant = sc > 2 ? kFull4 : (half ? kHalf : kFull2);

@@ -63,6 +63,23 @@ def gen_layer(q: int, N: int, K: int, g: int, seed: int, device="cpu", std: floa
     return signs, alpha
 
 
+def gen_layer_colwise(q: int, N: int, K: int, seed: int, device="cpu", std: float = 0.02):
+    """Greedy BCQ with column-wise scales (NEXT-f1): plane i takes
+    b_i = sign(r), alpha_i[k] = mean_n |r[n][k]| (one scale per input column), r -= alpha_i b_i.
+    Returns (signs int8 [q][N][K], alpha fp32 [q][K])."""
+    gen = _gen(seed, device)
+    r = torch.randn((N, K), generator=gen, device=device, dtype=torch.float32) * std
+    signs = torch.empty((q, N, K), dtype=torch.int8, device=device)
+    alpha = torch.empty((q, K), dtype=torch.float32, device=device)
+    for i in range(q):
+        b = torch.where(r >= 0, 1.0, -1.0)
+        a = r.abs().mean(dim=0)
+        signs[i] = b.to(torch.int8)
+        alpha[i] = a
+        r = r - a[None, :] * b
+    return signs, alpha
+
+
 def gen_x(M: int, K: int, seed: int, device="cpu", outlier_scale: float = 20.0):
     """fp16 activations [M][K]: N(0,1) with max(1, K//256) outlier channels x outlier_scale."""
     gen = _gen(seed, device)

@@ -371,3 +371,94 @@ def test_err_floor_metric():
 def test_fp16_output_rounding_is_rne():
     # 2049 is a tie between 2048 and 2050 in fp16 -> even mantissa 2048; 2051 -> 2052
     assert oracle.to_fp16(np.array([2049.0, 2051.0, 1e6])).tolist() == [2048.0, 2052.0, float("inf")]
+
+
+# --------------------------------------- S9: column-wise scales (NEXT-f1, "Ours (Acc.)")
+def test_s9_colwise_exact_pot_scales_reproduce_bcq_sum():
+    """alpha_i[k] = +-2^P exactly: dequant_colwise(pack_colwise(s, alpha)) = sum_i alpha_i[k]
+    s_i[n][k] element by element (Eq. 2 with K = 1 is exact on powers of two).  Pins the
+    per-column sign fold (a row-wise fold or a flipped polarity fails) and the bit order."""
+    rng = _rng(90)
+    q, N, K = 3, 5, 24
+    s = rng.choice([-1, 1], size=(q, N, K)).astype(np.int8)
+    P = rng.integers(-6, 7, size=(q, K))
+    sign = rng.choice([-1.0, 1.0], size=(q, K))
+    alpha = (sign * np.ldexp(1.0, P)).astype(np.float32)
+    planes, exps, ncl = oracle.pack_colwise(s, alpha)
+    assert ncl == 0 and exps.shape == (q, K) and np.array_equal(exps, P.astype(np.int8))
+    want = np.zeros((N, K))
+    for i in range(q):
+        for n in range(N):
+            for k in range(K):
+                want[n, k] += float(alpha[i, k]) * int(s[i, n, k])
+    assert np.array_equal(oracle.dequant_colwise(planes, exps, K), want)
+
+
+def test_s9_colwise_constant_exponents_reduce_to_rowwise_gemm():
+    """If every column of plane i has the same exponent c_i, column-wise and row-wise
+    (g = K) scales are the same weight: gemm_colwise must equal the pinned row-wise gemm."""
+    rng = _rng(91)
+    q, N, K = 3, 40, 256
+    planes = rng.integers(0, 256, size=(q, N, K // 8), dtype=np.uint8)
+    c = np.array([3, -2, 0], dtype=np.int8)
+    e_col = np.repeat(c[:, None], K, axis=1)
+    e_row = np.repeat(c[:, None, None], N, axis=1)                  # [q][N][1], g = K
+    x = _rand_fp16(rng, (2, K))
+    assert np.array_equal(oracle.gemm_colwise(x, planes, e_col), oracle.gemm(x, planes, e_row, K))
+
+
+def test_s9_colwise_all_ones_closed_form():
+    """All-ones planes: y[n] = sum_k x[k] * sum_i 2^{e_i[k]} for every row, exact rationals."""
+    rng = _rng(92)
+    q, N, K = 2, 3, 32
+    planes = np.full((q, N, K // 8), 0xFF, dtype=np.uint8)
+    e = rng.integers(-5, 6, size=(q, K)).astype(np.int8)
+    e[1, 7] = oracle.EXP_ZERO
+    x = _rand_fp16(rng, (1, K))
+    want = Fraction(0)
+    for k in range(K):
+        col = sum((Fraction(2) ** int(e[i, k]) for i in range(q) if e[i, k] != oracle.EXP_ZERO), Fraction(0))
+        want += _frac(x[0, k]) * col
+    y = oracle.gemm_colwise(x, planes, e)
+    assert np.all(y == float(want))
+
+
+def test_s9_colwise_column_scaling_equals_exponent_shift_on_that_column():
+    """Scaling x[k] by 2^d equals adding d to e_i[k] for every plane (exact in fp64).  With
+    N != K a scale applied per row instead of per column fails; a dropped plane fails too."""
+    rng = _rng(93)
+    q, N, K = 3, 24, 64
+    planes = rng.integers(0, 256, size=(q, N, K // 8), dtype=np.uint8)
+    e = rng.integers(-4, 5, size=(q, K)).astype(np.int8)
+    x = _rand_fp16(rng, (1, K)).astype(np.float64)
+    for k, d in [(0, 3), (17, -2), (63, 5)]:
+        x2 = x.copy()
+        x2[0, k] = np.ldexp(x2[0, k], d)
+        e2 = e.copy()
+        e2[:, k] += d
+        assert np.array_equal(oracle.gemm_colwise(x2, planes, e), oracle.gemm_colwise(x, planes, e2))
+    # and it is not a row-wise scale: shifting e of column 0 changes rows by column-0 terms
+    e3 = e.copy()
+    e3[:, 0] += 1
+    diff = oracle.gemm_colwise(x, planes, e3) - oracle.gemm_colwise(x, planes, e)
+    s0 = oracle.unpack_signs(planes, K)[:, :, 0].astype(np.float64)          # [q][N]
+    want = x[0, 0] * (s0 * np.ldexp(1.0, e[:, 0].astype(np.int64))[:, None]).sum(axis=0)
+    assert np.allclose(diff[0], want, rtol=0, atol=1e-12)
+
+
+def test_s9_colwise_lut_route_matches_definition():
+    rng = _rng(94)
+    q, N, K = 3, 33, 512
+    s, a = synth.gen_layer_colwise(q, N, K, seed=5)
+    planes, e, _ = oracle.pack_colwise(s.numpy(), a.numpy())
+    x = synth.gen_x(2, K, seed=6).numpy()
+    y0 = oracle.gemm_colwise(x, planes, e)
+    y1 = oracle.lut_gemm_colwise(x, planes, e)
+    assert oracle.err_floor(y1, y0) < 1e-12
+
+
+def test_s9_tile_planes_matches_to_tiled():
+    rng = _rng(95)
+    planes = rng.integers(0, 256, size=(2, 40, 64), dtype=np.uint8)
+    exps = np.zeros((2, 40, 4), dtype=np.int8)
+    assert np.array_equal(oracle.tile_planes(planes), oracle.to_tiled(planes, exps, 128)[0])
