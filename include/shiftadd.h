@@ -127,6 +127,31 @@ shiftadd_status shiftadd_lut_gemv(const uint16_t* x, const uint8_t* planes, cons
                                   void* workspace, size_t workspace_bytes, unsigned flags,
                                   void* stream);
 
+/* NEXT-f1 -- column-wise scales, "Ours (Acc.)" (Fig. 3(c); the paper's
+ * open gap "we lack the fast CUDA kernel", :545).  Plane i has one PoT scale per input
+ * column k, shared by all output rows:  W_hat[n][k] = sum_i 2^{e_i[k]} s_i(n, k).
+ *
+ * shiftadd_pack_colwise: signs int8 [q][N][K] (+-1), alpha_col fp32 [q][K] ->
+ *   planes (same byte format and layouts as shiftadd_pack, with each column's sign folded
+ *   into that column's bits of every row) and exps_col int8 [q][K] (same P rule, zero
+ *   sentinel and clamp counting as shiftadd_pack; no layout permutation).  1 <= q <= 8,
+ *   K % 8 == 0 (tiled: K % 256 == 0), N <= 1,048,576.  Errors as shiftadd_pack.
+ *
+ * shiftadd_lut_gemv_colwise: y[n] = fp16_rne( sum_i sum_k s_i(n,k) 2^{e_i[k]} x[k] ), M = 1,
+ *   tiled layout.  The kernel follows SPEC.md:375 (ColumnWisePerPlane): per 256-k slice it
+ *   builds one LUT bank per plane from x[k] * 2^{e_i[k]} (an exact fp32 shift), queries it
+ *   with that plane's key bytes and accumulates unscaled; the K-split is reduced inside a
+ *   thread-block cluster of K/256 CTAs.  Supported: layout TILED, K % 256 == 0,
+ *   K <= 4096, N such that a cluster band holds <= 512 row groups (N <= ~57 K rows on
+ *   B200); otherwise SHIFTADD_ERR_UNSUPPORTED.  1 <= q <= 4.  flags: 0 or SHIFTADD_FLAG_PDL.  No
+ *   workspace.  x 16-byte aligned, planes 16-byte aligned, exps_col 8-byte aligned. */
+shiftadd_status shiftadd_pack_colwise(const int8_t* signs, const float* alpha_col, int q, int N, int K,
+                                      int layout, uint8_t* planes, int8_t* exps_col, int32_t* counts,
+                                      void* stream);
+shiftadd_status shiftadd_lut_gemv_colwise(const uint16_t* x, const uint8_t* planes, const int8_t* exps_col,
+                                          int layout, int N, int K, int q, uint16_t* y, unsigned flags,
+                                          void* stream);
+
 /* Launch geometry the gemm call would use (for measurement/reporting; host only):
  * out[0] = grid CTAs, out[1] = threads per CTA, out[2] = dynamic smem bytes,
  * out[3] = kernel id (0 generic, 1 tiled M=1 split-K, 2 tiled small-batch, 3 tiled M=1

@@ -22,7 +22,7 @@ import torch
 __all__ = [
     "LAYOUT_CANONICAL", "LAYOUT_TILED", "FLAG_PDL", "FLAG_SPLITK", "EXP_ZERO", "ShiftAddError", "lib",
     "PackedLayer", "packed_bytes", "pack", "lut_gemm", "lut_gemv", "workspace_bytes",
-    "gemm_plan", "Workspace",
+    "gemm_plan", "Workspace", "pack_colwise", "lut_gemv_colwise",
 ]
 
 LAYOUT_CANONICAL = 0
@@ -71,6 +71,10 @@ def lib():
         L.shiftadd_lut_gemv.restype = c_int
         L.shiftadd_lut_gemv.argtypes = [vp, vp, vp, c_int, c_int, c_int, c_int, c_int, vp, vp, c_size,
                                         ctypes.c_uint, vp]
+        L.shiftadd_pack_colwise.restype = c_int
+        L.shiftadd_pack_colwise.argtypes = [vp, vp, c_int, c_int, c_int, c_int, vp, vp, vp, vp]
+        L.shiftadd_lut_gemv_colwise.restype = c_int
+        L.shiftadd_lut_gemv_colwise.argtypes = [vp, vp, vp, c_int, c_int, c_int, c_int, vp, ctypes.c_uint, vp]
         L.shiftadd_gemm_plan.restype = c_int
         L.shiftadd_gemm_plan.argtypes = [c_int] * 6 + [ctypes.POINTER(c_int * 4)]
         v = L.shiftadd_abi_version()
@@ -117,6 +121,7 @@ class PackedLayer:
     layout: int
     counts: torch.Tensor      # int32[2] on device: clamped exponents, invalid inputs
     _ws_bytes: dict = field(default_factory=dict, repr=False)   # M -> workspace bytes
+    colwise: bool = False     # NEXT-f1: exps is exps_col [q][K] (column-wise scales)
 
     @property
     def device(self):
@@ -151,6 +156,58 @@ def pack(signs: torch.Tensor, alpha: torch.Tensor, g: int, layout: int = LAYOUT_
                                  _ptr(counts), _stream_ptr(stream, dev))
     _check(st, "shiftadd_pack")
     return PackedLayer(planes, exps, q, N, K, g, layout, counts)
+
+
+def pack_colwise(signs: torch.Tensor, alpha_col: torch.Tensor, layout: int = LAYOUT_TILED,
+                 stream=None) -> PackedLayer:
+    """NEXT-f1 on the device: int8 sign planes [q][N][K] and column-wise fp32 scales [q][K]
+    -> key bytes (column signs folded) + exps_col int8 [q][K] (shiftadd_pack_colwise)."""
+    if signs.dtype != torch.int8 or alpha_col.dtype != torch.float32:
+        raise TypeError("signs must be int8 and alpha_col float32")
+    if not (signs.is_cuda and alpha_col.is_cuda):
+        raise ValueError("pack_colwise runs on the GPU; pass CUDA tensors")
+    if signs.dim() != 3 or alpha_col.dim() != 2:
+        raise ValueError("signs [q][N][K], alpha_col [q][K]")
+    q, N, K = signs.shape
+    if tuple(alpha_col.shape) != (q, K):
+        raise ValueError("alpha_col must be [q][K]")
+    signs = signs.contiguous()
+    alpha_col = alpha_col.contiguous()
+    pb, _ = packed_bytes(layout, q, N, K, K)   # plane bytes do not depend on g
+    dev = signs.device
+    planes = torch.empty(pb, dtype=torch.uint8, device=dev)
+    exps = torch.empty(q * K, dtype=torch.int8, device=dev)
+    counts = torch.zeros(2, dtype=torch.int32, device=dev)
+    with torch.cuda.device(dev):
+        st = lib().shiftadd_pack_colwise(_ptr(signs), _ptr(alpha_col), q, N, K, layout, _ptr(planes), _ptr(exps),
+                                         _ptr(counts), _stream_ptr(stream, dev))
+    _check(st, "shiftadd_pack_colwise")
+    return PackedLayer(planes, exps, q, N, K, K, layout, counts, colwise=True)
+
+
+def lut_gemv_colwise(x: torch.Tensor, layer: PackedLayer, out: torch.Tensor | None = None, pdl: bool = False,
+                     stream=None) -> torch.Tensor:
+    """NEXT-f1: y[N] = x[K] (.) a column-wise-scaled layer, fp16 (shiftadd_lut_gemv_colwise)."""
+    if not layer.colwise:
+        raise ValueError("layer was not packed with pack_colwise")
+    xv = x.reshape(-1)
+    if xv.dtype != torch.float16 or not xv.is_cuda or xv.numel() != layer.K:
+        raise ValueError("x must be fp16 [K] on the layer's device")
+    xv = xv.contiguous()
+    if out is None:
+        out = torch.empty(layer.N, dtype=torch.float16, device=layer.device)
+    if out.dtype != torch.float16 or out.numel() != layer.N or not out.is_contiguous():
+        raise ValueError("out must be contiguous fp16 [N]")
+    dev = layer.device
+    if torch.cuda.current_device() != dev.index:
+        torch.cuda.set_device(dev)
+    sptr = (stream if stream is not None else torch.cuda.current_stream(dev)).cuda_stream
+    st = lib().shiftadd_lut_gemv_colwise(xv.data_ptr(), layer.planes.data_ptr(), layer.exps.data_ptr(),
+                                         layer.layout, layer.N, layer.K, layer.q, out.data_ptr(),
+                                         FLAG_PDL if pdl else 0, sptr)
+    if st:
+        _check(st, "shiftadd_lut_gemv_colwise")
+    return out
 
 
 def workspace_bytes(layer: PackedLayer, M: int) -> int:

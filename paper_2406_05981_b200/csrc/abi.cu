@@ -139,6 +139,61 @@ shiftadd_status shiftadd_pack(const int8_t* signs, const float* alpha, int q, in
   return SHIFTADD_OK;
 }
 
+shiftadd_status shiftadd_pack_colwise(const int8_t* signs, const float* alpha_col, int q, int N, int K,
+                                      int layout, uint8_t* planes, int8_t* exps_col, int32_t* counts,
+                                      void* stream) {
+  if (!signs || !alpha_col || !planes || !exps_col) return fail(SHIFTADD_ERR_INVALID, "null pointer argument");
+  shiftadd_status st = check_shape(q, N, K, 8, 8);
+  if (st != SHIFTADD_OK) return st;
+  if ((st = check_layout(layout, K, 128)) != SHIFTADD_OK) return st;
+  if (!aligned(signs, 8) || !aligned(alpha_col, 4) || !aligned(planes, 16) || (counts && !aligned(counts, 4)))
+    return fail(SHIFTADD_ERR_INVALID, "misaligned pointer (signs 8 B, alpha 4 B, planes 16 B)");
+  DevInfo di;
+  if ((st = device_info(&di)) != SHIFTADD_OK) return st;
+  cudaError_t e = launch_pack_colwise(signs, alpha_col, q, N, K, layout, planes, exps_col, counts,
+                                      reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "pack_colwise launch");
+  return SHIFTADD_OK;
+}
+
+shiftadd_status shiftadd_lut_gemv_colwise(const uint16_t* x, const uint8_t* planes, const int8_t* exps_col,
+                                          int layout, int N, int K, int q, uint16_t* y, unsigned flags,
+                                          void* stream) {
+  if (!x || !planes || !exps_col || !y) return fail(SHIFTADD_ERR_INVALID, "null pointer argument");
+  shiftadd_status st = check_shape(q, N, K, 8, 4);
+  if (st != SHIFTADD_OK) return st;
+  if ((st = check_layout(layout, K, 128)) != SHIFTADD_OK) return st;
+  if (layout != SHIFTADD_LAYOUT_TILED)
+    return fail(SHIFTADD_ERR_UNSUPPORTED, "column-wise GEMV needs the tiled layout");
+  if (flags & ~SHIFTADD_FLAG_PDL) return fail(SHIFTADD_ERR_INVALID, "unknown flags 0x%x", flags);
+  if (!aligned(x, 16) || !aligned(planes, 16) || !aligned(exps_col, 8) || !aligned(y, 2))
+    return fail(SHIFTADD_ERR_INVALID, "misaligned pointer (x, planes 16 B; exps_col 8 B)");
+  DevInfo di;
+  if ((st = device_info(&di)) != SHIFTADD_OK) return st;
+  if (!colwise_applicable(N, K, q))
+    return fail(SHIFTADD_ERR_UNSUPPORTED, "column-wise GEMV: K=%d N=%d outside K <= 4096 / band limit", K, N);
+  GemmArgs a;
+  a.x = reinterpret_cast<const __half*>(x);
+  a.ldx = K;
+  a.planes = planes;
+  a.exps = exps_col;
+  a.M = 1;
+  a.N = N;
+  a.K = K;
+  a.q = q;
+  a.g = K;
+  a.y = reinterpret_cast<__half*>(y);
+  a.ldy = N;
+  a.workspace = nullptr;
+  a.workspace_bytes = 0;
+  a.flags = flags;
+  a.stream = reinterpret_cast<cudaStream_t>(stream);
+  const cudaError_t e = launch_gemv_colwise(a);
+  if (e == cudaErrorNotSupported) return fail(SHIFTADD_ERR_UNSUPPORTED, "no cluster configuration for this shape");
+  if (e != cudaSuccess) return cuda_fail(e, "lut_gemv_colwise launch");
+  return SHIFTADD_OK;
+}
+
 size_t shiftadd_workspace_bytes(int layout, int M, int N, int K, int q, int g) {
   if (check_shape(q, N, K, g, 4) != SHIFTADD_OK || check_layout(layout, K, g) != SHIFTADD_OK) return 0;
   if (M < 1 || M > 16) return 0;

@@ -184,6 +184,10 @@ cudaError_t launch_pack(const int8_t* signs, const float* alpha, int q, int N, i
                         int layout, uint8_t* planes, int8_t* exps, int32_t* counts,
                         cudaStream_t stream);
 
+cudaError_t launch_pack_colwise(const int8_t* signs, const float* alpha_col, int q, int N, int K,
+                                int layout, uint8_t* planes, int8_t* exps_col, int32_t* counts,
+                                cudaStream_t stream);
+
 LaunchPlan plan_generic(int M, int N, int K, int q, int g, int sms);
 cudaError_t launch_gemm_generic(const GemmArgs& a, const LaunchPlan& p);
 
@@ -192,6 +196,9 @@ size_t workspace_gemv_tiled(int N, int K);
 cudaError_t launch_gemv_tiled(const GemmArgs& a, const LaunchPlan& p);
 
 bool cluster_applicable(int N, int K, int q, int sms);
+// NEXT-f1: column-wise scales, M = 1, tiled planes, exps_col [q][K]; K <= 4096.
+bool colwise_applicable(int N, int K, int q);
+cudaError_t launch_gemv_colwise(const GemmArgs& a);
 LaunchPlan plan_gemv_cluster(int N, int K, int q, int sms);
 cudaError_t launch_gemv_cluster(const GemmArgs& a, const LaunchPlan& p);
 

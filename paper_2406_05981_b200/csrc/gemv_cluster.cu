@@ -35,7 +35,9 @@ namespace {
 
 constexpr int kMaxSc = 4;                 // resident LUT slots (slices per CTA)
 constexpr int kMaxC = 8;                  // portable cluster size
+constexpr int kMaxCColw = 16;             // column-wise kernel: non-portable clusters of <= 16
 constexpr int kMaxRGb = 128;              // row groups per band
+constexpr int kMaxRGbColw = 4 * kMaxRGb;  // column-wise: one slice per CTA
 
 // Shared-memory map of a variant with SCM LUT slots: LUT slabs, staged x, per-item row sums
 // part[t][row], receive buffer recv[rank][row of the owner's chunk].
@@ -44,7 +46,9 @@ struct Smem {
   static constexpr int lut = SCM <= 2 ? kLutBytes : 2 * kLutBytes;
   static constexpr int xstage = SCM * kTileK * 2;
   static constexpr int part = SCM * kMaxRGb * kTileRows * 4;
-  static constexpr int recv = (kMaxRGb * kTileRows + kMaxC) * 4;
+  // the 4-slot map also serves the column-wise kernel (one slice per CTA: part holds up to
+  // kMaxRGbColw row groups), whose bands may be 4x taller
+  static constexpr int recv = ((SCM == 4 ? 4 * kMaxRGb : kMaxRGb) * kTileRows + kMaxCColw) * 4;
   static constexpr int mbar = 16;   // the owner's receive mbarrier (8-byte aligned)
   static constexpr int total = lut + xstage + part + recv + mbar;
 };
@@ -135,6 +139,44 @@ __device__ __forceinline__ void build_lut_slot(uint32_t slot_base, uint32_t xadd
   }
 }
 
+// a2 for the column-wise variant (NEXT-f1): the LUT of plane i is built from the
+// pre-shifted activations x[k] * 2^{e_i[k]} (SPEC.md:375 ColumnWisePerPlane; the shift is an
+// exact fp32 multiply by a power of two: |x| < 2^17 and e in [-100, 100] keep it normal).
+__device__ __forceinline__ float pow2_or_zero(int e) {
+  return e == SHIFTADD_EXP_ZERO ? 0.f : __int_as_float((e + 127) << 23);
+}
+template <int NW>
+__device__ __forceinline__ void build_lut_slot_colw(uint32_t slot_base, uint32_t xaddr, const int8_t* e8, int warp,
+                                                    int lane) {
+  uint4 xv;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(xv.x), "=r"(xv.y), "=r"(xv.z), "=r"(xv.w)
+               : "r"(xaddr + 16 * lane));
+  const uint2 ev = __ldg(reinterpret_cast<const uint2*>(e8) + lane);
+  const float2 g01 = __half22float2(*reinterpret_cast<const __half2*>(&xv.x));
+  const float2 g23 = __half22float2(*reinterpret_cast<const __half2*>(&xv.y));
+  const float2 g45 = __half22float2(*reinterpret_cast<const __half2*>(&xv.z));
+  const float2 g67 = __half22float2(*reinterpret_cast<const __half2*>(&xv.w));
+  auto ex = [&](int b) { return (int)(int8_t)(((b < 4 ? ev.x : ev.y) >> (8 * (b & 3))) & 0xffu); };
+  const float2 f01 = make_float2(g01.x * pow2_or_zero(ex(0)), g01.y * pow2_or_zero(ex(1)));
+  const float2 f23 = make_float2(g23.x * pow2_or_zero(ex(2)), g23.y * pow2_or_zero(ex(3)));
+  const float2 f45 = make_float2(g45.x * pow2_or_zero(ex(4)), g45.y * pow2_or_zero(ex(5)));
+  const float2 f67 = make_float2(g67.x * pow2_or_zero(ex(6)), g67.y * pow2_or_zero(ex(7)));
+  const float A[4] = {-f01.x - f01.y, f01.x - f01.y, f01.y - f01.x, f01.x + f01.y};
+  const float B[4] = {-f23.x - f23.y, f23.x - f23.y, f23.y - f23.x, f23.x + f23.y};
+  float L[16];
+#pragma unroll
+  for (int lo = 0; lo < 16; ++lo) L[lo] = A[lo & 3] + B[lo >> 2];
+  const uint32_t col = slot_base + 4 * lane;
+#pragma unroll
+  for (int k = 0; k < 16 / NW; ++k) {
+    const int hi = warp + k * NW;
+    const float H = ((hi & 1 ? f45.x : -f45.x) + (hi & 2 ? f45.y : -f45.y)) +
+                    ((hi & 4 ? f67.x : -f67.x) + (hi & 8 ? f67.y : -f67.y));
+#pragma unroll
+    for (int lo = 0; lo < 16; ++lo) sts_f32(col + ((hi * 16 + lo) << 8), L[lo] + H);
+  }
+}
+
 // Lookup address of step j: byte 0 = column byte (cst byte j&1), byte 1 = key byte (word
 // byte j&3), byte 2 = 0 (cst byte 3), byte 3 = cluster rank (cst byte 2).
 __host__ __device__ constexpr uint32_t step_sel_c(int j) {
@@ -158,6 +200,38 @@ __device__ __forceinline__ float unit_dot_c(const uint4 (&w)[Q], const int (&e)[
   return acc;
 }
 
+// Column-wise (NEXT-f1): plane i queries its own LUT slot i (slab i >> 1 as the LDS
+// immediate, half i & 1 as the constant set) and the sums need no shift.
+template <int Q>
+__device__ __forceinline__ float unit_dot_colw(const uint4 (&w)[Q], const uint32_t (&cstE)[8],
+                                               const uint32_t (&cstO)[8]) {
+  float p0 = 0.f, p1 = 0.f;
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    constexpr uint32_t kSlab = kLutBytes;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const uint32_t word = (j < 4) ? w[i].x : (j < 8) ? w[i].y : (j < 12) ? w[i].z : w[i].w;
+      const uint32_t c = (i & 1) ? cstO[j >> 1] : cstE[j >> 1];
+      const uint32_t off = prmt(word, c, step_sel_c(j));
+      const float v = (i >> 1) ? lds_f32(kDynBase + kSlab + off) : lds_f32(kDynBase + off);
+      if (j & 1) p1 += v; else p0 += v;
+    }
+  }
+  return p0 + p1;
+}
+
+template <int Q>
+__device__ __forceinline__ void load_planes_unit(const uint4* __restrict__ planes, long long u, int lane, uint64_t pol,
+                                                 uint4 (&w)[Q]) {
+#pragma unroll
+  for (int i = 0; i < Q; ++i) w[i] = ldg_stream(planes + (u * Q + i) * 32 + lane, pol);
+}
+
+// column-wise: no exponent registers, 4 per plane per slot
+__host__ __device__ constexpr int cl_ring_colw(int Q, int REGS) {
+  return (REGS - 56) / (4 * Q) < 1 ? 1 : ((REGS - 56) / (4 * Q) > 8 ? 8 : (REGS - 56) / (4 * Q));
+}
 __host__ __device__ constexpr int cl_ring(int Q, int REGS) {
   return (REGS - 56) / (5 * Q) < 1 ? 1 : ((REGS - 56) / (5 * Q) > 8 ? 8 : (REGS - 56) / (5 * Q));
 }
@@ -176,12 +250,13 @@ struct Cursor {
 
 constexpr int kFlagPdl = 1, kFlagXFirst = 2, kFlagBarrierTail = 4;
 
-template <int Q, int SCM, int NW, int REGS>
+template <int Q, int SCM, int NW, int REGS, bool COLW>
 __global__ void __launch_bounds__(NW * 32) __maxnreg__(REGS)
 gemv_cluster_kernel(const __half* __restrict__ x, const uint4* __restrict__ planes,
                     const int8_t* __restrict__ exps, int N, int S, int RG, int C, __half* __restrict__ y,
                     int flags, unsigned long long* __restrict__ trace) {
-  constexpr int D = cl_ring(Q, REGS);
+  constexpr int D = COLW ? cl_ring_colw(Q, REGS) : cl_ring(Q, REGS);
+  static_assert(!COLW || (SCM == 4 && Q <= 4), "column-wise: one LUT slot per plane");
   const bool pdl = flags & kFlagPdl;
   if (threadIdx.x == 0) check_dyn_base();
   unsigned long long* tr = trace ? trace + 32 * blockIdx.x : nullptr;   // dev trace
@@ -234,7 +309,8 @@ gemv_cluster_kernel(const __half* __restrict__ x, const uint4* __restrict__ plan
 #pragma unroll
     for (int k = 0; k < D; ++k)
       if (k < Mw) {
-        load_unit<Q>(planes, exps, (long long)(s0 + ld.t) * RG + rg0 + ld.rgl, lane, pol_stream, w[k], e[k]);
+        if (COLW) load_planes_unit<Q>(planes, (long long)(s0 + ld.t) * RG + rg0 + ld.rgl, lane, pol_stream, w[k]);
+        else load_unit<Q>(planes, exps, (long long)(s0 + ld.t) * RG + rg0 + ld.rgl, lane, pol_stream, w[k], e[k]);
         ld.advance<NW>(RGb);
       }
   };
@@ -247,11 +323,19 @@ gemv_cluster_kernel(const __half* __restrict__ x, const uint4* __restrict__ plan
   if (!pdl && (flags & kFlagXFirst)) prefill();
   __syncthreads();
   if (tr && threadIdx.x == 0) tr[1] = gtimer_ns();
+  if (COLW) {   // one slice, one slot per plane built from x * 2^{e_i[k]}
+    const int K = S * kTileK;
 #pragma unroll
-  for (int t = 0; t < SCM; ++t)
-    if (t < Sc)
-      build_lut_slot<NW>(base + (uint32_t)(t >> 1) * kLutBytes + (uint32_t)(t & 1) * 128u, xs + t * (kTileK * 2), warp,
-                     lane);
+    for (int i = 0; i < Q; ++i)
+      build_lut_slot_colw<NW>(base + (uint32_t)(i >> 1) * kLutBytes + (uint32_t)(i & 1) * 128u, xs,
+                              exps + (size_t)i * K + (size_t)s0 * kTileK, warp, lane);
+  } else {
+#pragma unroll
+    for (int t = 0; t < SCM; ++t)
+      if (t < Sc)
+        build_lut_slot<NW>(base + (uint32_t)(t >> 1) * kLutBytes + (uint32_t)(t & 1) * 128u, xs + t * (kTileK * 2),
+                           warp, lane);
+  }
   __syncthreads();
   if (tr && threadIdx.x == 0) tr[2] = gtimer_ns();
 
@@ -270,7 +354,9 @@ gemv_cluster_kernel(const __half* __restrict__ x, const uint4* __restrict__ plan
       const int m = b + k;
       if (m >= Mw) break;
       float v;
-      if (SCM <= 2) {
+      if (COLW) {
+        v = unit_dot_colw<Q>(w[k], cstE, cstO);
+      } else if (SCM <= 2) {
         v = (pc.t & 1) ? unit_dot_c<Q, kDynBase>(w[k], e[k], cstO) : unit_dot_c<Q, kDynBase>(w[k], e[k], cstE);
       } else {
         switch (pc.t) {   // slot t: slab t >> 1 (LDS immediate), half t & 1 (constant set)
@@ -284,7 +370,8 @@ gemv_cluster_kernel(const __half* __restrict__ x, const uint4* __restrict__ plan
       if (h == 0) sts_f32(part + 4u * (uint32_t)((pc.t * RGb + pc.rgl) * kTileRows + r), v);
       pc.advance<NW>(RGb);
       if (m + D < Mw) {
-        load_unit<Q>(planes, exps, (long long)(s0 + ld.t) * RG + rg0 + ld.rgl, lane, pol_stream, w[k], e[k]);
+        if (COLW) load_planes_unit<Q>(planes, (long long)(s0 + ld.t) * RG + rg0 + ld.rgl, lane, pol_stream, w[k]);
+        else load_unit<Q>(planes, exps, (long long)(s0 + ld.t) * RG + rg0 + ld.rgl, lane, pol_stream, w[k], e[k]);
         ld.advance<NW>(RGb);
       }
     }
@@ -347,7 +434,7 @@ int cluster_trace() {
 // stream takes its place and, under PDL, prefetches its weights while this kernel's tail
 // (cluster barrier, reduction) runs.  FULL4: 16 warps, 4 slots (170 KB, one CTA per SM),
 // for K up to 8192 with clusters of <= 8.
-enum Variant { kHalf = 0, kFull2 = 1, kFull4 = 2 };
+enum Variant { kHalf = 0, kFull2 = 1, kFull4 = 2, kColw = 3 };
 struct ClusterShape {
   int variant;
   int sc;   // max slices per CTA
@@ -367,20 +454,23 @@ ClusterShape cluster_shape(int N, int K, int q) {
 int variant_threads(int v) { return v == kHalf ? 8 * 32 : 16 * 32; }
 int variant_smem(int v) { return v == kFull4 ? Smem<4>::total : Smem<2>::total; }
 
-template <int Q, int SCM, int NW, int REGS>
+template <int Q, int SCM, int NW, int REGS, bool COLW = false>
 cudaError_t set_attrs() {
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
   std::call_once(once, [] {
-    err = cudaFuncSetAttribute(gemv_cluster_kernel<Q, SCM, NW, REGS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               Smem<SCM>::total);
+    err = cudaFuncSetAttribute(gemv_cluster_kernel<Q, SCM, NW, REGS, COLW>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<SCM>::total);
+    if (err == cudaSuccess && COLW)
+      err = cudaFuncSetAttribute(gemv_cluster_kernel<Q, SCM, NW, REGS, COLW>,
+                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   });
   return err;
 }
 
-template <int SCM, int NW>
+template <int SCM, int NW, bool COLW = false>
 int occupancy_clusters(int C) {
-  if (set_attrs<2, SCM, NW, 128>() != cudaSuccess) return 0;
+  if (set_attrs<2, SCM, NW, 128, COLW>() != cudaSuccess) return 0;
   cudaLaunchConfig_t c = {};
   c.gridDim = dim3(C * 64);
   c.blockDim = dim3(NW * 32);
@@ -393,7 +483,7 @@ int occupancy_clusters(int C) {
   c.attrs = &attr;
   c.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, gemv_cluster_kernel<2, SCM, NW, 128>, &c) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&n, gemv_cluster_kernel<2, SCM, NW, 128, COLW>, &c) != cudaSuccess) {
     cudaGetLastError();
     n = 0;
   }
@@ -402,13 +492,15 @@ int occupancy_clusters(int C) {
 
 // Max co-resident clusters of size C for a variant (cached).
 int max_clusters(int variant, int C) {
-  static int cache[3][kMaxC + 1] = {};
+  static int cache[4][kMaxCColw + 1] = {};
   static std::mutex mu;
   std::lock_guard<std::mutex> g(mu);
   int& slot = cache[variant][C];
   if (slot) return slot;
-  const int n = variant == kHalf ? occupancy_clusters<2, 8>(C)
-                                 : (variant == kFull2 ? occupancy_clusters<2, 16>(C) : occupancy_clusters<4, 16>(C));
+  const int n = variant == kHalf    ? occupancy_clusters<2, 8>(C)
+                : variant == kFull2 ? occupancy_clusters<2, 16>(C)
+                : variant == kFull4 ? occupancy_clusters<4, 16>(C)
+                                    : occupancy_clusters<4, 16, true>(C);
   slot = n > 0 ? n : -1;
   return slot;
 }
@@ -422,9 +514,9 @@ int barrier_tail() {
   return v;
 }
 
-template <int Q, int SCM, int NW, int REGS>
+template <int Q, int SCM, int NW, int REGS, bool COLW = false>
 cudaError_t launch_cluster_q(const GemmArgs& a, const LaunchPlan& p, int C) {
-  const cudaError_t ae = set_attrs<Q, SCM, NW, REGS>();
+  const cudaError_t ae = set_attrs<Q, SCM, NW, REGS, COLW>();
   if (ae != cudaSuccess) return ae;
   const int S = a.K / kTileK;
   const int RG = (a.N + kTileRows - 1) / kTileRows;
@@ -447,7 +539,7 @@ cudaError_t launch_cluster_q(const GemmArgs& a, const LaunchPlan& p, int C) {
   if (cluster_trace() && a.workspace && a.workspace_bytes >= kCounterBytes + (size_t)p.grid * 256)
     trace = reinterpret_cast<unsigned long long*>(static_cast<char*>(a.workspace) + kCounterBytes);
   const int flags = (pdl ? kFlagPdl : 0) | (x_first() ? kFlagXFirst : 0) | (barrier_tail() ? kFlagBarrierTail : 0);
-  return cudaLaunchKernelEx(&c, gemv_cluster_kernel<Q, SCM, NW, REGS>, a.x,
+  return cudaLaunchKernelEx(&c, gemv_cluster_kernel<Q, SCM, NW, REGS, COLW>, a.x,
                             reinterpret_cast<const uint4*>(a.planes), a.exps, a.N, S, RG, C, a.y, flags, trace);
 }
 
@@ -492,6 +584,34 @@ LaunchPlan plan_gemv_cluster(int N, int K, int q, int sms) {
   const int ncl = max_clusters(cs.variant, cs.C);
   const int bands = ncl < RG ? ncl : RG;
   return LaunchPlan{bands * cs.C, variant_threads(cs.variant), variant_smem(cs.variant), 3};
+}
+
+// NEXT-f1: column-wise scales.  One slice per CTA (its q LUT slots are the q planes' banks),
+// so C = S; clusters of up to 16 (non-portable) cover K <= 4096.
+bool colwise_applicable(int N, int K, int q) {
+  const int S = K / kTileK;
+  if (K % kTileK || S < 1 || S > kMaxCColw || q < 1 || q > 4) return false;
+  const int ncl = max_clusters(kColw, S);
+  if (ncl <= 0) return false;
+  const int RG = (N + kTileRows - 1) / kTileRows;
+  const int bands = ncl < RG ? ncl : RG;
+  return (RG + bands - 1) / bands <= kMaxRGbColw;
+}
+
+cudaError_t launch_gemv_colwise(const GemmArgs& a) {
+  const int S = a.K / kTileK;
+  const int RG = (a.N + kTileRows - 1) / kTileRows;
+  const int ncl = max_clusters(kColw, S);
+  if (ncl <= 0) return cudaErrorNotSupported;
+  const int bands = ncl < RG ? ncl : RG;
+  const LaunchPlan p{bands * S, 16 * 32, Smem<4>::total, 4};
+  switch (a.q) {
+    case 1: return launch_cluster_q<1, 4, 16, 128, true>(a, p, S);
+    case 2: return launch_cluster_q<2, 4, 16, 128, true>(a, p, S);
+    case 3: return launch_cluster_q<3, 4, 16, 128, true>(a, p, S);
+    case 4: return launch_cluster_q<4, 4, 16, 128, true>(a, p, S);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 cudaError_t launch_gemv_cluster(const GemmArgs& a, const LaunchPlan& p) {

@@ -84,9 +84,11 @@ __device__ __forceinline__ bool byte_source(int layout, long long o, int q, int 
 
 // One thread per output key byte: 8 consecutive signs -> 8 bits (bit b <-> k = 8kb + b,
 // 1 <-> +1 after the sign fold of the byte's scale group).
+// colwise (NEXT-f1): alpha is alpha_col [q][K] and each bit b flips with the sign of its own
+// column's scale alpha_col[i][8kb + b] (the column-wise sign fold, R17).
 __global__ void pack_planes_kernel(const int8_t* __restrict__ signs, const float* __restrict__ alpha,
                                    int q, int N, int K, int g, int layout, long long nbytes, int RG,
-                                   uint8_t* __restrict__ planes, int32_t* counts) {
+                                   uint8_t* __restrict__ planes, int32_t* counts, int colwise) {
   const int KB = K >> 3;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long base = (long long)blockIdx.x * blockDim.x; base < nbytes; base += stride) {
@@ -98,8 +100,16 @@ __global__ void pack_planes_kernel(const int8_t* __restrict__ signs, const float
       if (byte_source(layout, o, q, N, KB, RG, &i, &n, &kb)) {
         const long long row = (long long)i * N + n;
         const uint2 sv = __ldg(reinterpret_cast<const uint2*>(signs + row * K) + kb);
-        const float a = __ldg(alpha + row * (K / g) + (kb * 8) / g);
-        const uint32_t flip = (a < 0.f) ? 0xffu : 0u;
+        uint32_t flip;
+        if (colwise) {
+          const float* ac = alpha + (long long)i * K + kb * 8;
+          flip = 0u;
+#pragma unroll
+          for (int b = 0; b < 8; ++b) flip |= (__ldg(ac + b) < 0.f ? 1u : 0u) << b;
+        } else {
+          const float a = __ldg(alpha + row * (K / g) + (kb * 8) / g);
+          flip = (a < 0.f) ? 0xffu : 0u;
+        }
         uint32_t bits = 0;
 #pragma unroll
         for (int b = 0; b < 8; ++b) {
@@ -159,11 +169,28 @@ cudaError_t launch_pack(const int8_t* signs, const float* alpha, int q, int N, i
   const long long nbytes = canon ? (long long)q * N * (K / 8)
                                  : (long long)(K / kTileK) * RG * q * kTileBytes;
   pack_planes_kernel<<<grid_for(nbytes, threads), threads, 0, stream>>>(signs, alpha, q, N, K, g, layout,
-                                                                         nbytes, RG, planes, counts);
+                                                                         nbytes, RG, planes, counts, 0);
   if (!canon) {
     const long long ne = (long long)(K / kTileK) * RG * q * kTileExps;
     pack_exps_tiled_kernel<<<grid_for(ne, threads), threads, 0, stream>>>(alpha, q, N, K, g, RG, ne, exps);
   }
+  return cudaGetLastError();
+}
+
+// NEXT-f1 column-wise pack: exps_col [q][K] (no layout permutation: the kernels read it by
+// column when they pre-shift x) and planes in either layout with the per-column sign fold.
+cudaError_t launch_pack_colwise(const int8_t* signs, const float* alpha_col, int q, int N, int K,
+                                int layout, uint8_t* planes, int8_t* exps_col, int32_t* counts,
+                                cudaStream_t stream) {
+  const int threads = 256;
+  const long long groups = (long long)q * K;
+  const bool canon = layout == SHIFTADD_LAYOUT_CANONICAL;
+  const int RG = (N + kTileRows - 1) / kTileRows;
+  pack_exps_kernel<<<grid_for(groups, threads), threads, 0, stream>>>(alpha_col, groups, exps_col, counts);
+  const long long nbytes = canon ? (long long)q * N * (K / 8)
+                                 : (long long)(K / kTileK) * RG * q * kTileBytes;
+  pack_planes_kernel<<<grid_for(nbytes, threads), threads, 0, stream>>>(signs, alpha_col, q, N, K, 8, layout,
+                                                                         nbytes, RG, planes, counts, 1);
   return cudaGetLastError();
 }
 

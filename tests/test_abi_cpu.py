@@ -128,3 +128,16 @@ def test_python_binding_fails_loudly_without_gpu_tensors():
     import paper_2406_05981_b200 as sa
     with pytest.raises(ValueError):
         sa.pack(torch.ones((1, 16, 256), dtype=torch.int8), torch.ones((1, 16, 2)), 128)
+
+
+def test_colwise_validation_happens_before_any_launch(L):
+    _r1, p = _buf(1 << 16)
+    # null pointers, bad q, canonical layout (the column-wise GEMV is tiled-only)
+    assert L.shiftadd_pack_colwise(None, p, 3, 16, 256, 1, p, p, None, None) == 2
+    assert L.shiftadd_pack_colwise(p, p, 9, 16, 256, 1, p, p, None, None) == 2
+    assert L.shiftadd_pack_colwise(p, p, 3, 16, 250, 1, p, p, None, None) == 2
+    assert L.shiftadd_lut_gemv_colwise(None, p, p, 1, 16, 256, 3, p, 0, None) == 2
+    assert L.shiftadd_lut_gemv_colwise(p, p, p, 1, 16, 256, 5, p, 0, None) == 2
+    assert L.shiftadd_lut_gemv_colwise(p, p, p, 0, 16, 256, 3, p, 0, None) == 6
+    assert L.shiftadd_lut_gemv_colwise(p, p, p, 1, 16, 256, 3, p, 8, None) == 2
+    assert b"flags" in L.shiftadd_last_error()

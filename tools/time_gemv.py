@@ -15,6 +15,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("shapes", nargs="+")
 ap.add_argument("--pdl", action="store_true")
 ap.add_argument("--splitk", action="store_true")
+ap.add_argument("--colwise", action="store_true", help="NEXT-f1 column-wise scales (M = 1)")
 ap.add_argument("--m", type=int, default=1)
 ap.add_argument("--reps", type=int, default=200)
 a = ap.parse_args()
@@ -23,17 +24,22 @@ l2 = torch.cuda.get_device_properties(dev).L2_cache_size
 peak = 6550.7
 for spec in a.shapes:
     N, K, q = map(int, spec.split(":"))
-    lb = q * N * K // 8 + q * N * K // 128
+    lb = q * N * K // 8 + (q * K if a.colwise else q * N * K // 128)
     R = max(2, -(-4 * l2 // lb))
     copies = []
     for r in range(R):
         if r < 2:
-            signs, alpha = synth.gen_layer(q, N, K, 128, seed=synth.seed_for(1, 0, r), device=dev)
-            copies.append(sa.pack(signs, alpha, 128, layout=sa.LAYOUT_TILED))
+            if a.colwise:
+                signs, alpha = synth.gen_layer_colwise(q, N, K, seed=synth.seed_for(1, 0, r), device=dev)
+                copies.append(sa.pack_colwise(signs, alpha))
+            else:
+                signs, alpha = synth.gen_layer(q, N, K, 128, seed=synth.seed_for(1, 0, r), device=dev)
+                copies.append(sa.pack(signs, alpha, 128, layout=sa.LAYOUT_TILED))
             del signs, alpha
         else:
             base = copies[r % 2]
-            copies.append(sa.PackedLayer(base.planes.clone(), base.exps.clone(), q, N, K, 128, base.layout, base.counts))
+            copies.append(sa.PackedLayer(base.planes.clone(), base.exps.clone(), q, N, K, base.g, base.layout,
+                                         base.counts, colwise=base.colwise))
     x = synth.gen_x(a.m, K, seed=1, device=dev)
     y = torch.empty((a.m, N), dtype=torch.float16, device=dev)
     ws = sa.Workspace(dev)
@@ -42,14 +48,20 @@ for spec in a.shapes:
     # and the GEMV on stream s would overwrite it.
     torch.cuda.synchronize(dev)
     s = torch.cuda.Stream(dev)
+    def call(L):
+        if a.colwise:
+            sa.lut_gemv_colwise(x, L, out=y.view(-1), pdl=a.pdl)
+        else:
+            sa.lut_gemm(x, L, out=y, workspace=ws, pdl=a.pdl, splitk=a.splitk)
+
     with torch.cuda.stream(s):
         for t in range(3):
-            sa.lut_gemm(x, copies[t % R], out=y, workspace=ws, pdl=a.pdl, splitk=a.splitk)
+            call(copies[t % R])
     s.synchronize()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=s):
         for t in range(a.reps):
-            sa.lut_gemm(x, copies[t % R], out=y, workspace=ws, pdl=a.pdl, splitk=a.splitk)
+            call(copies[t % R])
     with torch.cuda.stream(s):
         g.replay()
         e0 = torch.cuda.Event(enable_timing=True)
@@ -60,7 +72,8 @@ for spec in a.shapes:
     s.synchronize()
     us = e0.elapsed_time(e1) / a.reps * 1e3
     tot = lb + 2 * a.m * K + 2 * a.m * N
-    print("N=%6d K=%6d q=%d M=%2d  %8.2f us  %7.1f GB/s  frac %.3f  (R=%d, exp=%s)" % (
-        N, K, q, a.m, us, tot / us * 1e-3, tot / us * 1e-3 / peak, R, os.environ.get("SHIFTADD_EXP", "0")), flush=True)
+    print("N=%6d K=%6d q=%d M=%2d  %8.2f us  %7.1f GB/s  frac %.3f  (R=%d, %s)" % (
+        N, K, q, a.m, us, tot / us * 1e-3, tot / us * 1e-3 / peak, R, "colwise" if a.colwise else "rowwise g=128"),
+        flush=True)
     del copies, g
     torch.cuda.empty_cache()
