@@ -23,6 +23,9 @@ Parity status per function (see DESIGN.md §"Oracle pins"):
                     exponents per plane reduce to the pinned row-wise gemm with g = K;
                     all-ones closed form; x-column scaling == exponent shift of that column
                     on N != K; LUT route == definition)
+  additive_pot / pack_apot2 / dequant_apot2 / gemm_apot2  (NEXT-f2)
+                    pinned  (S10: SPEC.md:209-211 worked values, exact two-term scales,
+                    residual non-increasing, K=2 error <= K=1 error, c2 = 0 reduces to gemm)
 """
 
 from .ref import *  # noqa: F401,F403

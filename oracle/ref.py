@@ -44,7 +44,8 @@ __all__ = [
     "tiled_sizes", "dequant", "gemm", "gemm_scalar", "lut_direct", "lut_incremental",
     "lut_gemm", "to_fp16", "err_floor", "err_normwise", "packed_bytes",
     "algorithmic_bytes", "tile_planes", "pack_colwise", "dequant_colwise", "gemm_colwise",
-    "lut_gemm_colwise", "algorithmic_bytes_colwise",
+    "lut_gemm_colwise", "algorithmic_bytes_colwise", "additive_pot", "pack_apot2",
+    "dequant_apot2", "gemm_apot2",
 ]
 
 
@@ -414,6 +415,76 @@ def lut_gemm_colwise(x, planes, exps_col):
 def algorithmic_bytes_colwise(M, q, N, K):
     """HBM bytes of one column-wise GEMV call: planes + int8 exps [q][K] + fp16 x + fp16 y."""
     return q * N * K // 8 + q * K + 2 * M * K + 2 * M * N
+
+
+# --------------------------------------------- NEXT-f2: additive PoT with K = 2 terms
+# Eq. 2 (PAPER.md:174-177): alpha_k = POT(r_{k-1}), r_{k-1} = alpha - sum_{j<k} alpha_j,
+# POT(a) = sign(a) 2^round(log2|a|), K terms "adopt a greedy strategy".  Readings R19-R20.
+def additive_pot(alpha, K):
+    """Greedy K-term PoT of one scalar (Python floats, exact): [(sign, P), ...] of length
+    <= K (a zero residual ends the expansion early).  Term 1 uses pot_exponent's clamp."""
+    terms = []
+    r = float(np.float32(alpha))
+    for k in range(K):
+        if r == 0.0:
+            break
+        p = int(pot_exponent(np.float32(r))[0])
+        sgn = 1 if r > 0 else -1
+        terms.append((sgn, p))
+        r = r - sgn * math.ldexp(1.0, p)
+    return terms
+
+
+def pack_apot2(signs, alpha, g):
+    """K = 2 additive PoT pack: planes and exps exactly as pack_canonical (term 1, its sign
+    folded into the bits), plus exps2 int8 [q][N][K/g]: the second term relative to the
+    first, c2 = s1*s2*(P1 - P2), so a group's folded scale is 2^P1 (1 + sign(c2) 2^-|c2|).
+    c2 = 0 (no second term) when alpha == 0, the residual is 0, P1 was clamped, or
+    P2 < EXP_MIN or P1 - P2 > 127 (reading R19).  P2 <= P1 - 1 always (|r1| <= (sqrt2-1) 2^P1),
+    and r1 = alpha - s1 2^P1 is exact in fp32 (Sterbenz), so c2 is a pure function of alpha.
+    Returns planes, exps, exps2, n_clamped."""
+    planes, exps, n_clamped = pack_canonical(signs, alpha, g)
+    a = np.asarray(alpha, dtype=np.float32)
+    e1 = exps.astype(np.int64)
+    mag = np.abs(a.astype(np.float64))
+    zero = mag == 0.0
+    with np.errstate(divide="ignore"):
+        p_raw = np.rint(np.log2(np.where(zero, 1.0, mag)))
+    clamped = (~zero) & ((p_raw < EXP_MIN) | (p_raw > EXP_MAX))
+    s1 = np.where(a < 0, -1.0, 1.0)
+    r1 = a.astype(np.float64) - s1 * np.ldexp(1.0, np.where(zero, 0, e1))
+    rz = (r1 == 0.0) | zero | clamped
+    with np.errstate(divide="ignore"):
+        p2 = np.rint(np.log2(np.where(rz, 1.0, np.abs(r1))))
+    d = e1 - p2
+    ok = (~rz) & (p2 >= EXP_MIN) & (d <= 127)
+    sign = s1 * np.where(r1 < 0, -1.0, 1.0)
+    exps2 = np.where(ok, sign * d, 0).astype(np.int8)
+    return planes, exps, exps2, n_clamped
+
+
+def dequant_apot2(planes, exps, exps2, g, K):
+    """W_hat[n][k] = sum_i 2^{e_i} (1 + sign(c2) 2^{-|c2|}) s_i[n][k] (folded bits), fp64."""
+    p = np.asarray(planes, dtype=np.uint8)
+    e = np.asarray(exps, dtype=np.int8).astype(np.int64)
+    c2 = np.asarray(exps2, dtype=np.int8).astype(np.int64)
+    s = unpack_signs(p, K).astype(np.float64)
+    one = np.where(e == EXP_ZERO, 0.0, np.ldexp(1.0, np.where(e == EXP_ZERO, 0, e)))
+    two = np.where(c2 == 0, 0.0, np.sign(c2) * np.ldexp(one, -np.abs(c2)))
+    return (s * np.repeat(one + two, g, axis=2)).sum(axis=0)
+
+
+def gemm_apot2(x, planes, exps, exps2, g, row_chunk=2048):
+    """y = x W_hat^T in fp64 with K = 2 additive PoT scales (the plain definition)."""
+    xf = np.atleast_2d(np.asarray(x, dtype=np.float64))
+    p = np.asarray(planes, dtype=np.uint8)
+    q, n, kb = p.shape
+    K = kb * 8
+    y = np.empty((xf.shape[0], n), dtype=np.float64)
+    for n0 in range(0, n, row_chunk):
+        n1 = min(n, n0 + row_chunk)
+        y[:, n0:n1] = xf @ dequant_apot2(p[:, n0:n1], exps[:, n0:n1], exps2[:, n0:n1], g, K).T
+    return y
 
 
 # ----------------------------------------------------------------------- output + metrics

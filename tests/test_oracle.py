@@ -462,3 +462,74 @@ def test_s9_tile_planes_matches_to_tiled():
     planes = rng.integers(0, 256, size=(2, 40, 64), dtype=np.uint8)
     exps = np.zeros((2, 40, 4), dtype=np.int8)
     assert np.array_equal(oracle.tile_planes(planes), oracle.to_tiled(planes, exps, 128)[0])
+
+
+# ---------------------------------------------- S10: additive PoT, K = 2 terms (NEXT-f2)
+def test_s10_additive_pot_spec_examples():
+    for c in _gold("apot_spec.json")["cases"]:
+        terms = oracle.additive_pot(c["alpha"], c["K"])
+        assert [list(t) for t in terms] == c["terms"], c["cite"]
+        val = sum(sg * 2.0 ** p for sg, p in terms)
+        assert c["alpha"] - val == c["residual"], c["cite"]
+
+
+def test_s10_residual_non_increasing_and_k2_no_worse_than_k1():
+    """residual magnitude non-increasing per term; the K-term error <= 1-term."""
+    rng = _rng(100)
+    for a in rng.standard_normal(2000) * 10.0 ** rng.uniform(-6, 3, 2000):
+        a = float(np.float32(a))
+        prev = abs(a)
+        val = 0.0
+        for sg, p in oracle.additive_pot(a, 3):
+            val += sg * 2.0 ** p
+            assert abs(a - val) <= prev
+            prev = abs(a - val)
+
+
+def test_s10_exact_two_term_scales_are_reproduced():
+    """alpha = +-(2^A + sigma 2^B), A - B >= 2: round(log2|alpha|) = A, the residual is exactly
+    sigma 2^B, so W_hat = alpha * s exactly (element by element, against alpha itself)."""
+    rng = _rng(101)
+    q, N, K, g = 2, 4, 64, 16
+    A = rng.integers(-8, 4, size=(q, N, K // g))
+    B = A - rng.integers(2, 9, size=A.shape)
+    sig = rng.choice([-1.0, 1.0], size=A.shape)
+    sgn = rng.choice([-1.0, 1.0], size=A.shape)
+    alpha = (sgn * (np.ldexp(1.0, A) + sig * np.ldexp(1.0, B))).astype(np.float32)
+    assert np.array_equal(alpha.astype(np.float64), sgn * (np.ldexp(1.0, A) + sig * np.ldexp(1.0, B)))
+    s = rng.choice([-1, 1], size=(q, N, K)).astype(np.int8)
+    planes, e1, c2, ncl = oracle.pack_apot2(s, alpha, g)
+    assert ncl == 0 and np.array_equal(e1, A.astype(np.int8))
+    assert np.array_equal(np.abs(c2.astype(np.int64)), A - B)
+    want = (s.astype(np.float64) * np.repeat(alpha.astype(np.float64), g, axis=2)).sum(axis=0)
+    assert np.array_equal(oracle.dequant_apot2(planes, e1, c2, g, K), want)
+
+
+def test_s10_vectorised_pack_matches_scalar_greedy():
+    """The vectorised c2 of pack_apot2 equals the scalar greedy of additive_pot (K = 2) on
+    random alphas, including tiny, huge (clamped) and zero ones."""
+    rng = _rng(102)
+    a = (rng.standard_normal(4000) * 10.0 ** rng.uniform(-8, 4, 4000)).astype(np.float32)
+    a[:5] = [0.0, 3.0, -3.0, 2.0 ** -140, 2.0 ** 120]
+    s = np.ones((1, 1, 8 * a.size), dtype=np.int8)
+    _, e1, c2, _ = oracle.pack_apot2(s, a.reshape(1, 1, -1), 8)
+    for k, av in enumerate(a):
+        terms = oracle.additive_pot(float(av), 2)
+        p_raw = math.log2(abs(float(av))) if av != 0 else 0.0
+        if av == 0 or round(p_raw) < oracle.EXP_MIN or round(p_raw) > oracle.EXP_MAX or len(terms) < 2:
+            assert c2[0, 0, k] == 0, (k, av)
+            continue
+        (s1, p1), (s2, p2) = terms
+        if p2 < oracle.EXP_MIN or p1 - p2 > 127:
+            assert c2[0, 0, k] == 0
+            continue
+        assert e1[0, 0, k] == p1 and c2[0, 0, k] == s1 * s2 * (p1 - p2), (k, av, terms, c2[0, 0, k])
+
+
+def test_s10_zero_second_terms_reduce_to_gemm():
+    rng = _rng(103)
+    q, N, K, g = 3, 20, 256, 128
+    planes = rng.integers(0, 256, size=(q, N, K // 8), dtype=np.uint8)
+    e = rng.integers(-6, 6, size=(q, N, K // g)).astype(np.int8)
+    x = _rand_fp16(rng, (2, K))
+    assert np.array_equal(oracle.gemm_apot2(x, planes, e, np.zeros_like(e), g), oracle.gemm(x, planes, e, g))
