@@ -152,6 +152,28 @@ shiftadd_status shiftadd_lut_gemv_colwise(const uint16_t* x, const uint8_t* plan
                                           int layout, int N, int K, int q, uint16_t* y, unsigned flags,
                                           void* stream);
 
+/* NEXT-f2 -- additive PoT with K = 2 terms per scale (Eq. 2: "the k-th
+ * PoT minimizes the residual of the (k-1)-th").
+ *
+ * shiftadd_pack_apot2: as shiftadd_pack (same planes and exps: term 1, P1 = round(log2|a|),
+ *   its sign folded into the bits) plus exps2 (int8, same size and layout permutation as
+ *   exps): the second term relative to the first, c2 = s1*s2*(P1 - P2) with
+ *   P2 = round(log2|a - s1 2^P1|), so a group's folded scale is 2^P1 (1 + sign(c2) 2^-|c2|).
+ *   c2 = 0 when a is 0, P1 was clamped, the residual is 0, P2 < EXP_MIN or P1 - P2 > 127.
+ *
+ * shiftadd_lut_gemm_apot2: y[m][n] = fp16_rne( sum_i sum_G 2^{e_i} (1 + sign(c2) 2^-|c2|)
+ *   sum_{k in G} s(i,n,k) x[m][k] ): each 128-k chunk (tiled) or lookup (canonical) sum p
+ *   adds v1 = p 2^{e1} and sign(c2) v1 2^-|c2| (two exponent adds).  Supported: canonical
+ *   layout, any shape shiftadd_lut_gemm accepts (M <= 16); tiled layout, M = 1, K <= 4096
+ *   (and K <= 8192 up to 12 MB of planes) -- otherwise SHIFTADD_ERR_UNSUPPORTED.  No
+ *   workspace.  flags: 0 or SHIFTADD_FLAG_PDL.  Terms below 2^-126 are flushed to 0. */
+shiftadd_status shiftadd_pack_apot2(const int8_t* signs, const float* alpha, int q, int N, int K, int g,
+                                    int layout, uint8_t* planes, int8_t* exps, int8_t* exps2, int32_t* counts,
+                                    void* stream);
+shiftadd_status shiftadd_lut_gemm_apot2(const uint16_t* x, int ldx, const uint8_t* planes, const int8_t* exps,
+                                        const int8_t* exps2, int layout, int M, int N, int K, int q, int g,
+                                        uint16_t* y, int ldy, unsigned flags, void* stream);
+
 /* Launch geometry the gemm call would use (for measurement/reporting; host only):
  * out[0] = grid CTAs, out[1] = threads per CTA, out[2] = dynamic smem bytes,
  * out[3] = kernel id (0 generic, 1 tiled M=1 split-K, 2 tiled small-batch, 3 tiled M=1

@@ -22,7 +22,7 @@ import torch
 __all__ = [
     "LAYOUT_CANONICAL", "LAYOUT_TILED", "FLAG_PDL", "FLAG_SPLITK", "EXP_ZERO", "ShiftAddError", "lib",
     "PackedLayer", "packed_bytes", "pack", "lut_gemm", "lut_gemv", "workspace_bytes",
-    "gemm_plan", "Workspace", "pack_colwise", "lut_gemv_colwise",
+    "gemm_plan", "Workspace", "pack_colwise", "lut_gemv_colwise", "pack_apot2",
 ]
 
 LAYOUT_CANONICAL = 0
@@ -75,6 +75,11 @@ def lib():
         L.shiftadd_pack_colwise.argtypes = [vp, vp, c_int, c_int, c_int, c_int, vp, vp, vp, vp]
         L.shiftadd_lut_gemv_colwise.restype = c_int
         L.shiftadd_lut_gemv_colwise.argtypes = [vp, vp, vp, c_int, c_int, c_int, c_int, vp, ctypes.c_uint, vp]
+        L.shiftadd_pack_apot2.restype = c_int
+        L.shiftadd_pack_apot2.argtypes = [vp, vp, c_int, c_int, c_int, c_int, c_int, vp, vp, vp, vp, vp]
+        L.shiftadd_lut_gemm_apot2.restype = c_int
+        L.shiftadd_lut_gemm_apot2.argtypes = [vp, c_int, vp, vp, vp, c_int, c_int, c_int, c_int, c_int, c_int,
+                                              vp, c_int, ctypes.c_uint, vp]
         L.shiftadd_gemm_plan.restype = c_int
         L.shiftadd_gemm_plan.argtypes = [c_int] * 6 + [ctypes.POINTER(c_int * 4)]
         v = L.shiftadd_abi_version()
@@ -122,6 +127,7 @@ class PackedLayer:
     counts: torch.Tensor      # int32[2] on device: clamped exponents, invalid inputs
     _ws_bytes: dict = field(default_factory=dict, repr=False)   # M -> workspace bytes
     colwise: bool = False     # NEXT-f1: exps is exps_col [q][K] (column-wise scales)
+    exps2: torch.Tensor | None = None   # NEXT-f2: second additive-PoT term codes (like exps)
 
     @property
     def device(self):
@@ -156,6 +162,34 @@ def pack(signs: torch.Tensor, alpha: torch.Tensor, g: int, layout: int = LAYOUT_
                                  _ptr(counts), _stream_ptr(stream, dev))
     _check(st, "shiftadd_pack")
     return PackedLayer(planes, exps, q, N, K, g, layout, counts)
+
+
+def pack_apot2(signs: torch.Tensor, alpha: torch.Tensor, g: int, layout: int = LAYOUT_TILED,
+               stream=None) -> PackedLayer:
+    """NEXT-f2: as ``pack`` plus the second additive-PoT term of every scale (K = 2,
+    Eq. 2) in ``exps2`` (shiftadd_pack_apot2)."""
+    if signs.dtype != torch.int8 or alpha.dtype != torch.float32:
+        raise TypeError("signs must be int8 and alpha float32")
+    if not (signs.is_cuda and alpha.is_cuda):
+        raise ValueError("pack_apot2 runs on the GPU; pass CUDA tensors")
+    if signs.dim() != 3 or alpha.dim() != 3:
+        raise ValueError("signs [q][N][K], alpha [q][N][K/g]")
+    q, N, K = signs.shape
+    if tuple(alpha.shape) != (q, N, K // g if g else 0):
+        raise ValueError("alpha must be [q][N][K/g]")
+    signs = signs.contiguous()
+    alpha = alpha.contiguous()
+    pb, eb = packed_bytes(layout, q, N, K, g)
+    dev = signs.device
+    planes = torch.empty(pb, dtype=torch.uint8, device=dev)
+    exps = torch.empty(eb, dtype=torch.int8, device=dev)
+    exps2 = torch.empty(eb, dtype=torch.int8, device=dev)
+    counts = torch.zeros(2, dtype=torch.int32, device=dev)
+    with torch.cuda.device(dev):
+        st = lib().shiftadd_pack_apot2(_ptr(signs), _ptr(alpha), q, N, K, g, layout, _ptr(planes), _ptr(exps),
+                                       _ptr(exps2), _ptr(counts), _stream_ptr(stream, dev))
+    _check(st, "shiftadd_pack_apot2")
+    return PackedLayer(planes, exps, q, N, K, g, layout, counts, exps2=exps2)
 
 
 def pack_colwise(signs: torch.Tensor, alpha_col: torch.Tensor, layout: int = LAYOUT_TILED,
@@ -262,6 +296,22 @@ def lut_gemm(x: torch.Tensor, layer: PackedLayer, out: torch.Tensor | None = Non
         out = torch.empty((M, layer.N), dtype=torch.float16, device=dev)
     if out.dtype != torch.float16 or out.dim() != 2 or out.shape[0] != M or out.stride(-1) != 1:
         raise ValueError("out must be fp16 [M][>=N] with unit column stride")
+    if layer.colwise:
+        if M != 1:
+            raise ShiftAddError("column-wise layers: batch-1 only (shiftadd_lut_gemv_colwise)")
+        lut_gemv_colwise(x2[0], layer, out=out[0], pdl=pdl, stream=stream)
+        return out[0] if squeeze else out
+    if layer.exps2 is not None:
+        if torch.cuda.current_device() != dev.index:
+            torch.cuda.set_device(dev)
+        sptr = (stream if stream is not None else torch.cuda.current_stream(dev)).cuda_stream
+        st = lib().shiftadd_lut_gemm_apot2(x2.data_ptr(), x2.stride(0), layer.planes.data_ptr(),
+                                           layer.exps.data_ptr(), layer.exps2.data_ptr(), layer.layout, M,
+                                           layer.N, layer.K, layer.q, layer.g, out.data_ptr(), out.stride(0),
+                                           FLAG_PDL if pdl else 0, sptr)
+        if st:
+            _check(st, "shiftadd_lut_gemm_apot2")
+        return out[0] if squeeze else out
     need = layer._ws_bytes.get(M)
     if need is None:
         need = layer._ws_bytes[M] = workspace_bytes(layer, M)

@@ -194,6 +194,61 @@ shiftadd_status shiftadd_lut_gemv_colwise(const uint16_t* x, const uint8_t* plan
   return SHIFTADD_OK;
 }
 
+shiftadd_status shiftadd_pack_apot2(const int8_t* signs, const float* alpha, int q, int N, int K, int g,
+                                    int layout, uint8_t* planes, int8_t* exps, int8_t* exps2, int32_t* counts,
+                                    void* stream) {
+  if (!exps2) return fail(SHIFTADD_ERR_INVALID, "null pointer argument");
+  const shiftadd_status st = shiftadd_pack(signs, alpha, q, N, K, g, layout, planes, exps, counts, stream);
+  if (st != SHIFTADD_OK) return st;
+  const cudaError_t e = launch_pack_apot2(alpha, q, N, K, g, layout, exps2, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "pack_apot2 launch");
+  return SHIFTADD_OK;
+}
+
+shiftadd_status shiftadd_lut_gemm_apot2(const uint16_t* x, int ldx, const uint8_t* planes, const int8_t* exps,
+                                        const int8_t* exps2, int layout, int M, int N, int K, int q, int g,
+                                        uint16_t* y, int ldy, unsigned flags, void* stream) {
+  if (!x || !planes || !exps || !exps2 || !y) return fail(SHIFTADD_ERR_INVALID, "null pointer argument");
+  shiftadd_status st = check_shape(q, N, K, g, 4);
+  if (st != SHIFTADD_OK) return st;
+  if ((st = check_layout(layout, K, g)) != SHIFTADD_OK) return st;
+  if (M < 1) return fail(SHIFTADD_ERR_INVALID, "M=%d < 1", M);
+  if (M > 16) return fail(SHIFTADD_ERR_UNSUPPORTED, "M=%d > 16", M);
+  if (ldx < K || ldy < N) return fail(SHIFTADD_ERR_INVALID, "ldx=%d < K=%d or ldy=%d < N=%d", ldx, K, ldy, N);
+  if (flags & ~SHIFTADD_FLAG_PDL) return fail(SHIFTADD_ERR_INVALID, "unknown flags 0x%x", flags);
+  if (!aligned(x, 16) || (M > 1 && (ldx % 8)) || !aligned(planes, 16) || !aligned(y, 2))
+    return fail(SHIFTADD_ERR_INVALID, "misaligned pointer (x rows and planes need 16 B)");
+  if (layout == SHIFTADD_LAYOUT_TILED && M != 1)
+    return fail(SHIFTADD_ERR_UNSUPPORTED, "additive-PoT-2 tiled path is batch-1 (use the canonical layout)");
+  DevInfo di;
+  if ((st = device_info(&di)) != SHIFTADD_OK) return st;
+  if (layout == SHIFTADD_LAYOUT_TILED && !cluster_applicable(N, K, q, di.sms))
+    return fail(SHIFTADD_ERR_UNSUPPORTED, "additive-PoT-2 tiled path: K=%d N=%d q=%d outside the cluster kernel", K,
+                N, q);
+  GemmArgs a;
+  a.x = reinterpret_cast<const __half*>(x);
+  a.ldx = ldx;
+  a.planes = planes;
+  a.exps = exps;
+  a.exps2 = exps2;
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.q = q;
+  a.g = g;
+  a.y = reinterpret_cast<__half*>(y);
+  a.ldy = ldy;
+  a.workspace = nullptr;
+  a.workspace_bytes = 0;
+  a.flags = flags;
+  a.stream = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  if (layout == SHIFTADD_LAYOUT_CANONICAL) e = launch_gemm_generic(a, plan_generic(M, N, K, q, g, di.sms));
+  else e = launch_gemv_cluster(a, plan_gemv_cluster(N, K, q, di.sms));
+  if (e != cudaSuccess) return cuda_fail(e, "lut_gemm_apot2 launch");
+  return SHIFTADD_OK;
+}
+
 size_t shiftadd_workspace_bytes(int layout, int M, int N, int K, int q, int g) {
   if (check_shape(q, N, K, g, 4) != SHIFTADD_OK || check_layout(layout, K, g) != SHIFTADD_OK) return 0;
   if (M < 1 || M > 16) return 0;

@@ -90,6 +90,19 @@ __device__ __forceinline__ float shift_pow2(float p, int e) {
   return (e == -128) ? 0.f : __uint_as_float(r);
 }
 
+// NEXT-f2 -- the second additive-PoT term (Eq. 2 with K = 2): given
+// v1 = p * 2^{e1} and the code c2 = s1*s2*(P1 - P2), returns sign(c2) * v1 * 2^{-|c2|}
+// (= s1 s2 p 2^{P2}): an exponent-field subtract.  c2 == 0 -> 0; Inf/NaN pass through; a
+// result below the fp32 normal range (|.| < 2^-126) is flushed to 0 (reading R20).
+__device__ __forceinline__ float shift_apot2(float v1, int c2) {
+  const int d = c2 < 0 ? -c2 : c2;
+  const uint32_t b = __float_as_uint(v1);
+  const int ex = (int)((b >> 23) & 0xffu);
+  float r = (ex == 255) ? v1 : (ex > d ? __uint_as_float(b - ((uint32_t)d << 23)) : 0.f);
+  r = c2 < 0 ? -r : r;
+  return c2 == 0 ? 0.f : r;
+}
+
 // Programmatic dependent launch (sm_90+): wait for the upstream grid before touching
 // anything it may produce or consume (x, y, workspace); let dependents start early.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
@@ -163,6 +176,7 @@ struct GemmArgs {
   int ldx;
   const uint8_t* planes;
   const int8_t* exps;
+  const int8_t* exps2 = nullptr;   // NEXT-f2 second additive-PoT term codes (same layout as exps)
   int M, N, K, q, g;
   __half* y;
   int ldy;
@@ -184,6 +198,8 @@ cudaError_t launch_pack(const int8_t* signs, const float* alpha, int q, int N, i
                         int layout, uint8_t* planes, int8_t* exps, int32_t* counts,
                         cudaStream_t stream);
 
+cudaError_t launch_pack_apot2(const float* alpha, int q, int N, int K, int g, int layout, int8_t* exps2,
+                              cudaStream_t stream);
 cudaError_t launch_pack_colwise(const int8_t* signs, const float* alpha_col, int q, int N, int K,
                                 int layout, uint8_t* planes, int8_t* exps_col, int32_t* counts,
                                 cudaStream_t stream);

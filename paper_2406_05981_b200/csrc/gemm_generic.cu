@@ -9,7 +9,8 @@
 // 32 different LUT columns, so the lookups are bank-conflict free by construction --
 // shifts the queried partial sum by its group exponent (a4), and reduces
 // the warp with a fixed shuffle tree (a5).  Results accumulate in shared memory and are
-// stored as fp16 (RNE) at the end: deterministic, no workspace.
+// stored as fp16 (RNE) at the end: deterministic, no workspace.  With exps2 (NEXT-f2) each
+// shifted partial sum also adds its second additive-PoT term (shift_apot2).
 #include "common.cuh"
 
 namespace shiftadd {
@@ -21,8 +22,8 @@ constexpr int kMaxM = 16;
 
 __global__ void __launch_bounds__(kWarps * 32)
 gemm_generic_kernel(const __half* __restrict__ x, int ldx, const uint8_t* __restrict__ planes,
-                    const int8_t* __restrict__ exps, int M, int N, int K, int q, int g,
-                    __half* __restrict__ y, int ldy) {
+                    const int8_t* __restrict__ exps, const int8_t* __restrict__ exps2, int M, int N,
+                    int K, int q, int g, __half* __restrict__ y, int ldy) {
   __shared__ float lut[256 * 32];          // word (key, t) = key*32 + t
   __shared__ float acc[kMaxM * kRows];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -68,7 +69,9 @@ gemm_generic_kernel(const __half* __restrict__ x, int ldx, const uint8_t* __rest
             const size_t row = (size_t)i * N + n;
             const uint32_t key = __ldg(planes + row * KB + s0 + lane);
             const int e = __ldg(exps + row * KG + k0 / g);
-            v += shift_pow2(lut[key * 32 + lane], e);
+            const float v1 = shift_pow2(lut[key * 32 + lane], e);
+            v += v1;
+            if (exps2) v += shift_apot2(v1, __ldg(exps2 + row * KG + k0 / g));   // NEXT-f2
           }
         }
         // a5: fixed-order butterfly over the 32 columns.
@@ -93,8 +96,8 @@ LaunchPlan plan_generic(int M, int N, int K, int q, int g, int sms) {
 }
 
 cudaError_t launch_gemm_generic(const GemmArgs& a, const LaunchPlan& p) {
-  gemm_generic_kernel<<<p.grid, p.threads, 0, a.stream>>>(a.x, a.ldx, a.planes, a.exps, a.M, a.N,
-                                                           a.K, a.q, a.g, a.y, a.ldy);
+  gemm_generic_kernel<<<p.grid, p.threads, 0, a.stream>>>(a.x, a.ldx, a.planes, a.exps, a.exps2, a.M,
+                                                           a.N, a.K, a.q, a.g, a.y, a.ldy);
   return cudaGetLastError();
 }
 

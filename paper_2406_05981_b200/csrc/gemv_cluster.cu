@@ -183,8 +183,9 @@ __host__ __device__ constexpr uint32_t step_sel_c(int j) {
   return (6u << 12) | (7u << 8) | ((uint32_t)(j & 3) << 4) | (4u + (j & 1));
 }
 
-template <int Q, uint32_t IMM>
-__device__ __forceinline__ float unit_dot_c(const uint4 (&w)[Q], const int (&e)[Q], const uint32_t (&cst)[8]) {
+template <int Q, uint32_t IMM, bool AP2 = false>
+__device__ __forceinline__ float unit_dot_c(const uint4 (&w)[Q], const int (&e)[Q], const int (&e2)[Q],
+                                            const uint32_t (&cst)[8]) {
   float acc = 0.f;
 #pragma unroll
   for (int i = 0; i < Q; ++i) {
@@ -195,7 +196,8 @@ __device__ __forceinline__ float unit_dot_c(const uint4 (&w)[Q], const int (&e)[
       const float v = lds_f32(IMM + prmt(word, cst[j >> 1], step_sel_c(j)));
       if (j & 1) p1 += v; else p0 += v;
     }
-    acc += shift_pow2(p0 + p1, e[i]);
+    const float v1 = shift_pow2(p0 + p1, e[i]);
+    acc += AP2 ? v1 + shift_apot2(v1, e2[i]) : v1;   // NEXT-f2: second additive-PoT term
   }
   return acc;
 }
@@ -232,6 +234,10 @@ __device__ __forceinline__ void load_planes_unit(const uint4* __restrict__ plane
 __host__ __device__ constexpr int cl_ring_colw(int Q, int REGS) {
   return (REGS - 56) / (4 * Q) < 1 ? 1 : ((REGS - 56) / (4 * Q) > 8 ? 8 : (REGS - 56) / (4 * Q));
 }
+// additive PoT K = 2: one more exponent register per plane per slot
+__host__ __device__ constexpr int cl_ring_ap2(int Q, int REGS) {
+  return (REGS - 56) / (6 * Q) < 1 ? 1 : ((REGS - 56) / (6 * Q) > 8 ? 8 : (REGS - 56) / (6 * Q));
+}
 __host__ __device__ constexpr int cl_ring(int Q, int REGS) {
   return (REGS - 56) / (5 * Q) < 1 ? 1 : ((REGS - 56) / (5 * Q) > 8 ? 8 : (REGS - 56) / (5 * Q));
 }
@@ -250,12 +256,13 @@ struct Cursor {
 
 constexpr int kFlagPdl = 1, kFlagXFirst = 2, kFlagBarrierTail = 4;
 
-template <int Q, int SCM, int NW, int REGS, bool COLW>
+template <int Q, int SCM, int NW, int REGS, bool COLW, bool AP2 = false>
 __global__ void __launch_bounds__(NW * 32) __maxnreg__(REGS)
 gemv_cluster_kernel(const __half* __restrict__ x, const uint4* __restrict__ planes,
                     const int8_t* __restrict__ exps, int N, int S, int RG, int C, __half* __restrict__ y,
-                    int flags, unsigned long long* __restrict__ trace) {
-  constexpr int D = COLW ? cl_ring_colw(Q, REGS) : cl_ring(Q, REGS);
+                    int flags, unsigned long long* __restrict__ trace, const int8_t* __restrict__ exps2) {
+  constexpr int D = COLW ? cl_ring_colw(Q, REGS) : (AP2 ? cl_ring_ap2(Q, REGS) : cl_ring(Q, REGS));
+  static_assert(!(COLW && AP2), "column-wise and additive-PoT-2 layers are separate formats");
   static_assert(!COLW || (SCM == 4 && Q <= 4), "column-wise: one LUT slot per plane");
   const bool pdl = flags & kFlagPdl;
   if (threadIdx.x == 0) check_dyn_base();
@@ -297,6 +304,13 @@ gemv_cluster_kernel(const __half* __restrict__ x, const uint4* __restrict__ plan
   Cursor pc = ld;
   uint4 w[D][Q];
   int e[D][Q];
+  int e2[D][Q];
+  auto load_e2 = [&](long long u, int k) {
+    if (AP2) {
+#pragma unroll
+      for (int i = 0; i < Q; ++i) e2[k][i] = ldg_s8_stream(exps2 + (u * Q + i) * 32 + lane, pol_stream);
+    }
+  };
   auto stage_x = [&]() {
     if (xthread) {
       const uint4 xv = ldg_keep(xsrc, pol_keep);
@@ -311,6 +325,7 @@ gemv_cluster_kernel(const __half* __restrict__ x, const uint4* __restrict__ plan
       if (k < Mw) {
         if (COLW) load_planes_unit<Q>(planes, (long long)(s0 + ld.t) * RG + rg0 + ld.rgl, lane, pol_stream, w[k]);
         else load_unit<Q>(planes, exps, (long long)(s0 + ld.t) * RG + rg0 + ld.rgl, lane, pol_stream, w[k], e[k]);
+        load_e2((long long)(s0 + ld.t) * RG + rg0 + ld.rgl, k);
         ld.advance<NW>(RGb);
       }
   };
@@ -357,13 +372,14 @@ gemv_cluster_kernel(const __half* __restrict__ x, const uint4* __restrict__ plan
       if (COLW) {
         v = unit_dot_colw<Q>(w[k], cstE, cstO);
       } else if (SCM <= 2) {
-        v = (pc.t & 1) ? unit_dot_c<Q, kDynBase>(w[k], e[k], cstO) : unit_dot_c<Q, kDynBase>(w[k], e[k], cstE);
+        v = (pc.t & 1) ? unit_dot_c<Q, kDynBase, AP2>(w[k], e[k], e2[k], cstO)
+                       : unit_dot_c<Q, kDynBase, AP2>(w[k], e[k], e2[k], cstE);
       } else {
         switch (pc.t) {   // slot t: slab t >> 1 (LDS immediate), half t & 1 (constant set)
-          case 0: v = unit_dot_c<Q, kDynBase>(w[k], e[k], cstE); break;
-          case 1: v = unit_dot_c<Q, kDynBase>(w[k], e[k], cstO); break;
-          case 2: v = unit_dot_c<Q, kDynBase + kLutBytes>(w[k], e[k], cstE); break;
-          default: v = unit_dot_c<Q, kDynBase + kLutBytes>(w[k], e[k], cstO); break;
+          case 0: v = unit_dot_c<Q, kDynBase, AP2>(w[k], e[k], e2[k], cstE); break;
+          case 1: v = unit_dot_c<Q, kDynBase, AP2>(w[k], e[k], e2[k], cstO); break;
+          case 2: v = unit_dot_c<Q, kDynBase + kLutBytes, AP2>(w[k], e[k], e2[k], cstE); break;
+          default: v = unit_dot_c<Q, kDynBase + kLutBytes, AP2>(w[k], e[k], e2[k], cstO); break;
         }
       }
       v += __shfl_xor_sync(0xffffffffu, v, 1);
@@ -372,6 +388,7 @@ gemv_cluster_kernel(const __half* __restrict__ x, const uint4* __restrict__ plan
       if (m + D < Mw) {
         if (COLW) load_planes_unit<Q>(planes, (long long)(s0 + ld.t) * RG + rg0 + ld.rgl, lane, pol_stream, w[k]);
         else load_unit<Q>(planes, exps, (long long)(s0 + ld.t) * RG + rg0 + ld.rgl, lane, pol_stream, w[k], e[k]);
+        load_e2((long long)(s0 + ld.t) * RG + rg0 + ld.rgl, k);
         ld.advance<NW>(RGb);
       }
     }
@@ -454,15 +471,15 @@ ClusterShape cluster_shape(int N, int K, int q) {
 int variant_threads(int v) { return v == kHalf ? 8 * 32 : 16 * 32; }
 int variant_smem(int v) { return v == kFull4 ? Smem<4>::total : Smem<2>::total; }
 
-template <int Q, int SCM, int NW, int REGS, bool COLW = false>
+template <int Q, int SCM, int NW, int REGS, bool COLW = false, bool AP2 = false>
 cudaError_t set_attrs() {
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
   std::call_once(once, [] {
-    err = cudaFuncSetAttribute(gemv_cluster_kernel<Q, SCM, NW, REGS, COLW>,
+    err = cudaFuncSetAttribute(gemv_cluster_kernel<Q, SCM, NW, REGS, COLW, AP2>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<SCM>::total);
     if (err == cudaSuccess && COLW)
-      err = cudaFuncSetAttribute(gemv_cluster_kernel<Q, SCM, NW, REGS, COLW>,
+      err = cudaFuncSetAttribute(gemv_cluster_kernel<Q, SCM, NW, REGS, COLW, AP2>,
                                  cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   });
   return err;
@@ -514,9 +531,9 @@ int barrier_tail() {
   return v;
 }
 
-template <int Q, int SCM, int NW, int REGS, bool COLW = false>
+template <int Q, int SCM, int NW, int REGS, bool COLW = false, bool AP2 = false>
 cudaError_t launch_cluster_q(const GemmArgs& a, const LaunchPlan& p, int C) {
-  const cudaError_t ae = set_attrs<Q, SCM, NW, REGS, COLW>();
+  const cudaError_t ae = set_attrs<Q, SCM, NW, REGS, COLW, AP2>();
   if (ae != cudaSuccess) return ae;
   const int S = a.K / kTileK;
   const int RG = (a.N + kTileRows - 1) / kTileRows;
@@ -539,17 +556,18 @@ cudaError_t launch_cluster_q(const GemmArgs& a, const LaunchPlan& p, int C) {
   if (cluster_trace() && a.workspace && a.workspace_bytes >= kCounterBytes + (size_t)p.grid * 256)
     trace = reinterpret_cast<unsigned long long*>(static_cast<char*>(a.workspace) + kCounterBytes);
   const int flags = (pdl ? kFlagPdl : 0) | (x_first() ? kFlagXFirst : 0) | (barrier_tail() ? kFlagBarrierTail : 0);
-  return cudaLaunchKernelEx(&c, gemv_cluster_kernel<Q, SCM, NW, REGS, COLW>, a.x,
-                            reinterpret_cast<const uint4*>(a.planes), a.exps, a.N, S, RG, C, a.y, flags, trace);
+  return cudaLaunchKernelEx(&c, gemv_cluster_kernel<Q, SCM, NW, REGS, COLW, AP2>, a.x,
+                            reinterpret_cast<const uint4*>(a.planes), a.exps, a.N, S, RG, C, a.y, flags, trace,
+                            a.exps2);
 }
 
-template <int SCM, int NW>
+template <int SCM, int NW, bool AP2 = false>
 cudaError_t launch_cluster_v(const GemmArgs& a, const LaunchPlan& p, int C) {
   switch (a.q) {
-    case 1: return launch_cluster_q<1, SCM, NW, 128>(a, p, C);
-    case 2: return launch_cluster_q<2, SCM, NW, 128>(a, p, C);
-    case 3: return launch_cluster_q<3, SCM, NW, 128>(a, p, C);
-    case 4: return launch_cluster_q<4, SCM, NW, 128>(a, p, C);
+    case 1: return launch_cluster_q<1, SCM, NW, 128, false, AP2>(a, p, C);
+    case 2: return launch_cluster_q<2, SCM, NW, 128, false, AP2>(a, p, C);
+    case 3: return launch_cluster_q<3, SCM, NW, 128, false, AP2>(a, p, C);
+    case 4: return launch_cluster_q<4, SCM, NW, 128, false, AP2>(a, p, C);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -616,6 +634,8 @@ cudaError_t launch_gemv_colwise(const GemmArgs& a) {
 
 cudaError_t launch_gemv_cluster(const GemmArgs& a, const LaunchPlan& p) {
   const ClusterShape cs = cluster_shape(a.N, a.K, a.q);
+  if (a.exps2)   // NEXT-f2: additive PoT K = 2 (16-warp variants only)
+    return cs.sc <= 2 ? launch_cluster_v<2, 16, true>(a, p, cs.C) : launch_cluster_v<4, 16, true>(a, p, cs.C);
   switch (cs.variant) {
     case kHalf: return launch_cluster_v<2, 8>(a, p, cs.C);
     case kFull2: return launch_cluster_v<2, 16>(a, p, cs.C);

@@ -149,6 +149,50 @@ __global__ void pack_exps_tiled_kernel(const float* __restrict__ alpha, int q, i
   }
 }
 
+// NEXT-f2: the second additive-PoT term code of one scale (R19): term 1 is the
+// pot_exponent above (sign folded into the bits); r1 = alpha - s1 2^P1 is exact in fp32
+// (Sterbenz: |alpha| / 2^P1 in [2^-0.5, 2^0.5)); c2 = s1 s2 (P1 - P2) with P2 the unclamped
+// round(log2|r1|); 0 if alpha is 0/Inf/NaN, P1 was clamped, r1 == 0, P2 < EXP_MIN or
+// P1 - P2 > 127.
+__device__ __forceinline__ int apot2_code(float alpha) {
+  int clamped, invalid;
+  const int e1 = pot_exponent(alpha, &clamped, &invalid);
+  if (invalid || clamped || e1 == SHIFTADD_EXP_ZERO) return 0;
+  const float t1 = __int_as_float((e1 + 127) << 23);
+  const float r1 = alpha < 0.f ? alpha + t1 : alpha - t1;
+  const uint32_t u = __float_as_uint(r1) & 0x7fffffffu;
+  if (u == 0u) return 0;
+  const int ef = (int)(u >> 23);
+  if (ef == 0) return 0;                                    // subnormal: P2 < -126
+  const int e2 = ef - 127 + ((u & 0x7fffffu) >= 0x3504F4u ? 1 : 0);
+  const int d = e1 - e2;
+  if (e2 < SHIFTADD_EXP_MIN || d > 127) return 0;
+  const bool neg = (alpha < 0.f) != (r1 < 0.f);
+  return neg ? -d : d;
+}
+
+__global__ void pack_apot2_kernel(const float* __restrict__ alpha, int q, int N, int K, int g, int layout, int RG,
+                                  long long count, int8_t* __restrict__ exps2) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x; o < count; o += stride) {
+    long long src;
+    if (layout == SHIFTADD_LAYOUT_CANONICAL) {
+      src = o;
+    } else {   // tiled: same permutation as pack_exps_tiled_kernel
+      const int h = (int)(o & 1);
+      const int r = (int)((o >> 1) & 15);
+      const long long t = o >> 5;
+      const int i = (int)(t % q);
+      const long long sr = t / q;
+      const int rg = (int)(sr % RG);
+      const int s = (int)(sr / RG);
+      const int n = rg * kTileRows + r;
+      src = n < N ? ((long long)i * N + n) * (K / g) + (s * kTileK + h * 128) / g : -1;
+    }
+    exps2[o] = (int8_t)(src < 0 ? 0 : apot2_code(__ldg(alpha + src)));
+  }
+}
+
 int grid_for(long long work, int threads) {
   long long b = (work + threads - 1) / threads;
   if (b > 148LL * 32) b = 148LL * 32;
@@ -174,6 +218,16 @@ cudaError_t launch_pack(const int8_t* signs, const float* alpha, int q, int N, i
     const long long ne = (long long)(K / kTileK) * RG * q * kTileExps;
     pack_exps_tiled_kernel<<<grid_for(ne, threads), threads, 0, stream>>>(alpha, q, N, K, g, RG, ne, exps);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_apot2(const float* alpha, int q, int N, int K, int g, int layout, int8_t* exps2,
+                              cudaStream_t stream) {
+  const int threads = 256;
+  const int RG = (N + kTileRows - 1) / kTileRows;
+  const long long count = layout == SHIFTADD_LAYOUT_CANONICAL ? (long long)q * N * (K / g)
+                                                              : (long long)(K / kTileK) * RG * q * kTileExps;
+  pack_apot2_kernel<<<grid_for(count, threads), threads, 0, stream>>>(alpha, q, N, K, g, layout, RG, count, exps2);
   return cudaGetLastError();
 }
 

@@ -141,3 +141,11 @@ def test_colwise_validation_happens_before_any_launch(L):
     assert L.shiftadd_lut_gemv_colwise(p, p, p, 0, 16, 256, 3, p, 0, None) == 6
     assert L.shiftadd_lut_gemv_colwise(p, p, p, 1, 16, 256, 3, p, 8, None) == 2
     assert b"flags" in L.shiftadd_last_error()
+
+
+def test_apot2_validation_happens_before_any_launch(L):
+    _r1, p = _buf(1 << 16)
+    assert L.shiftadd_pack_apot2(p, p, 3, 16, 256, 128, 1, p, p, None, None, None) == 2
+    assert L.shiftadd_lut_gemm_apot2(p, 512, p, p, None, 1, 1, 64, 512, 3, 128, p, 64, 0, None) == 2
+    assert L.shiftadd_lut_gemm_apot2(p, 512, p, p, p, 1, 2, 64, 512, 3, 128, p, 64, 0, None) == 6
+    assert L.shiftadd_lut_gemm_apot2(p, 512, p, p, p, 1, 1, 64, 512, 3, 128, p, 64, 2, None) == 2

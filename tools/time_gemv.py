@@ -16,6 +16,7 @@ ap.add_argument("shapes", nargs="+")
 ap.add_argument("--pdl", action="store_true")
 ap.add_argument("--splitk", action="store_true")
 ap.add_argument("--colwise", action="store_true", help="NEXT-f1 column-wise scales (M = 1)")
+ap.add_argument("--apot2", action="store_true", help="NEXT-f2 additive PoT, K = 2 terms")
 ap.add_argument("--m", type=int, default=1)
 ap.add_argument("--reps", type=int, default=200)
 a = ap.parse_args()
@@ -24,7 +25,7 @@ l2 = torch.cuda.get_device_properties(dev).L2_cache_size
 peak = 6550.7
 for spec in a.shapes:
     N, K, q = map(int, spec.split(":"))
-    lb = q * N * K // 8 + (q * K if a.colwise else q * N * K // 128)
+    lb = q * N * K // 8 + (q * K if a.colwise else (2 if a.apot2 else 1) * q * N * K // 128)
     R = max(2, -(-4 * l2 // lb))
     copies = []
     for r in range(R):
@@ -32,6 +33,9 @@ for spec in a.shapes:
             if a.colwise:
                 signs, alpha = synth.gen_layer_colwise(q, N, K, seed=synth.seed_for(1, 0, r), device=dev)
                 copies.append(sa.pack_colwise(signs, alpha))
+            elif a.apot2:
+                signs, alpha = synth.gen_layer(q, N, K, 128, seed=synth.seed_for(1, 0, r), device=dev)
+                copies.append(sa.pack_apot2(signs, alpha, 128, layout=sa.LAYOUT_TILED))
             else:
                 signs, alpha = synth.gen_layer(q, N, K, 128, seed=synth.seed_for(1, 0, r), device=dev)
                 copies.append(sa.pack(signs, alpha, 128, layout=sa.LAYOUT_TILED))
@@ -39,7 +43,8 @@ for spec in a.shapes:
         else:
             base = copies[r % 2]
             copies.append(sa.PackedLayer(base.planes.clone(), base.exps.clone(), q, N, K, base.g, base.layout,
-                                         base.counts, colwise=base.colwise))
+                                         base.counts, colwise=base.colwise,
+                                         exps2=None if base.exps2 is None else base.exps2.clone()))
     x = synth.gen_x(a.m, K, seed=1, device=dev)
     y = torch.empty((a.m, N), dtype=torch.float16, device=dev)
     ws = sa.Workspace(dev)
@@ -73,7 +78,7 @@ for spec in a.shapes:
     us = e0.elapsed_time(e1) / a.reps * 1e3
     tot = lb + 2 * a.m * K + 2 * a.m * N
     print("N=%6d K=%6d q=%d M=%2d  %8.2f us  %7.1f GB/s  frac %.3f  (R=%d, %s)" % (
-        N, K, q, a.m, us, tot / us * 1e-3, tot / us * 1e-3 / peak, R, "colwise" if a.colwise else "rowwise g=128"),
+        N, K, q, a.m, us, tot / us * 1e-3, tot / us * 1e-3 / peak, R, "colwise" if a.colwise else ("apot2 g=128" if a.apot2 else "rowwise g=128")),
         flush=True)
     del copies, g
     torch.cuda.empty_cache()
