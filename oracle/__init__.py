@@ -26,6 +26,11 @@ Parity status per function (see DESIGN.md §"Oracle pins"):
   additive_pot / pack_apot2 / dequant_apot2 / gemm_apot2  (NEXT-f2)
                     pinned  (S10: SPEC.md:209-211 worked values, exact two-term scales,
                     residual non-increasing, K=2 error <= K=1 error, c2 = 0 reduces to gemm)
+  pot_round_exact / bcq_greedy / bcq_ls / bcq_bs_codes / bcq_quantize  (NEXT-f4)
+                    pinned  (S11: SPEC.md:107-168 worked values; q = 1 analytic optimum vs
+                    brute force over all sign patterns; LS normal equations; BS nearest level
+                    by enumeration incl. tie-breaks; alternating monotonicity; exact recovery
+                    of a representable w)
 """
 
 from .ref import *  # noqa: F401,F403

@@ -45,7 +45,8 @@ __all__ = [
     "lut_gemm", "to_fp16", "err_floor", "err_normwise", "packed_bytes",
     "algorithmic_bytes", "tile_planes", "pack_colwise", "dequant_colwise", "gemm_colwise",
     "lut_gemm_colwise", "algorithmic_bytes_colwise", "additive_pot", "pack_apot2",
-    "dequant_apot2", "gemm_apot2",
+    "dequant_apot2", "gemm_apot2", "pot_round_exact", "bcq_greedy", "bcq_ls", "bcq_bs_codes",
+    "bcq_quantize",
 ]
 
 
@@ -485,6 +486,93 @@ def gemm_apot2(x, planes, exps, exps2, g, row_chunk=2048):
         n1 = min(n, n0 + row_chunk)
         y[:, n0:n1] = xf @ dequant_apot2(p[:, n0:n1], exps[:, n0:n1], exps2[:, n0:n1], g, K).T
     return y
+
+
+# ------------------------------------------- NEXT-f4: Alg. 1 alternating multi-bit BCQ
+# greedy init (Eq. 1, Line 4), then T cycles of least-squares scale refit
+# (Line 6) and binary-search code refit (Line 7); scales projected to PoT "during the
+# alternating optimization cycles".  Per scale group (a row's g
+# consecutive weights), fp64.  Readings R21-R23.
+def pot_round_exact(a):
+    """sign(a) 2^round(log2|a|) for an fp64 scalar, by exact rational comparison (no log):
+    P = floor(log2|a|) + (|a|^2 >= 2^(2 floor + 1)).  0 -> 0."""
+    a = float(a)
+    if a == 0.0:
+        return 0.0
+    m, e = math.frexp(abs(a))            # |a| = m 2^e, m in [0.5, 1)
+    p = e - 1                             # floor(log2|a|)
+    if Fraction(abs(a)) ** 2 >= Fraction(2) ** (2 * p + 1):
+        p += 1
+    return math.copysign(math.ldexp(1.0, p), a)
+
+
+def bcq_greedy(w, q):
+    """Eq. 1 on one group vector w (fp64): r_0 = w; b_i = sign(r_{i-1}) (sign(0) = +1, R21),
+    alpha_i = r_{i-1}^T b_i / n; r_i = r_{i-1} - alpha_i b_i.  Returns (alpha [q], B [q][n])."""
+    r = np.asarray(w, dtype=np.float64).copy()
+    n = r.size
+    alpha = np.zeros(q)
+    B = np.zeros((q, n))
+    for i in range(q):
+        b = np.where(r >= 0, 1.0, -1.0)
+        alpha[i] = float(np.dot(r, b)) / n
+        B[i] = b
+        r = r - alpha[i] * b
+    return alpha, B
+
+
+def bcq_ls(B, w):
+    """Line 6: alpha = (B^T B)^-1 B^T w with B = [b_1..b_q] as columns; the Gram matrix gets
+    1e-8 * n on its diagonal (reading R22).  numpy.linalg.solve (LAPACK)."""
+    B = np.asarray(B, dtype=np.float64)
+    n = B.shape[1]
+    G = B @ B.T + 1e-8 * n * np.eye(B.shape[0])
+    return np.linalg.solve(G, B @ np.asarray(w, dtype=np.float64))
+
+
+def bcq_bs_codes(alpha, w):
+    """Line 7: each w_j takes the representable level sum_i c_i alpha_i (c in {-1,1}^q)
+    nearest to it; ties -> smaller |level|, then the negative level (R23).
+    Exhaustive over the 2^q levels (the binary search of the paper finds the same level).
+    Returns B [q][n]."""
+    a = np.asarray(alpha, dtype=np.float64)
+    q = a.size
+    codes = np.array([[1.0 if (c >> i) & 1 else -1.0 for i in range(q)] for c in range(1 << q)])  # [2^q][q]
+    levels = codes @ a
+    wv = np.asarray(w, dtype=np.float64)
+    dist = np.abs(wv[:, None] - levels[None, :])                    # [n][2^q]
+    key = np.stack([dist, np.abs(levels)[None, :].repeat(wv.size, 0), levels[None, :].repeat(wv.size, 0)])
+    # lexicographic argmin over (distance, |level|, level)
+    order = np.lexsort((key[2], key[1], key[0]), axis=1)
+    best = order[:, 0]
+    return codes[best].T.copy()
+
+
+def bcq_quantize(w, q, g, T, pot=False):
+    """Alg. 1 per scale group of a weight matrix w [N][K] (groups: g consecutive k of a row).
+
+    For each group: greedy (Eq. 1); then T times: LS (Line 6), optional PoT projection of
+    every alpha_i (pot_round_exact, Eq. 2 with K = 1), BS (Line 7).  Returns signs int8
+    [q][N][K] and alpha fp64 [q][N][K/g] (the codes are BS of the returned alphas when T >= 1,
+    the greedy codes when T == 0)."""
+    W = np.asarray(w, dtype=np.float64)
+    N, K = W.shape
+    if K % g:
+        raise ValueError("g must divide K")
+    signs = np.empty((q, N, K), dtype=np.int8)
+    alphas = np.empty((q, N, K // g))
+    for n in range(N):
+        for G in range(K // g):
+            wg = W[n, G * g:(G + 1) * g]
+            alpha, B = bcq_greedy(wg, q)
+            for _ in range(T):
+                alpha = bcq_ls(B, wg)
+                if pot:
+                    alpha = np.array([pot_round_exact(v) for v in alpha])
+                B = bcq_bs_codes(alpha, wg)
+            signs[:, n, G * g:(G + 1) * g] = B.astype(np.int8)
+            alphas[:, n, G] = alpha
+    return signs, alphas
 
 
 # ----------------------------------------------------------------------- output + metrics

@@ -533,3 +533,105 @@ def test_s10_zero_second_terms_reduce_to_gemm():
     e = rng.integers(-6, 6, size=(q, N, K // g)).astype(np.int8)
     x = _rand_fp16(rng, (2, K))
     assert np.array_equal(oracle.gemm_apot2(x, planes, e, np.zeros_like(e), g), oracle.gemm(x, planes, e, g))
+
+
+# ------------------------------------ S11: Alg. 1 alternating BCQ quantiser (NEXT-f4)
+def test_s11_spec_worked_values():
+    """SPEC.md:107-110 (1-bit analytic), :117-118 (greedy q=2), :134-136 (BS examples)."""
+    a, B = oracle.bcq_greedy([1.0, 2.0, -3.0, 0.5], 1)
+    assert a[0] == 1.625 and list(B[0]) == [1, 1, -1, 1]
+    a, B = oracle.bcq_greedy([1.0, 2.0, -3.0, 0.5], 2)
+    assert a[0] == 1.625 and a[1] == 0.875
+    r = np.array([1.0, 2.0, -3.0, 0.5]) - 1.625 * B[0]
+    assert list(r) == [-0.625, 0.375, -1.375, -1.125] and list(B[1]) == list(np.where(r >= 0, 1, -1))
+    codes = oracle.bcq_bs_codes([1.0, 0.5], [0.7, 1.0])
+    assert list(codes[:, 0]) == [1, -1]                    # 0.7 -> level +0.5
+    assert list(codes[:, 1]) == [1, -1]                    # tie 0.5 / 1.5 -> smaller |level|
+    assert list(oracle.bcq_bs_codes([2.0], [0.3])[:, 0]) == [1]
+
+
+def test_s11_one_bit_is_the_brute_force_optimum():
+    """q = 1: b = sign(w), alpha = w^T b / n minimises ||w - alpha b||^2 over all 2^n sign
+    patterns (each with its own optimal alpha)."""
+    rng = _rng(110)
+    for _ in range(20):
+        n = int(rng.integers(2, 11))
+        w = rng.standard_normal(n)
+        a, B = oracle.bcq_greedy(w, 1)
+        got = float(np.sum((w - a[0] * B[0]) ** 2))
+        best = min(float(np.sum((w - (w @ b) / n * b) ** 2))
+                   for c in range(1 << n) for b in [np.array([1.0 if (c >> j) & 1 else -1.0 for j in range(n)])])
+        assert got <= best + 1e-12
+
+
+def test_s11_ls_solves_the_normal_equations_exactly():
+    """Against an exact rational solve of (B^T B + 1e-8 n I) alpha = B^T w (q = 2, 3)."""
+    rng = _rng(111)
+    for q in (2, 3):
+        n = 24
+        w = rng.standard_normal(n)
+        _, B = oracle.bcq_greedy(w, q)
+        a = oracle.bcq_ls(B, w)
+        G = [[sum(Fraction(int(B[i, j]) * int(B[k, j])) for j in range(n)) + (Fraction(1e-8) * n if i == k else 0)
+              for k in range(q)] for i in range(q)]
+        rhs = [sum(Fraction(float(w[j])) * int(B[i, j]) for j in range(n)) for i in range(q)]
+        # Gauss-Jordan in rationals
+        M = [row[:] + [rhs[i]] for i, row in enumerate(G)]
+        for c in range(q):
+            piv = next(r for r in range(c, q) if M[r][c] != 0)
+            M[c], M[piv] = M[piv], M[c]
+            M[c] = [v / M[c][c] for v in M[c]]
+            for r in range(q):
+                if r != c and M[r][c] != 0:
+                    M[r] = [vr - M[r][c] * vc for vr, vc in zip(M[r], M[c])]
+        exact = np.array([float(M[i][q]) for i in range(q)])
+        assert np.allclose(a, exact, rtol=1e-12, atol=1e-15)
+
+
+def test_s11_bs_picks_the_nearest_level_by_enumeration():
+    rng = _rng(112)
+    for q in (1, 2, 3, 4):
+        alpha = np.sort(rng.uniform(0.05, 1.0, q))[::-1]
+        w = rng.standard_normal(300)
+        codes = oracle.bcq_bs_codes(alpha, w)
+        lv = alpha @ codes
+        for j in range(w.size):
+            best = None
+            for c in range(1 << q):
+                level = sum(alpha[i] * (1 if (c >> i) & 1 else -1) for i in range(q))
+                k = (abs(w[j] - level), abs(level), level)
+                best = k if best is None or k < best else best
+            assert abs(w[j] - lv[j]) == best[0] and lv[j] == best[2]
+
+
+def test_s11_alternating_is_monotone_and_recovers_representable_weights():
+    rng = _rng(113)
+    for trial in range(30):
+        w = rng.standard_normal(64)
+        alpha, B = oracle.bcq_greedy(w, 3)
+        prev = float(np.sum((w - alpha @ B) ** 2))
+        for _ in range(10):
+            alpha = oracle.bcq_ls(B, w)
+            B = oracle.bcq_bs_codes(alpha, w)
+            cur = float(np.sum((w - alpha @ B) ** 2))
+            assert cur <= prev + 1e-9
+            prev = cur
+    # w drawn from the level set of alpha = (1, 0.5): exactly representable at q = 2
+    lv = np.array([-1.5, -0.5, 0.5, 1.5])
+    w = rng.choice(lv, size=(1, 64))
+    s, a = oracle.bcq_quantize(w, 2, 64, T=15)
+    assert np.allclose((a[:, 0, 0][:, None] * s[:, 0, :]).sum(axis=0), w[0], atol=1e-6)
+
+
+def test_s11_t0_is_greedy_and_pot_projection_matches_pot_exponent():
+    rng = _rng(114)
+    w = rng.standard_normal((3, 256)) * 0.02
+    s, a = oracle.bcq_quantize(w, 3, 128, T=0)
+    for n in range(3):
+        for G in range(2):
+            ag, Bg = oracle.bcq_greedy(w[n, G * 128:(G + 1) * 128], 3)
+            assert np.array_equal(a[:, n, G], ag) and np.array_equal(s[:, n, G * 128:(G + 1) * 128], Bg)
+    vals = (rng.standard_normal(2000) * 10.0 ** rng.uniform(-6, 4, 2000)).astype(np.float32)
+    e, _ = oracle.pot_exponent(vals)
+    for v, ei in zip(vals, e):
+        assert oracle.pot_round_exact(float(v)) == math.copysign(2.0 ** int(ei), float(v))
