@@ -174,6 +174,21 @@ shiftadd_status shiftadd_lut_gemm_apot2(const uint16_t* x, int ldx, const uint8_
                                         const int8_t* exps2, int layout, int M, int N, int K, int q, int g,
                                         uint16_t* y, int ldy, unsigned flags, void* stream);
 
+/* NEXT-f4 -- Alg. 1 alternating multi-bit BCQ quantiser, the step before
+ * shiftadd_pack.  Per scale group (g consecutive k of one output row of w fp32 [N][K]):
+ * greedy init (Eq. 1: b_i = sign(r_{i-1}), sign(0) = +1; alpha_i = mean|r_{i-1}|), then T
+ * cycles of least-squares scale refit alpha = (B^T B + 1e-8 g I)^-1 B^T w (Line 6) -- with
+ * SHIFTADD_BCQ_POT each alpha_i is then projected to sign * 2^round(log2|alpha_i|) (Eq. 2,
+ * K = 1) -- and code refit to the nearest representable level sum_i +-alpha_i (Line 7; ties
+ * -> smaller |level|, then the negative level).  fp64 throughout.
+ *   w     : fp32 [N][K] device, 4-byte aligned;  1 <= q <= 4;  g | K, 1 <= g;  0 <= T <= 1000
+ *   signs : int8 [q][N][K] device (output, +-1; the codes of the final alphas)
+ *   alpha : fp32 [q][N][K/g] device (output; feed both to shiftadd_pack)
+ * One CTA per group; N*K/g < 2^31.  Errors: SHIFTADD_ERR_INVALID on bad sizes/pointers. */
+#define SHIFTADD_BCQ_POT 1u
+shiftadd_status shiftadd_bcq_quantize(const float* w, int N, int K, int q, int g, int T, unsigned flags,
+                                      int8_t* signs, float* alpha, void* stream);
+
 /* Launch geometry the gemm call would use (for measurement/reporting; host only):
  * out[0] = grid CTAs, out[1] = threads per CTA, out[2] = dynamic smem bytes,
  * out[3] = kernel id (0 generic, 1 tiled M=1 split-K, 2 tiled small-batch, 3 tiled M=1

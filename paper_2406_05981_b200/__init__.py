@@ -22,7 +22,7 @@ import torch
 __all__ = [
     "LAYOUT_CANONICAL", "LAYOUT_TILED", "FLAG_PDL", "FLAG_SPLITK", "EXP_ZERO", "ShiftAddError", "lib",
     "PackedLayer", "packed_bytes", "pack", "lut_gemm", "lut_gemv", "workspace_bytes",
-    "gemm_plan", "Workspace", "pack_colwise", "lut_gemv_colwise", "pack_apot2",
+    "gemm_plan", "Workspace", "pack_colwise", "lut_gemv_colwise", "pack_apot2", "bcq_quantize",
 ]
 
 LAYOUT_CANONICAL = 0
@@ -80,6 +80,8 @@ def lib():
         L.shiftadd_lut_gemm_apot2.restype = c_int
         L.shiftadd_lut_gemm_apot2.argtypes = [vp, c_int, vp, vp, vp, c_int, c_int, c_int, c_int, c_int, c_int,
                                               vp, c_int, ctypes.c_uint, vp]
+        L.shiftadd_bcq_quantize.restype = c_int
+        L.shiftadd_bcq_quantize.argtypes = [vp, c_int, c_int, c_int, c_int, c_int, ctypes.c_uint, vp, vp, vp]
         L.shiftadd_gemm_plan.restype = c_int
         L.shiftadd_gemm_plan.argtypes = [c_int] * 6 + [ctypes.POINTER(c_int * 4)]
         v = L.shiftadd_abi_version()
@@ -162,6 +164,28 @@ def pack(signs: torch.Tensor, alpha: torch.Tensor, g: int, layout: int = LAYOUT_
                                  _ptr(counts), _stream_ptr(stream, dev))
     _check(st, "shiftadd_pack")
     return PackedLayer(planes, exps, q, N, K, g, layout, counts)
+
+
+BCQ_POT = 1
+
+
+def bcq_quantize(w: torch.Tensor, q: int, g: int, T: int = 15, pot: bool = False, stream=None):
+    """NEXT-f4: Alg. 1 alternating multi-bit BCQ of an fp32 weight matrix [N][K] on the device
+    (shiftadd_bcq_quantize).  Returns (signs int8 [q][N][K], alpha fp32 [q][N][K/g]) -- the
+    inputs of ``pack``."""
+    if w.dtype != torch.float32 or not w.is_cuda or w.dim() != 2:
+        raise ValueError("w must be a CUDA fp32 [N][K] tensor")
+    w = w.contiguous()
+    N, K = w.shape
+    if g <= 0 or K % g:
+        raise ValueError("g must divide K")
+    signs = torch.empty((q, N, K), dtype=torch.int8, device=w.device)
+    alpha = torch.empty((q, N, K // g), dtype=torch.float32, device=w.device)
+    with torch.cuda.device(w.device):
+        st = lib().shiftadd_bcq_quantize(_ptr(w), N, K, q, g, T, BCQ_POT if pot else 0, _ptr(signs), _ptr(alpha),
+                                         _stream_ptr(stream, w.device))
+    _check(st, "shiftadd_bcq_quantize")
+    return signs, alpha
 
 
 def pack_apot2(signs: torch.Tensor, alpha: torch.Tensor, g: int, layout: int = LAYOUT_TILED,

@@ -249,6 +249,24 @@ shiftadd_status shiftadd_lut_gemm_apot2(const uint16_t* x, int ldx, const uint8_
   return SHIFTADD_OK;
 }
 
+shiftadd_status shiftadd_bcq_quantize(const float* w, int N, int K, int q, int g, int T, unsigned flags,
+                                      int8_t* signs, float* alpha, void* stream) {
+  if (!w || !signs || !alpha) return fail(SHIFTADD_ERR_INVALID, "null pointer argument");
+  if (q < 1 || q > 4) return fail(SHIFTADD_ERR_INVALID, "q=%d outside [1, 4]", q);
+  if (N < 1 || K < 1 || g < 1 || K % g) return fail(SHIFTADD_ERR_INVALID, "need N, K, g >= 1 and g | K");
+  if (T < 0 || T > 1000) return fail(SHIFTADD_ERR_INVALID, "T=%d outside [0, 1000]", T);
+  if ((long long)N * (K / g) >= 0x7fffffffLL) return fail(SHIFTADD_ERR_INVALID, "too many scale groups");
+  if (flags & ~SHIFTADD_BCQ_POT) return fail(SHIFTADD_ERR_INVALID, "unknown flags 0x%x", flags);
+  if (!aligned(w, 4) || !aligned(alpha, 4)) return fail(SHIFTADD_ERR_INVALID, "misaligned pointer");
+  DevInfo di;
+  shiftadd_status st;
+  if ((st = device_info(&di)) != SHIFTADD_OK) return st;
+  const cudaError_t e = launch_bcq_quantize(w, N, K, q, g, T, (flags & SHIFTADD_BCQ_POT) ? 1 : 0, signs, alpha,
+                                            reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "bcq_quantize launch");
+  return SHIFTADD_OK;
+}
+
 size_t shiftadd_workspace_bytes(int layout, int M, int N, int K, int q, int g) {
   if (check_shape(q, N, K, g, 4) != SHIFTADD_OK || check_layout(layout, K, g) != SHIFTADD_OK) return 0;
   if (M < 1 || M > 16) return 0;

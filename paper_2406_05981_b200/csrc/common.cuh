@@ -204,6 +204,9 @@ cudaError_t launch_pack_colwise(const int8_t* signs, const float* alpha_col, int
                                 int layout, uint8_t* planes, int8_t* exps_col, int32_t* counts,
                                 cudaStream_t stream);
 
+cudaError_t launch_bcq_quantize(const float* w, int N, int K, int q, int g, int T, int pot, int8_t* signs,
+                                float* alpha, cudaStream_t stream);
+
 LaunchPlan plan_generic(int M, int N, int K, int q, int g, int sms);
 cudaError_t launch_gemm_generic(const GemmArgs& a, const LaunchPlan& p);
 

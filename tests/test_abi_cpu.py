@@ -149,3 +149,13 @@ def test_apot2_validation_happens_before_any_launch(L):
     assert L.shiftadd_lut_gemm_apot2(p, 512, p, p, None, 1, 1, 64, 512, 3, 128, p, 64, 0, None) == 2
     assert L.shiftadd_lut_gemm_apot2(p, 512, p, p, p, 1, 2, 64, 512, 3, 128, p, 64, 0, None) == 6
     assert L.shiftadd_lut_gemm_apot2(p, 512, p, p, p, 1, 1, 64, 512, 3, 128, p, 64, 2, None) == 2
+
+
+def test_quantize_validation_happens_before_any_launch(L):
+    _r1, p = _buf(1 << 16)
+    assert L.shiftadd_bcq_quantize(None, 4, 256, 2, 128, 3, 0, p, p, None) == 2
+    assert L.shiftadd_bcq_quantize(p, 4, 256, 5, 128, 3, 0, p, p, None) == 2
+    assert L.shiftadd_bcq_quantize(p, 4, 256, 2, 100, 3, 0, p, p, None) == 2
+    assert L.shiftadd_bcq_quantize(p, 4, 256, 2, 128, -1, 0, p, p, None) == 2
+    assert L.shiftadd_bcq_quantize(p, 4, 256, 2, 128, 3, 4, p, p, None) == 2
+    assert L.shiftadd_bcq_quantize(p, 4, 256, 2, 128, 3, 1, p, p, None) == 7   # valid: no GPU here

@@ -177,6 +177,30 @@ def config0(dev):
             "GBps": round(b / us * 1e-3, 1)}
 
 
+def quantize(dev):
+    """NEXT-f4: Alg. 1 on the device (fp64), OPT-6.7B FC1 (16384 x 4096) and attention
+    (4096 x 4096) weights, g = 128, q = 3, T = 15, PoT projection on."""
+    out = []
+    for name, N, K in (("attn", 4096, 4096), ("fc1", 16384, 4096)):
+        gen = torch.Generator(device=dev).manual_seed(5)
+        w = torch.randn((N, K), generator=gen, device=dev) * 0.02
+        sa.bcq_quantize(w, 3, 128, T=15, pot=True)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        s, a = sa.bcq_quantize(w, 3, 128, T=15, pot=True)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        wq = (s.float() * a.repeat_interleave(128, dim=2)).sum(dim=0)
+        rel = float(((w - wq) ** 2).sum() / (w ** 2).sum())
+        out.append({"name": "quantize", "layer": name, "N": N, "K": K, "q": 3, "g": 128, "T": 15, "pot": True,
+                    "ms": round(ms, 3), "weights_per_s": round(N * K / (ms * 1e-3), 0),
+                    "rel_sq_error": round(rel, 5)})
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", nargs="*")
@@ -190,6 +214,7 @@ def main():
         "llama7b_batch": lambda: llama7b_batch(dev),
         "llama70b_mlp": lambda: llama70b_mlp(dev),
         "opt66b_decode": lambda: [opt66b_decode(dev, 2), opt66b_decode(dev, 3)],
+        "quantize": lambda: quantize(dev),
     }
     lines = []
     for name, fn in jobs.items():
