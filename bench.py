@@ -241,6 +241,9 @@ def main():
     ap.add_argument("--impl", default="shiftadd", choices=["shiftadd", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pdl", action="store_true")
+    ap.add_argument("--gather", default="nccl", choices=["nccl", "fused"],
+                    help="N > 1: NCCL all_gather_into_tensor after each GEMV, or the fused-gather "
+                         "epilogue (NEXT-f3: peer stores over CUDA IPC/NVLink + flag wait)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -288,9 +291,17 @@ def main():
         wsp.get(max(sa.workspace_bytes(L, 1) for L in copies[0]))
     stream.synchronize()
 
+    fused = None
+    if group is not None and args.gather == "fused":
+        from paper_2406_05981_b200.dist import FusedGatherLinear
+        fused = [FusedGatherLinear(copies[0][li], N, group=group) for li, (_, N, _, _, _, _) in enumerate(shard)]
+
     def step(t):
         cur = copies[t % R]
         for li in range(len(shard)):
+            if fused is not None:
+                fused[li](xs[li], pdl=pdl, stream=stream, layer=cur[li])
+                continue
             sa.lut_gemm(xs[li], cur[li], out=ys[li], workspace=wsp, pdl=pdl)
             if group is not None:
                 torch.distributed.all_gather_into_tensor(yfull[li], ys[li], group=group)
@@ -403,6 +414,9 @@ def main():
         cur = copies[t % R]
         for li in range(len(shard)):
             xd[li].copy_(xh[li], non_blocking=True)
+            if fused is not None:
+                yh[li].copy_(fused[li](xd[li], stream=stream, layer=cur[li]).reshape(1, -1), non_blocking=True)
+                continue
             sa.lut_gemm(xd[li], cur[li], out=ys[li], workspace=wsp, pdl=False)
             if group is not None:
                 torch.distributed.all_gather_into_tensor(yfull[li], ys[li], group=group)

@@ -189,6 +189,30 @@ shiftadd_status shiftadd_lut_gemm_apot2(const uint16_t* x, int ldx, const uint8_
 shiftadd_status shiftadd_bcq_quantize(const float* w, int N, int K, int q, int g, int T, unsigned flags,
                                       int8_t* signs, float* alpha, void* stream);
 
+/* NEXT-f3 -- batch-1 LUT-GEMV with the all-gather fused into its epilogue (§8(e) rows are
+ * independent per rank; BASELINE.json north_star's all-gather of y).  Rank `rank` of P owns
+ * N rows (its packed shard).  Call c = *epoch + 1 stores each output element directly into
+ * every rank's gathered buffer c % 2, y_peers[(c%2)*P + r][rank*N + n] (peer memory over
+ * NVLink / CUDA IPC); the last CTA of the launch then publishes c into flag_peers[r][rank]
+ * of every rank (one system-scope release pattern).  shiftadd_gather_wait(flags_local, P,
+ * epoch) enqueues a wait (acquire, system scope) until all P ranks have published
+ * *epoch + 1 and then advances *epoch; after it the local buffer c % 2 holds the whole y
+ * [P*N].  The call counter lives on the device, so both calls may be captured in a CUDA graph
+ * and replayed.  Double buffering is safe: a rank reaches call c + 2 only after every rank
+ * finished call c + 1, which consumed buffer c % 2.
+ *   y_peers: device array of 2P device pointers; flag_peers: device array of P device
+ *   pointers (flag arrays uint32[P], zero-initialised); epoch: device uint32, starts at 0,
+ *   one per (rank, layer).  2 <= P <= 8.
+ *   workspace: shiftadd_workspace_bytes(...) and >= 256 KB + 16 B (a launch counter at
+ *   byte 256 KB, left zero).  Supported: tiled layout, shapes the cluster kernel takes
+ *   (K <= 4096; shiftadd_gemm_plan kernel id 3); otherwise SHIFTADD_ERR_UNSUPPORTED.
+ *   The wait traps (CUDA error) after ~5 s without progress instead of hanging. */
+shiftadd_status shiftadd_lut_gemv_gather(const uint16_t* x, const uint8_t* planes, const int8_t* exps, int layout,
+                                         int N, int K, int q, int g, uint16_t* const* y_peers,
+                                         uint32_t* const* flag_peers, int P, int rank, uint32_t* epoch,
+                                         void* workspace, size_t workspace_bytes, unsigned flags, void* stream);
+shiftadd_status shiftadd_gather_wait(const uint32_t* flags_local, int P, uint32_t* epoch, void* stream);
+
 /* Launch geometry the gemm call would use (for measurement/reporting; host only):
  * out[0] = grid CTAs, out[1] = threads per CTA, out[2] = dynamic smem bytes,
  * out[3] = kernel id (0 generic, 1 tiled M=1 split-K, 2 tiled small-batch, 3 tiled M=1

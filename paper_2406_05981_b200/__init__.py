@@ -82,6 +82,11 @@ def lib():
                                               vp, c_int, ctypes.c_uint, vp]
         L.shiftadd_bcq_quantize.restype = c_int
         L.shiftadd_bcq_quantize.argtypes = [vp, c_int, c_int, c_int, c_int, c_int, ctypes.c_uint, vp, vp, vp]
+        L.shiftadd_lut_gemv_gather.restype = c_int
+        L.shiftadd_lut_gemv_gather.argtypes = [vp, vp, vp, c_int, c_int, c_int, c_int, c_int, vp, vp, c_int, c_int,
+                                               vp, vp, c_size, ctypes.c_uint, vp]
+        L.shiftadd_gather_wait.restype = c_int
+        L.shiftadd_gather_wait.argtypes = [vp, c_int, vp, vp]
         L.shiftadd_gemm_plan.restype = c_int
         L.shiftadd_gemm_plan.argtypes = [c_int] * 6 + [ctypes.POINTER(c_int * 4)]
         v = L.shiftadd_abi_version()

@@ -267,6 +267,63 @@ shiftadd_status shiftadd_bcq_quantize(const float* w, int N, int K, int q, int g
   return SHIFTADD_OK;
 }
 
+shiftadd_status shiftadd_lut_gemv_gather(const uint16_t* x, const uint8_t* planes, const int8_t* exps, int layout,
+                                         int N, int K, int q, int g, uint16_t* const* y_peers,
+                                         uint32_t* const* flag_peers, int P, int rank, uint32_t* epoch,
+                                         void* workspace, size_t workspace_bytes, unsigned flags, void* stream) {
+  if (!x || !planes || !exps || !y_peers || !flag_peers || !epoch || !workspace)
+    return fail(SHIFTADD_ERR_INVALID, "null pointer argument");
+  shiftadd_status st = check_shape(q, N, K, g, 4);
+  if (st != SHIFTADD_OK) return st;
+  if ((st = check_layout(layout, K, g)) != SHIFTADD_OK) return st;
+  if (P < 2 || P > 8 || rank < 0 || rank >= P) return fail(SHIFTADD_ERR_INVALID, "need 2 <= P <= 8, 0 <= rank < P");
+  if (flags & ~SHIFTADD_FLAG_PDL) return fail(SHIFTADD_ERR_INVALID, "unknown flags 0x%x", flags);
+  if (layout != SHIFTADD_LAYOUT_TILED) return fail(SHIFTADD_ERR_UNSUPPORTED, "fused gather needs the tiled layout");
+  if (workspace_bytes < kCounterBytes + 16 || !aligned(workspace, 16))
+    return fail(SHIFTADD_ERR_INVALID, "workspace needs >= %zu bytes, 16-B aligned", kCounterBytes + 16);
+  if (!aligned(x, 16) || !aligned(planes, 16)) return fail(SHIFTADD_ERR_INVALID, "misaligned x / planes");
+  DevInfo di;
+  if ((st = device_info(&di)) != SHIFTADD_OK) return st;
+  if (!cluster_applicable(N, K, q, di.sms))
+    return fail(SHIFTADD_ERR_UNSUPPORTED, "fused gather: K=%d N=%d q=%d outside the cluster kernel", K, N, q);
+  GemmArgs a;
+  a.x = reinterpret_cast<const __half*>(x);
+  a.ldx = K;
+  a.planes = planes;
+  a.exps = exps;
+  a.M = 1;
+  a.N = N;
+  a.K = K;
+  a.q = q;
+  a.g = g;
+  a.y = nullptr;
+  a.ldy = N;
+  a.workspace = workspace;
+  a.workspace_bytes = workspace_bytes;
+  a.flags = flags;
+  a.stream = reinterpret_cast<cudaStream_t>(stream);
+  a.gather.y_peers = reinterpret_cast<__half* const*>(y_peers);
+  a.gather.flag_peers = flag_peers;
+  a.gather.counter = reinterpret_cast<unsigned*>(static_cast<char*>(workspace) + kCounterBytes);
+  a.gather.P = P;
+  a.gather.rank = rank;
+  a.gather.epoch = epoch;
+  const cudaError_t e = launch_gemv_cluster(a, plan_gemv_cluster(N, K, q, di.sms));
+  if (e != cudaSuccess) return cuda_fail(e, "lut_gemv_gather launch");
+  return SHIFTADD_OK;
+}
+
+shiftadd_status shiftadd_gather_wait(const uint32_t* flags_local, int P, uint32_t* epoch, void* stream) {
+  if (!flags_local || !epoch) return fail(SHIFTADD_ERR_INVALID, "null pointer argument");
+  if (P < 1 || P > 32) return fail(SHIFTADD_ERR_INVALID, "P=%d outside [1, 32]", P);
+  DevInfo di;
+  shiftadd_status st;
+  if ((st = device_info(&di)) != SHIFTADD_OK) return st;
+  const cudaError_t e = launch_gather_wait(flags_local, P, epoch, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "gather_wait launch");
+  return SHIFTADD_OK;
+}
+
 size_t shiftadd_workspace_bytes(int layout, int M, int N, int K, int q, int g) {
   if (check_shape(q, N, K, g, 4) != SHIFTADD_OK || check_layout(layout, K, g) != SHIFTADD_OK) return 0;
   if (M < 1 || M > 16) return 0;

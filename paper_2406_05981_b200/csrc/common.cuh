@@ -171,12 +171,26 @@ __device__ __forceinline__ void load_unit(const uint4* __restrict__ planes, cons
   for (int i = 0; i < Q; ++i) e[i] = ldg_s8_stream(exps + (u * Q + i) * 32 + lane, pol);
 }
 
+// NEXT-f3 fused all-gather epilogue (P == 0: off).  y_peers: device array of 2P device
+// pointers (y_peers[b*P + r] = rank r's gathered buffer b, [P*N], mapped here); flag_peers:
+// device array of P pointers (rank r's flag array uint32[P]); epoch: this rank's device call
+// counter for the layer (call c = *epoch + 1 writes buffer c & 1 and publishes c).
+struct GatherArgs {
+  __half* const* y_peers = nullptr;
+  uint32_t* const* flag_peers = nullptr;
+  const uint32_t* epoch = nullptr;
+  unsigned* counter = nullptr;
+  int P = 0;
+  int rank = 0;
+};
+
 struct GemmArgs {
   const __half* x;
   int ldx;
   const uint8_t* planes;
   const int8_t* exps;
   const int8_t* exps2 = nullptr;   // NEXT-f2 second additive-PoT term codes (same layout as exps)
+  GatherArgs gather;               // NEXT-f3
   int M, N, K, q, g;
   __half* y;
   int ldy;
@@ -218,6 +232,7 @@ bool cluster_applicable(int N, int K, int q, int sms);
 // NEXT-f1: column-wise scales, M = 1, tiled planes, exps_col [q][K]; K <= 4096.
 bool colwise_applicable(int N, int K, int q);
 cudaError_t launch_gemv_colwise(const GemmArgs& a);
+cudaError_t launch_gather_wait(const uint32_t* flags, int P, uint32_t* epoch, cudaStream_t stream);
 LaunchPlan plan_gemv_cluster(int N, int K, int q, int sms);
 cudaError_t launch_gemv_cluster(const GemmArgs& a, const LaunchPlan& p);
 

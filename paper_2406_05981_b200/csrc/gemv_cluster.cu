@@ -242,6 +242,31 @@ __host__ __device__ constexpr int cl_ring(int Q, int REGS) {
   return (REGS - 56) / (5 * Q) < 1 ? 1 : ((REGS - 56) / (5 * Q) > 8 ? 8 : (REGS - 56) / (5 * Q));
 }
 
+// NEXT-f3 completion signal.  After bar.sync, thread 0 of every CTA adds 1 to the launch
+// counter with a gpu-scope acq_rel atomic (its release half covers the CTA's peer stores,
+// cumulative through the barrier).  The last CTA -- whose acquire observed every other
+// CTA's release -- re-arms the counter and publishes `epoch` into flag[rank] of every rank
+// with one release pattern (fence.acq_rel.sys, then relaxed system-scope stores).  Causality is transitive through the two
+// synchronising pairs (gpu scope inside this GPU, system scope to the peers), so a consumer
+// that acquires all P flags == epoch sees every rank's whole y shard.  (A system-scope
+// fence or atomic in every CTA measured 6-12 us per launch; one in the last CTA is cheap.)
+__device__ __forceinline__ void gather_signal(const GatherArgs& ga) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned prev;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(ga.counter) : "memory");
+    if (prev == gridDim.x - 1) {
+      // one release pattern for all P flags: fence.acq_rel.sys + strong relaxed stores
+      // (st.release.sys per flag compiles to a MEMBAR.ALL.SYS each)
+      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(ga.counter) : "memory");
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+      for (int r = 0; r < ga.P; ++r)
+        asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(ga.flag_peers[r] + ga.rank), "r"(*ga.epoch + 1u)
+                     : "memory");
+    }
+  }
+}
+
 // Items of a CTA: i = t * RGb + rgl (slice t of its Sc, row group rgl of the band), warp w
 // takes i = w, w + NW, ...; item i is tiled-layout unit (s0 + t) * RG + rg0 + rgl.  The
 // warp walks its items with (t, rgl) cursors (no division per item).
@@ -260,7 +285,8 @@ template <int Q, int SCM, int NW, int REGS, bool COLW, bool AP2 = false>
 __global__ void __launch_bounds__(NW * 32) __maxnreg__(REGS)
 gemv_cluster_kernel(const __half* __restrict__ x, const uint4* __restrict__ planes,
                     const int8_t* __restrict__ exps, int N, int S, int RG, int C, __half* __restrict__ y,
-                    int flags, unsigned long long* __restrict__ trace, const int8_t* __restrict__ exps2) {
+                    int flags, unsigned long long* __restrict__ trace, const int8_t* __restrict__ exps2,
+                    GatherArgs ga) {
   constexpr int D = COLW ? cl_ring_colw(Q, REGS) : (AP2 ? cl_ring_ap2(Q, REGS) : cl_ring(Q, REGS));
   static_assert(!(COLW && AP2), "column-wise and additive-PoT-2 layers are separate formats");
   static_assert(!COLW || (SCM == 4 && Q <= 4), "column-wise: one LUT slot per plane");
@@ -422,8 +448,17 @@ gemv_cluster_kernel(const __half* __restrict__ x, const uint4* __restrict__ plan
     float v = lds_f32(recv + 4u * (uint32_t)j);
     for (int c = 1; c < C; ++c) v += lds_f32(recv + 4u * (uint32_t)(c * chunk + j));
     const int n = rg0 * kTileRows + own_lo + j;
-    if (n < N) y[n] = __float2half_rn(v);
+    if (n < N) {
+      const __half hv = __float2half_rn(v);
+      if (ga.P == 0) {
+        y[n] = hv;
+      } else {   // NEXT-f3: store straight into every rank's gathered y (peer memory)
+        const int b = (int)((*ga.epoch + 1u) & 1u);
+        for (int r = 0; r < ga.P; ++r) ga.y_peers[b * ga.P + r][(size_t)ga.rank * N + n] = hv;
+      }
+    }
   }
+  if (ga.P > 0) gather_signal(ga);
   if (tr && threadIdx.x == 0) {
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -500,7 +535,7 @@ int occupancy_clusters(int C) {
   c.attrs = &attr;
   c.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, gemv_cluster_kernel<2, SCM, NW, 128, COLW>, &c) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&n, gemv_cluster_kernel<2, SCM, NW, 128, COLW, false>, &c) != cudaSuccess) {
     cudaGetLastError();
     n = 0;
   }
@@ -558,7 +593,7 @@ cudaError_t launch_cluster_q(const GemmArgs& a, const LaunchPlan& p, int C) {
   const int flags = (pdl ? kFlagPdl : 0) | (x_first() ? kFlagXFirst : 0) | (barrier_tail() ? kFlagBarrierTail : 0);
   return cudaLaunchKernelEx(&c, gemv_cluster_kernel<Q, SCM, NW, REGS, COLW, AP2>, a.x,
                             reinterpret_cast<const uint4*>(a.planes), a.exps, a.N, S, RG, C, a.y, flags, trace,
-                            a.exps2);
+                            a.exps2, a.gather);
 }
 
 template <int SCM, int NW, bool AP2 = false>
@@ -572,7 +607,45 @@ cudaError_t launch_cluster_v(const GemmArgs& a, const LaunchPlan& p, int C) {
   }
 }
 
+// NEXT-f3 consumer side: wait until every rank published call *epoch + 1 (acquire, system
+// scope), then advance *epoch (the device call counter the producer reads).  Bounded: ~5 s
+// without progress traps (an error, not a hung GPU).
+__global__ void gather_wait_kernel(const uint32_t* __restrict__ flags, int P, uint32_t* __restrict__ epoch_ctr) {
+  // Launched with PDL: it may start while the producing GEMV still runs (it only reads
+  // flags, and this rank's own flag covers that GEMV's stores), and lets its dependents
+  // start at once -- they call griddepcontrol.wait, i.e. wait for this kernel to finish.
+  pdl_launch_dependents();
+  const int r = threadIdx.x;
+  const uint32_t epoch = *epoch_ctr + 1u;
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (; r < P;) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + r) : "memory");
+    if ((int)(v - epoch) >= 0) break;
+    __nanosleep(200);
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 5000000000ull) __trap();
+  }
+  __syncwarp();
+  if (r == 0) *epoch_ctr = epoch;
+}
+
 }  // namespace
+
+cudaError_t launch_gather_wait(const uint32_t* flags, int P, uint32_t* epoch, cudaStream_t stream) {
+  cudaLaunchConfig_t c = {};
+  c.gridDim = dim3(1);
+  c.blockDim = dim3(32);
+  c.stream = stream;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr.val.programmaticStreamSerializationAllowed = 1;
+  c.attrs = &attr;
+  c.numAttrs = 1;
+  return cudaLaunchKernelEx(&c, gather_wait_kernel, flags, P, epoch);
+}
 
 // Clusters of <= 4 pack 132 of the 148 SMs; of 5-8 fewer (120 at C = 8, measured), which
 // costs more than the grid split-K's hand-off once the layer streams long enough: C > 4 only

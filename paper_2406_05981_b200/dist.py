@@ -15,9 +15,11 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
-from . import LAYOUT_TILED, PackedLayer, Workspace, lut_gemm, pack
+import ctypes
 
-__all__ = ["shard_range", "gather_output", "ShardedLinear"]
+from . import FLAG_PDL, LAYOUT_TILED, PackedLayer, Workspace, _check, lib, lut_gemm, pack
+
+__all__ = ["shard_range", "gather_output", "ShardedLinear", "FusedGatherLinear"]
 
 
 def shard_range(N: int, world: int, rank: int):
@@ -76,3 +78,90 @@ class ShardedLinear:
         if not dist.is_initialized():
             return y_local
         return gather_output(y_local, self.group)
+
+
+def _share(t: torch.Tensor):
+    """Picklable CUDA IPC description of ``t`` (torch's own reducer)."""
+    from torch.multiprocessing.reductions import reduce_tensor
+    return reduce_tensor(t)
+
+
+def _open(desc):
+    fn, args = desc
+    return fn(*args)
+
+
+class FusedGatherLinear:
+    """NEXT-f3: row-sharded layer whose GEMV epilogue writes y straight into every rank's
+    gathered buffer (shiftadd_lut_gemv_gather), followed by an on-stream flag wait
+    (shiftadd_gather_wait) -- no NCCL call on the data path.
+
+    Each rank allocates two gathered buffers [P*n] (double-buffered by call parity, see
+    include/shiftadd.h) and a flag array uint32[P]; their CUDA IPC handles are exchanged once
+    over ``group`` (any backend; gloo works) and mapped into every process.  Peers on other
+    GPUs are reached over NVLink through the IPC mappings; ranks may also share one GPU
+    (that is how the single-GPU test exercises the protocol)."""
+
+    def __init__(self, layer: PackedLayer, N_full: int, group=None):
+        self.layer = layer
+        self.group = group
+        self.P = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.n = layer.N
+        if self.n * self.P != N_full:
+            raise ValueError("N_full must equal P * local rows")
+        dev = layer.device
+        self.ybuf = [torch.zeros(self.P * self.n, dtype=torch.float16, device=dev) for _ in range(2)]
+        self.flags = torch.zeros(self.P, dtype=torch.int32, device=dev)
+        mine = [_share(self.ybuf[0]), _share(self.ybuf[1]), _share(self.flags)]
+        allh = [None] * self.P
+        dist.all_gather_object(allh, mine, group=group)
+        self._peers = []                                  # keep mapped tensors alive
+        yp = [[], []]
+        fp = []
+        for r in range(self.P):
+            if r == self.rank:
+                t = [self.ybuf[0], self.ybuf[1], self.flags]
+            else:
+                t = [_open(d) for d in allh[r]]
+                self._peers.append(t)
+            yp[0].append(t[0].data_ptr())
+            yp[1].append(t[1].data_ptr())
+            fp.append(t[2].data_ptr())
+        self.y_ptrs = torch.tensor(yp[0] + yp[1], dtype=torch.int64, device=dev)   # [2P]: buffer b of rank r
+        self.flag_ptrs = torch.tensor(fp, dtype=torch.int64, device=dev)
+        self.epoch = torch.zeros(1, dtype=torch.int32, device=dev)                 # device call counter
+        self.workspace = Workspace(dev)
+        from . import workspace_bytes
+        self.workspace.get(max(workspace_bytes(layer, 1), 256 * 1024 + 16))
+        self.calls = 0                                                             # host mirror (parity)
+        torch.cuda.synchronize(dev)
+        dist.barrier(group=group)
+
+    def __call__(self, x: torch.Tensor, pdl: bool = False, stream=None, layer: PackedLayer | None = None):
+        """y [1][P*n] for x [K] or [1][K] fp16; the returned view is valid until call + 2.
+        ``layer`` may substitute another packed layer of the same shape (rotating copies).
+        The call counter is on the device (graph capture works); the returned view follows
+        the host's count of calls, so a replayed graph should hold an even number of calls
+        of this layer when its outputs are read."""
+        L = layer if layer is not None else self.layer
+        xv = x.reshape(-1)
+        if xv.dtype != torch.float16 or xv.numel() != L.K:
+            raise ValueError("x must be fp16 [K]")
+        xv = xv.contiguous()
+        self.calls += 1
+        par = self.calls & 1
+        dev = L.device
+        sptr = (stream if stream is not None else torch.cuda.current_stream(dev)).cuda_stream
+        ws = self.workspace.buf
+        lib_ = lib()
+        st = lib_.shiftadd_lut_gemv_gather(xv.data_ptr(), L.planes.data_ptr(), L.exps.data_ptr(), L.layout, self.n,
+                                          L.K, L.q, L.g, self.y_ptrs.data_ptr(), self.flag_ptrs.data_ptr(),
+                                          self.P, self.rank, self.epoch.data_ptr(), ws.data_ptr(), ws.numel(),
+                                          FLAG_PDL if pdl else 0, sptr)
+        if st:
+            _check(st, "shiftadd_lut_gemv_gather")
+        st = lib_.shiftadd_gather_wait(self.flags.data_ptr(), self.P, self.epoch.data_ptr(), sptr)
+        if st:
+            _check(st, "shiftadd_gather_wait")
+        return self.ybuf[par].view(1, -1)

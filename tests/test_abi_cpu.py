@@ -159,3 +159,15 @@ def test_quantize_validation_happens_before_any_launch(L):
     assert L.shiftadd_bcq_quantize(p, 4, 256, 2, 128, -1, 0, p, p, None) == 2
     assert L.shiftadd_bcq_quantize(p, 4, 256, 2, 128, 3, 4, p, p, None) == 2
     assert L.shiftadd_bcq_quantize(p, 4, 256, 2, 128, 3, 1, p, p, None) == 7   # valid: no GPU here
+
+
+def test_gather_validation_happens_before_any_launch(L):
+    _r1, p = _buf(1 << 20)
+    args = (p, p, p, 1, 4096, 4096, 3, 128)
+    assert L.shiftadd_lut_gemv_gather(*args, None, p, 2, 0, p, p, 1 << 19, 0, None) == 2
+    assert L.shiftadd_lut_gemv_gather(*args, p, p, 2, 0, None, p, 1 << 19, 0, None) == 2  # no epoch counter
+    assert L.shiftadd_lut_gemv_gather(*args, p, p, 1, 0, p, p, 1 << 19, 0, None) == 2     # P < 2
+    assert L.shiftadd_lut_gemv_gather(*args, p, p, 2, 2, p, p, 1 << 19, 0, None) == 2     # rank >= P
+    assert L.shiftadd_lut_gemv_gather(*args, p, p, 2, 0, p, p, 1024, 0, None) == 2        # workspace
+    assert L.shiftadd_lut_gemv_gather(p, p, p, 0, 4096, 4096, 3, 128, p, p, 2, 0, p, p, 1 << 19, 0, None) == 6
+    assert L.shiftadd_gather_wait(None, 2, p, None) == 2
