@@ -513,7 +513,7 @@ cudaError_t set_attrs() {
   std::call_once(once, [] {
     err = cudaFuncSetAttribute(gemv_cluster_kernel<Q, SCM, NW, REGS, COLW, AP2>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<SCM>::total);
-    if (err == cudaSuccess && COLW)
+    if (err == cudaSuccess)   // clusters of up to 16 (column-wise; one slice per CTA)
       err = cudaFuncSetAttribute(gemv_cluster_kernel<Q, SCM, NW, REGS, COLW, AP2>,
                                  cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   });
@@ -659,7 +659,7 @@ bool cluster_applicable(int N, int K, int q, int sms) {
   const int S = K / kTileK;
   if (S < 1) return false;
   const ClusterShape cs = cluster_shape(N, K, q);
-  if (cs.C > kMaxC) return false;
+  if (cs.C > (cs.sc == 1 ? kMaxCColw : kMaxC)) return false;
   if (cs.variant == kFull4 && cs.C > 4 && (double)q * N * K / 8 > kBigC) return false;
   const int ncl = max_clusters(cs.variant, cs.C);
   if (ncl <= 0) return false;
