@@ -403,45 +403,77 @@ def main():
                 "how": "per layer: CUDA events around one replay of a graph of %d back-to-back launches "
                        "(rotating copies) on the launch stream; achieved = sum bytes / sum times" % reps}
 
-    # ---- e2e through the public API with host buffers (pinned H2D of x, D2H of y)
-    xh = [x.cpu().pin_memory() for x in xs]
-    yh = [torch.empty((1, N), dtype=torch.float16).pin_memory() for (_, N, _, _) in LAYERS]
-    xd = [torch.empty_like(x) for x in xs]
-    torch.cuda.synchronize(dev)   # xd was allocated on the default stream; used on `stream`
-    e2e_steps = max(10, min(args.steps, 500))
+    # ---- e2e through the public API with host buffers.  Every step copies that step's inputs
+    # (the four layers' x, one pinned host buffer) host -> device, runs the four GEMVs (plus
+    # the all-gathers when N > 1) and reads the four outputs back device -> host (one pinned
+    # buffer).  With N = 1 the steps are replayed from a CUDA graph (R steps per graph, the
+    # copies inside it), as a serving loop would issue them; with N > 1 they are issued eagerly.
+    Ks = [K for (_, _, K, _, _, _) in shard]
+    Nf = [N for (_, N, _, _) in LAYERS]
+    xoff = [0]
+    for K in Ks:
+        xoff.append(xoff[-1] + K)
+    yoff = [0]
+    for N in Nf:
+        yoff.append(yoff[-1] + N)
+    xh_all = torch.cat([x.reshape(-1).cpu() for x in xs]).pin_memory()
+    yh_all = torch.empty(yoff[-1], dtype=torch.float16).pin_memory()
+    with torch.cuda.stream(stream):
+        xd_all = torch.empty(xoff[-1], dtype=torch.float16, device=dev)
+        yd_all = torch.empty(yoff[-1], dtype=torch.float16, device=dev)
+    torch.cuda.synchronize(dev)
 
     def e2e_step(t):
         cur = copies[t % R]
+        xd_all.copy_(xh_all, non_blocking=True)
         for li in range(len(shard)):
-            xd[li].copy_(xh[li], non_blocking=True)
+            xv = xd_all[xoff[li]:xoff[li + 1]].view(1, -1)
+            yv = yd_all[yoff[li]:yoff[li + 1]].view(1, -1)
             if fused is not None:
-                yh[li].copy_(fused[li](xd[li], stream=stream, layer=cur[li]).reshape(1, -1), non_blocking=True)
-                continue
-            sa.lut_gemm(xd[li], cur[li], out=ys[li], workspace=wsp, pdl=False)
-            if group is not None:
-                torch.distributed.all_gather_into_tensor(yfull[li], ys[li], group=group)
-                yh[li].copy_(yfull[li].reshape(1, -1), non_blocking=True)
+                yv.copy_(fused[li](xv, stream=stream, layer=cur[li]))
+            elif group is not None:
+                sa.lut_gemm(xv, cur[li], out=ys[li], workspace=wsp, pdl=pdl)
+                torch.distributed.all_gather_into_tensor(yv.view(-1), ys[li].view(-1), group=group)
             else:
-                yh[li].copy_(ys[li], non_blocking=True)
+                sa.lut_gemm(xv, cur[li], out=yv, workspace=wsp, pdl=pdl)
+        yh_all.copy_(yd_all, non_blocking=True)
 
+    e2e_rounds = max(2, min(args.steps, 500) // R)
+    e2e_steps = e2e_rounds * R
     with torch.cuda.stream(stream):
         for t in range(3):
             e2e_step(t)
+    stream.synchronize()
+    g_e2e = None
+    if group is None:
+        g_e2e = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_e2e, stream=stream):
+            for t in range(R):
+                e2e_step(t)
+        with torch.cuda.stream(stream):
+            g_e2e.replay()
+        stream.synchronize()
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(stream):
         e0.record(stream)
-        for t in range(e2e_steps):
-            e2e_step(t)
+        for r_ in range(e2e_rounds):
+            if g_e2e is not None:
+                g_e2e.replay()
+            else:
+                for t in range(R):
+                    e2e_step(t)
         e1.record(stream)
     barrier()
+    # the last step's outputs really arrived on the host
+    assert torch.isfinite(yh_all.float()).all()
     e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     if group is not None:
         torch.distributed.all_reduce(e2e_ms, op=torch.distributed.ReduceOp.MAX, group=group)
     e2e_val = full_bytes * e2e_steps / (float(e2e_ms.item()) * 1e-3) / 1e9
-    h2d = sum(2 * K for (_, _, K, _) in LAYERS)
-    d2h = sum(2 * N for (_, N, _, _) in LAYERS)
+    h2d = xh_all.numel() * xh_all.element_size()
+    d2h = yh_all.numel() * yh_all.element_size()
 
     if rank == 0:
         line = {

@@ -499,6 +499,7 @@ ClusterShape cluster_shape(int N, int K, int q) {
   static const int half = env_int("SHIFTADD_CLUSTER_HALF", 0);
   const int S = K / kTileK;
   const int sc = forced_sc > 0 ? (forced_sc > kMaxSc ? kMaxSc : forced_sc) : ((S + 1) / 2 <= kMaxC ? 2 : kMaxSc);
+  // (S + sc - 1) / sc may exceed the portable 8: clusters of up to 16 are non-portable
   const int variant = sc > 2 ? kFull4 : (half ? kHalf : kFull2);
   return ClusterShape{variant, sc, (S + sc - 1) / sc};
 }
@@ -659,8 +660,10 @@ bool cluster_applicable(int N, int K, int q, int sms) {
   const int S = K / kTileK;
   if (S < 1) return false;
   const ClusterShape cs = cluster_shape(N, K, q);
-  if (cs.C > (cs.sc == 1 ? kMaxCColw : kMaxC)) return false;
-  if (cs.variant == kFull4 && cs.C > 4 && (double)q * N * K / 8 > kBigC) return false;
+  if (cs.C > (cs.sc == 1 || env_int("SHIFTADD_CLUSTER_C16", 1) ? kMaxCColw : kMaxC)) return false;
+  static const double big_c = env_int("SHIFTADD_CLUSTER_BIGC", 0) > 0 ? env_int("SHIFTADD_CLUSTER_BIGC", 0) * 1048576.0
+                                                                       : kBigC;
+  if (cs.variant == kFull4 && cs.C > 4 && (double)q * N * K / 8 > big_c) return false;
   const int ncl = max_clusters(cs.variant, cs.C);
   if (ncl <= 0) return false;
   const int RG = (N + kTileRows - 1) / kTileRows;

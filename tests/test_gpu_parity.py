@@ -101,6 +101,7 @@ SHAPES = [
     (2, 23700, 512, 128),  # cluster kernel, C = 1, ragged band of ~10 row groups
     (1, 4000, 3072, 128),  # cluster kernel, C = 3 (12 slices)
     (1, 12000, 4096, 128), # cluster kernel, C = 4, 23 row groups per band
+    (3, 1000, 11008, 128), # cluster kernel, 43 slices over clusters of 11 (uneven split)
 ]
 # (layout, force split-K): the tiled M = 1 path has two decompositions
 KERNELS = [(1, False), (1, True), (0, False)]
@@ -162,14 +163,15 @@ def test_mixed_bit_dispatch_interleaved(sa):
 
 # ------------------------------------------------------------ full-size config parity
 def test_m1_kernel_choice(sa):
-    """Cluster split-K for K <= 4096 (and K <= 8192 up to 12 MB of planes) with <= 128 row
-    groups per band; grid split-K otherwise."""
+    """Cluster split-K for K <= 4096 (and larger K up to 12 MB of planes, clusters of <= 16)
+    with <= 128 row groups per band; grid split-K otherwise."""
     def kid(N, K, M=1, q=1):
         signs, alpha = synth.gen_layer(q, N, K, 128, seed=1, device=DEV)
         return sa.gemm_plan(sa.pack(signs, alpha, 128, layout=sa.LAYOUT_TILED), M)[3]
     assert kid(4096, 4096) == 3 and kid(16384, 4096) == 3 and kid(256, 256) == 3 and kid(768, 768) == 3
     assert kid(2048, 8192) == 3 and kid(28672, 8192, q=3) == 1
-    assert kid(4096, 11008) == 1 and kid(80000, 4096) == 1
+    assert kid(4096, 11008, q=1) == 3                     # 5.6 MB: clusters of 11 (non-portable)
+    assert kid(4096, 11008, q=3) == 1 and kid(80000, 4096) == 1
     assert kid(4096, 4096, M=2) == 2
 
 
