@@ -80,7 +80,11 @@ size_t tiled_rows(int N) { return (size_t)((N + kTileRows - 1) / kTileRows); }
 
 LaunchPlan make_plan(int layout, int M, int N, int K, int q, int g, int sms, unsigned flags) {
   if (layout == SHIFTADD_LAYOUT_CANONICAL) return plan_generic(M, N, K, q, g, sms);
-  if (M == 1) return !(flags & SHIFTADD_FLAG_SPLITK) && cluster_applicable(N, K, q, sms) ? plan_gemv_cluster(N, K, q, sms) : plan_gemv_tiled(N, K, q, sms);
+  if (M == 1) {
+    if (!(flags & SHIFTADD_FLAG_SPLITK) && cluster_applicable(N, K, q, sms)) return plan_gemv_cluster(N, K, q, sms);
+    if (stream_applicable(N, K, q, sms)) return plan_gemv_stream(N, K, q, sms);
+    return plan_gemv_tiled(N, K, q, sms);
+  }
   return plan_gemm_tiled_mb(M, N, K, q, sms);
 }
 
@@ -381,7 +385,9 @@ shiftadd_status shiftadd_lut_gemm(const uint16_t* x, int ldx, const uint8_t* pla
   a.workspace_bytes = workspace_bytes;
   a.flags = flags;
   a.stream = reinterpret_cast<cudaStream_t>(stream);
-  const LaunchPlan p = make_plan(layout, M, N, K, q, g, di.sms, flags);
+  LaunchPlan p = make_plan(layout, M, N, K, q, g, di.sms, flags);
+  // the TMA ring copies exponent tiles with 16-B bulk copies
+  if (p.kernel == 4 && !aligned(exps, 16)) p = plan_gemv_tiled(N, K, q, di.sms);
   cudaError_t e;
   if (layout == SHIFTADD_LAYOUT_CANONICAL) e = launch_gemm_generic(a, p);
   else if (p.kernel == 3) e = launch_gemv_cluster(a, p);

@@ -204,7 +204,8 @@ struct LaunchPlan {
   int grid;
   int threads;
   int smem;
-  int kernel;  // 0 generic, 1 tiled M=1 split-K, 2 tiled small batch, 3 tiled M=1 cluster split-K
+  int kernel;  // 0 generic, 1 tiled M=1 split-K, 2 tiled small batch, 3 tiled M=1 cluster split-K,
+              // 4 tiled M=1 split-K with the TMA weight ring
 };
 
 // Implemented in the kernel translation units.
@@ -225,6 +226,8 @@ LaunchPlan plan_generic(int M, int N, int K, int q, int g, int sms);
 cudaError_t launch_gemm_generic(const GemmArgs& a, const LaunchPlan& p);
 
 LaunchPlan plan_gemv_tiled(int N, int K, int q, int sms);
+bool stream_applicable(int N, int K, int q, int sms);
+LaunchPlan plan_gemv_stream(int N, int K, int q, int sms);
 size_t workspace_gemv_tiled(int N, int K);
 cudaError_t launch_gemv_tiled(const GemmArgs& a, const LaunchPlan& p);
 

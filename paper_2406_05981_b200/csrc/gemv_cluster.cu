@@ -39,18 +39,21 @@ constexpr int kMaxCColw = 16;             // column-wise kernel: non-portable cl
 constexpr int kMaxRGb = 128;              // row groups per band
 constexpr int kMaxRGbColw = 4 * kMaxRGb;  // column-wise: one slice per CTA
 
-// Shared-memory map of a variant with SCM LUT slots: LUT slabs, staged x, per-item row sums
-// part[t][row], receive buffer recv[rank][row of the owner's chunk].
+// Shared-memory map of a variant with SCM LUT slots: LUT slabs, staged x, receive buffer
+// recv[slice s][row of the owner's chunk] (every (slice, row) partial sum of the owner's rows,
+// pushed by the CTA that streamed it), the owner's receive mbarrier.
 template <int SCM>
 struct Smem {
   static constexpr int lut = SCM <= 2 ? kLutBytes : 2 * kLutBytes;
   static constexpr int xstage = SCM * kTileK * 2;
-  static constexpr int part = SCM * kMaxRGb * kTileRows * 4;
-  // the 4-slot map also serves the column-wise kernel (one slice per CTA: part holds up to
-  // kMaxRGbColw row groups), whose bands may be 4x taller
-  static constexpr int recv = ((SCM == 4 ? 4 * kMaxRGb : kMaxRGb) * kTileRows + kMaxCColw) * 4;
+  // chunks are whole row groups: S * chunk <= SCM * (RGb + C) * 16 rows (regular variants);
+  // the column-wise kernel (4-slot map, one slice per CTA) has S = C and bands up to 4x taller
+  static constexpr int recv_rows = SCM * (kMaxRGb + kMaxC) * kTileRows;
+  static constexpr int recv_rows_colw = (kMaxRGbColw + kMaxCColw) * kTileRows;
+  static constexpr int recv = 4 * (SCM == 4 && recv_rows_colw > recv_rows ? recv_rows_colw : recv_rows);
+  static constexpr int part = SCM * kMaxRGb * kTileRows * 4;   // push-at-end mode: part[t][row]
   static constexpr int mbar = 16;   // the owner's receive mbarrier (8-byte aligned)
-  static constexpr int total = lut + xstage + part + recv + mbar;
+  static constexpr int total = lut + xstage + recv + part + mbar;
 };
 static_assert(Smem<2>::total <= 113 * 1024, "two half-SM CTAs must fit one SM");
 
@@ -79,14 +82,6 @@ __device__ __forceinline__ void cluster_arrive_relaxed() {
 __device__ __forceinline__ void cluster_wait() {
   asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
 }
-__device__ __forceinline__ void cluster_sync_full() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void st_dsmem_f32(uint32_t local_addr, uint32_t rank, float v) {
-  uint32_t remote;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_addr), "r"(rank));
-  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(remote), "f"(v) : "memory");
-}
 // Owner-side receive barrier: one arrival (the owner's own expect_tx) + the bytes its peers
 // push with st.async ... complete_tx.
 __device__ __forceinline__ void mbar_init_expect(uint32_t bar, uint32_t tx_bytes) {
@@ -101,6 +96,22 @@ __device__ __forceinline__ void mbar_wait_parity0(uint32_t bar) {
                  : "=r"(done) : "r"(bar) : "memory");
   } while (!done);
 }
+// x staging by the bulk-copy engine (TMA, 1-D): `bytes` from global `src` into this CTA's
+// shared `dst`, completing on `xbar` (already armed with expect_tx).  It does not queue behind
+// the LSU's weight loads.
+__device__ __forceinline__ void mbar_init1(uint32_t bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_load_x(uint32_t dst, const void* src, uint32_t bytes, uint32_t xbar,
+                                            uint64_t pol) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(xbar), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      ::"r"(dst), "l"(src), "r"(bytes), "r"(xbar), "l"(pol) : "memory");
+}
+
 // Asynchronous 4-byte store into CTA `rank`'s shared memory that completes 4 transaction
 // bytes on that CTA's mbarrier (both addresses given in this CTA's window, mapped here).
 __device__ __forceinline__ void st_async_f32(uint32_t local_addr, uint32_t local_bar, uint32_t rank, float v) {
@@ -279,7 +290,8 @@ struct Cursor {
   }
 };
 
-constexpr int kFlagPdl = 1, kFlagXFirst = 2, kFlagBarrierTail = 4;
+constexpr int kFlagPdl = 1, kFlagXFirst = 2, kFlagPushEnd = 4, kFlagXTma = 8;
+constexpr int kPreShift = 8;   // flags bits 8..15: ring slots prefilled before griddepcontrol.wait
 
 template <int Q, int SCM, int NW, int REGS, bool COLW, bool AP2 = false>
 __global__ void __launch_bounds__(NW * 32) __maxnreg__(REGS)
@@ -291,6 +303,7 @@ gemv_cluster_kernel(const __half* __restrict__ x, const uint4* __restrict__ plan
   static_assert(!(COLW && AP2), "column-wise and additive-PoT-2 layers are separate formats");
   static_assert(!COLW || (SCM == 4 && Q <= 4), "column-wise: one LUT slot per plane");
   const bool pdl = flags & kFlagPdl;
+  const int pre = (flags >> kPreShift) & 0xff;
   if (threadIdx.x == 0) check_dyn_base();
   unsigned long long* tr = trace ? trace + 32 * blockIdx.x : nullptr;   // dev trace
   if (tr && threadIdx.x == 0) tr[0] = gtimer_ns();
@@ -311,17 +324,25 @@ gemv_cluster_kernel(const __half* __restrict__ x, const uint4* __restrict__ plan
 
   const uint32_t base = dyn_smem_base_cluster();   // kDynBase | rank << 24
   const uint32_t xs = base + Smem<SCM>::lut;
-  const uint32_t part = xs + Smem<SCM>::xstage;
-  const uint32_t recv = part + Smem<SCM>::part;
-  const uint32_t bar = recv + Smem<SCM>::recv;
-  // a5 set-up: this CTA owns rows [rank*chunk, rank*chunk + cnt) of the band and expects
-  // (C - 1) * cnt fp32 sums from its peers.
+  const uint32_t recv = xs + Smem<SCM>::xstage;
+  const uint32_t part = recv + Smem<SCM>::recv;
+  const uint32_t bar = part + Smem<SCM>::part;
+  const bool push_end = flags & kFlagPushEnd;
+  // a5 set-up: the band's rows are cut into C chunks of whole row groups; rank o owns rows
+  // [o*chunk, o*chunk + cnt) and receives the S slice partials of each, recv[s][row - o*chunk],
+  // (S - Sc) * cnt of them pushed by its peers.
+  const int chunk_rg = (RGb + C - 1) / C;
+  const int chunk = chunk_rg * kTileRows;
   const int rows = RGb * kTileRows;
-  const int chunk = (rows + C - 1) / C;
   const int own_lo = (int)rank * chunk;
   const int cnt = rows - own_lo < chunk ? (rows - own_lo > 0 ? rows - own_lo : 0) : chunk;
-  const bool btail = flags & kFlagBarrierTail;
-  if (tid == 0 && !btail) mbar_init_expect(bar, (uint32_t)((C - 1) * cnt * 4));
+  const float inv_chunk_rg = 1.f / (float)chunk_rg;   // owner of row group g: (g + .5) / chunk_rg
+  const bool xtma = flags & kFlagXTma;
+  const uint32_t xbar = bar + 8;
+  if (tid == 0) {
+    mbar_init_expect(bar, (uint32_t)((push_end ? C - 1 : S - Sc) * cnt * 4));
+    if (xtma) mbar_init1(xbar);
+  }
   cluster_arrive_relaxed();
   const bool xthread = tid < Sc * (kTileK / 8);    // one 16-B chunk of x per thread
   static_assert(NW * 32 >= SCM * (kTileK / 8), "x staging: one chunk per thread");
@@ -337,31 +358,40 @@ gemv_cluster_kernel(const __half* __restrict__ x, const uint4* __restrict__ plan
       for (int i = 0; i < Q; ++i) e2[k][i] = ldg_s8_stream(exps2 + (u * Q + i) * 32 + lane, pol_stream);
     }
   };
-  auto stage_x = [&]() {
-    if (xthread) {
-      const uint4 xv = ldg_keep(xsrc, pol_keep);
-      asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(xs + 16 * tid), "r"(xv.x), "r"(xv.y), "r"(xv.z),
-                   "r"(xv.w) : "memory");
-      if (tr && threadIdx.x == 0) tr[9] = gtimer_ns();
-    }
-  };
-  auto prefill = [&]() {
+  // ring slots [k0, k1) of the first D items
+  auto prefill = [&](int k0, int k1) {
 #pragma unroll
     for (int k = 0; k < D; ++k)
-      if (k < Mw) {
+      if (k >= k0 && k < k1 && k < Mw) {
         if (COLW) load_planes_unit<Q>(planes, (long long)(s0 + ld.t) * RG + rg0 + ld.rgl, lane, pol_stream, w[k]);
         else load_unit<Q>(planes, exps, (long long)(s0 + ld.t) * RG + rg0 + ld.rgl, lane, pol_stream, w[k], e[k]);
         load_e2((long long)(s0 + ld.t) * RG + rg0 + ld.rgl, k);
         ld.advance<NW>(RGb);
       }
   };
-  // Weights do not depend on the upstream kernel: under PDL they are requested before
-  // griddepcontrol.wait.  Without PDL the order is a measured choice (kFlagXFirst).
-  if (pdl || !(flags & kFlagXFirst)) prefill();
+  // Weights do not depend on the upstream kernel: under PDL the first `pre` ring slots are
+  // requested before griddepcontrol.wait -- no more than HBM delivers during the wait, since
+  // x queues behind every weight request issued before it (measured: 1.1 us late on FC1
+  // with the whole ring in flight) -- and the rest right behind x's request.
+  const int pre_n = pdl ? pre : ((flags & kFlagXFirst) ? 0 : D);
+  prefill(0, pre_n);
   if (pdl) pdl_wait();
   if (tr && threadIdx.x == 0) tr[8] = gtimer_ns();
-  stage_x();
-  if (!pdl && (flags & kFlagXFirst)) prefill();
+  uint4 xv = make_uint4(0, 0, 0, 0);
+  if (xtma) {
+    if (tid == 0) bulk_load_x(xs, x + (size_t)s0 * kTileK, (uint32_t)(Sc * kTileK * 2), xbar, pol_keep);
+  } else if (xthread) {
+    xv = ldg_keep(xsrc, pol_keep);
+  }
+  prefill(pre_n, D);
+  if (xtma) {
+    mbar_wait_parity0(xbar);
+    if (tr && threadIdx.x == 0) tr[9] = gtimer_ns();
+  } else if (xthread) {
+    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(xs + 16 * tid), "r"(xv.x), "r"(xv.y), "r"(xv.z),
+                 "r"(xv.w) : "memory");
+    if (tr && threadIdx.x == 0) tr[9] = gtimer_ns();
+  }
   __syncthreads();
   if (tr && threadIdx.x == 0) tr[1] = gtimer_ns();
   if (COLW) {   // one slice, one slot per plane built from x * 2^{e_i[k]}
@@ -379,6 +409,7 @@ gemv_cluster_kernel(const __half* __restrict__ x, const uint4* __restrict__ plan
   }
   __syncthreads();
   if (tr && threadIdx.x == 0) tr[2] = gtimer_ns();
+  cluster_wait();   // every peer's receive mbarrier is initialised (arrived at kernel start)
 
   // column bytes of steps 2c, 2c+1 for even slots (cstE) and odd slots (+128 B, cstO)
   uint32_t cstE[8], cstO[8];
@@ -409,7 +440,18 @@ gemv_cluster_kernel(const __half* __restrict__ x, const uint4* __restrict__ plan
         }
       }
       v += __shfl_xor_sync(0xffffffffu, v, 1);
-      if (h == 0) sts_f32(part + 4u * (uint32_t)((pc.t * RGb + pc.rgl) * kTileRows + r), v);
+      // a5, pushed as soon as the item is done: row pc.rgl*16 + r's partial of slice s0 + t
+      // goes to recv[s0 + t][row - o*chunk] of its owner o (st.async completes 4 bytes on the
+      // owner's mbarrier; the owner's own rows are plain stores, covered by its bar.sync)
+      if (h == 0 && push_end) {
+        sts_f32(part + 4u * (uint32_t)((pc.t * RGb + pc.rgl) * kTileRows + r), v);
+      } else if (h == 0) {
+        const int o = (int)(((float)pc.rgl + 0.5f) * inv_chunk_rg);
+        const uint32_t dst =
+            recv + 4u * (uint32_t)((s0 + pc.t) * chunk + (pc.rgl - o * chunk_rg) * kTileRows + r);
+        if (o == (int)rank) sts_f32(dst, v);
+        else st_async_f32(dst, bar, (uint32_t)o, v);
+      }
       pc.advance<NW>(RGb);
       if (m + D < Mw) {
         if (COLW) load_planes_unit<Q>(planes, (long long)(s0 + ld.t) * RG + rg0 + ld.rgl, lane, pol_stream, w[k]);
@@ -419,34 +461,26 @@ gemv_cluster_kernel(const __half* __restrict__ x, const uint4* __restrict__ plan
       }
     }
   }
-  __syncthreads();
+  __syncthreads();         // the CTA's own partials
   if (tr && threadIdx.x == 0) tr[3] = gtimer_ns();
-
-  // a5: each CTA sums its slices (t in order) per row and pushes the sum into the owner
-  // rank's receive buffer recv[rank][row - owner*chunk] with st.async, which completes 4
-  // bytes on the owner's mbarrier; the owner waits for exactly its (C-1)*cnt pushed sums --
-  // no cluster-wide barrier at the end, so finished CTAs leave (their slots go to the next
-  // kernel) while others still stream.  The owner then sums ranks 0..C-1 in order.
-  cluster_wait();   // every peer's mbarrier is initialised (arrived at kernel start)
-  for (int i = tid; i < rows; i += NW * 32) {
-    float v = 0.f;
-    for (int t = 0; t < Sc; ++t) v += lds_f32(part + 4u * (uint32_t)(t * rows + i));
-    const int o = i / chunk;
-    const uint32_t dst = recv + 4u * (uint32_t)(rank * chunk + (i - o * chunk));
-    if (o == (int)rank) sts_f32(dst, v);
-    else if (btail) st_dsmem_f32(dst, (uint32_t)o, v);
-    else st_async_f32(dst, bar, (uint32_t)o, v);
+  if (push_end) {   // 3-4 slices per CTA: sum them per row first, push one value per row
+    for (int i = tid; i < rows; i += NW * 32) {
+      float v = 0.f;
+      for (int t = 0; t < Sc; ++t) v += lds_f32(part + 4u * (uint32_t)(t * rows + i));
+      const int o = i / chunk;
+      const uint32_t dst = recv + 4u * (uint32_t)(rank * chunk + (i - o * chunk));
+      if (o == (int)rank) sts_f32(dst, v);
+      else st_async_f32(dst, bar, (uint32_t)o, v);
+    }
+    __syncthreads();
   }
-  if (btail) {
-    cluster_sync_full();     // measured alternative: one full cluster barrier
-  } else {
-    __syncthreads();         // the CTA's own sums
-    mbar_wait_parity0(bar);  // the peers' sums
-  }
+  mbar_wait_parity0(bar);  // the peers' partials
   if (tr && threadIdx.x == 0) tr[4] = gtimer_ns();
+  // the owner sums slices 0..S-1 of each of its rows in order (deterministic) and stores
   for (int j = tid; j < cnt; j += NW * 32) {
     float v = lds_f32(recv + 4u * (uint32_t)j);
-    for (int c = 1; c < C; ++c) v += lds_f32(recv + 4u * (uint32_t)(c * chunk + j));
+    const int nsrc = push_end ? C : S;   // ranks 0..C-1, or slices 0..S-1, in order
+    for (int s = 1; s < nsrc; ++s) v += lds_f32(recv + 4u * (uint32_t)(s * chunk + j));
     const int n = rg0 * kTileRows + own_lo + j;
     if (n < N) {
       const __half hv = __float2half_rn(v);
@@ -558,12 +592,16 @@ int max_clusters(int variant, int C) {
   return slot;
 }
 
-int x_first() {
-  static int v = env_int("SHIFTADD_CLUSTER_XFIRST", 0);
+int x_tma() {
+  static int v = env_int("SHIFTADD_X_TMA", 0);
   return v;
 }
-int barrier_tail() {
-  static int v = env_int("SHIFTADD_CLUSTER_BTAIL", 0);
+int push_end_mode() {
+  static int v = env_int("SHIFTADD_PUSH_END", -1);   // -1: at the end for 4-slot CTAs
+  return v;
+}
+int x_first() {
+  static int v = env_int("SHIFTADD_CLUSTER_XFIRST", 0);
   return v;
 }
 
@@ -591,7 +629,16 @@ cudaError_t launch_cluster_q(const GemmArgs& a, const LaunchPlan& p, int C) {
   unsigned long long* trace = nullptr;
   if (cluster_trace() && a.workspace && a.workspace_bytes >= kCounterBytes + (size_t)p.grid * 256)
     trace = reinterpret_cast<unsigned long long*>(static_cast<char*>(a.workspace) + kCounterBytes);
-  const int flags = (pdl ? kFlagPdl : 0) | (x_first() ? kFlagXFirst : 0) | (barrier_tail() ? kFlagBarrierTail : 0);
+  // ring slots requested before griddepcontrol.wait: ~pre_kb KB per CTA (what HBM delivers
+  // to an SM's share during the wait; more only delays x, which queues behind them)
+  constexpr int D = COLW ? cl_ring_colw(Q, REGS) : (AP2 ? cl_ring_ap2(Q, REGS) : cl_ring(Q, REGS));
+  static const int pre_kb = env_int("SHIFTADD_PRE_KB", 1024);
+  const int slot_bytes = (p.threads / 32) * Q * kTileBytes;
+  int pre = (pre_kb * 1024 + slot_bytes / 2) / slot_bytes;
+  pre = pre < 0 ? 0 : (pre > D ? D : pre);
+  const int flags = (pdl ? kFlagPdl : 0) | (x_first() ? kFlagXFirst : 0) | (pre << kPreShift) |
+                    (push_end_mode() > 0 || (push_end_mode() < 0 && SCM > 2) ? kFlagPushEnd : 0) |
+                    (x_tma() ? kFlagXTma : 0);
   return cudaLaunchKernelEx(&c, gemv_cluster_kernel<Q, SCM, NW, REGS, COLW, AP2>, a.x,
                             reinterpret_cast<const uint4*>(a.planes), a.exps, a.N, S, RG, C, a.y, flags, trace,
                             a.exps2, a.gather);

@@ -517,6 +517,247 @@ cudaError_t launch_q(const GemmArgs& a, const LaunchPlan& p) {
   }
 }
 
+
+// ------------------------------------------------------------------------------------------
+// TMA-ring variant for large layers (kernel id 4).  Same units, LUTs, lookup loop, shift and
+// split-K reduction as gemv_tiled_kernel; what changes is how the weights reach the SM.  The
+// register-ring kernel keeps at most D units per warp in flight (48 KB per SM at q = 3 with
+// 64 registers), which caps a long layer at bytes-in-flight / HBM latency.  Here one producer
+// thread streams the CTA's contiguous chunk of units with bulk copies (cp.async.bulk, the TMA
+// engine) into a ring of NST shared-memory stages of 16 units (~157 KB in flight at q = 3),
+// completing on a per-stage "full" mbarrier; 16 consumer warps take one unit each per stage
+// (LDS.128 of the lane's 16 key bytes per plane: conflict-free), look it up and release the
+// stage on its "empty" mbarrier.  One CTA per SM, grid = #SMs; a chunk spans at most two
+// slices (S < gridDim), whose LUTs are both built up front in the two column halves.
+constexpr int kStreamNWC = 16;     // consumer warps
+constexpr int kStageUnits = 16;    // units per stage: one per consumer warp
+
+template <int Q>
+struct StreamSmem {
+  static constexpr int lut = kLutBytes;
+  static constexpr int stage_planes = kStageUnits * Q * kTileBytes;
+  static constexpr int stage_exps = kStageUnits * Q * kTileExps;
+  static constexpr int stage = stage_planes + stage_exps;
+  static constexpr int budget = 227 * 1024 - lut - 256;
+  static constexpr int nst = budget / stage > 8 ? 8 : budget / stage;
+  static constexpr int ring = nst * stage;
+  static constexpr int bars = 128;   // full[8] at +0, empty[8] at +64
+  static constexpr int total = lut + ring + bars;
+};
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      ::"r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(pol) : "memory");
+}
+__device__ __forceinline__ uint4 lds_u4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ int lds_s8(uint32_t addr) {
+  int v;
+  asm volatile("ld.shared.s8 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
+template <int Q>
+__global__ void __launch_bounds__((kStreamNWC + 1) * 32, 1)
+gemv_stream_kernel(const __half* __restrict__ x, const uint8_t* __restrict__ planes,
+                   const int8_t* __restrict__ exps, int N, int S, int RG, long long U,
+                   __half* __restrict__ y, float* __restrict__ partial, unsigned* __restrict__ cnt, int pdl,
+                   int npre, int loads_only) {
+  using SM = StreamSmem<Q>;
+  constexpr int NST = SM::nst;
+  constexpr int NWC = kStreamNWC;
+  if (threadIdx.x == 0) check_dyn_base();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NT = (NWC + 1) * 32;
+  const long long G = gridDim.x;
+  const unsigned Uu = (unsigned)U, Gu = (unsigned)G, qq = Uu / Gu, rr = Uu % Gu, cb = blockIdx.x;
+  const long long u0 = (long long)(cb * qq + (cb * rr) / Gu);
+  const long long u1 = (long long)((cb + 1) * qq + ((cb + 1) * rr) / Gu);
+  const int Npad = RG * kTileRows;
+  const uint32_t ring = kDynBase + SM::lut;
+  const uint32_t full = ring + SM::ring, empty = full + 64;
+  if (tid == 0) {
+    for (int j = 0; j < NST; ++j) {
+      mbar_init(full + 8 * j, 1);
+      mbar_init(empty + 8 * j, NWC);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  if (pdl) pdl_launch_dependents();
+  const int nstages = (int)((u1 - u0 + kStageUnits - 1) / kStageUnits);
+
+  if (warp == NWC) {
+    // producer: stages [0, npre) before griddepcontrol.wait (weights never depend on the
+    // upstream kernel; more would only queue x behind them), the rest as slots free up
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      for (int t = 0; t < nstages; ++t) {
+        if (t == npre && pdl) pdl_wait();
+        const int j = t % NST;
+        if (t >= NST) mbar_wait(empty + 8 * j, (uint32_t)((t / NST - 1) & 1));
+        const long long ub = u0 + (long long)t * kStageUnits;
+        const int n = (int)min((long long)kStageUnits, u1 - ub);
+        const uint32_t bp = (uint32_t)(n * Q * kTileBytes), be = (uint32_t)(n * Q * kTileExps);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full + 8 * j), "r"(bp + be)
+                     : "memory");
+        bulk_g2s(ring + j * SM::stage, planes + (size_t)ub * Q * kTileBytes, bp, full + 8 * j, pol);
+        bulk_g2s(ring + j * SM::stage + SM::stage_planes, exps + (size_t)ub * Q * kTileExps, be, full + 8 * j, pol);
+      }
+    }
+  } else {
+    // consumers: the LUTs of the (at most two) slices of the chunk, then the ring
+    const int s_first = (int)((unsigned)u0 / (unsigned)RG);
+    const int s_last = u1 > u0 ? (int)((unsigned)(u1 - 1) / (unsigned)RG) : s_first;
+    const uint64_t pol_keep = policy_evict_last();
+    if (pdl) pdl_wait();
+    const uint4 xa = ldg_keep(x + (size_t)s_first * kTileK + 8 * lane, pol_keep);
+    uint4 xb = xa;
+    if (s_last != s_first) xb = ldg_keep(x + (size_t)s_last * kTileK + 8 * lane, pol_keep);
+    build_lut<NWC>(xa, 0u, warp, lane);
+    if (s_last != s_first) build_lut<NWC>(xb, 128u, warp, lane);
+    asm volatile("bar.sync 1, %0;" ::"r"(NWC * 32) : "memory");   // consumer warps only
+    const int r = lane >> 1, h = lane & 1;
+    uint32_t cst[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint32_t v = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) v |= (4u * (uint32_t)(16 * h + ((4 * k + b + r) & 15))) << (8 * b);
+      cst[k] = v;
+    }
+    SegCtx c{nullptr, nullptr, N, S, Npad, 0, y, partial, cnt, 0};
+    for (int t = 0; t < nstages; ++t) {
+      const int j = t % NST;
+      const long long u = u0 + (long long)t * kStageUnits + warp;
+      mbar_wait(full + 8 * j, (uint32_t)((t / NST) & 1));
+      if (u < u1) {
+        uint4 w[Q];
+        int e[Q];
+        const uint32_t sp = ring + j * SM::stage + warp * Q * kTileBytes + 16 * lane;
+        const uint32_t se = ring + j * SM::stage + SM::stage_planes + warp * Q * kTileExps + lane;
+#pragma unroll
+        for (int i = 0; i < Q; ++i) w[i] = lds_u4(sp + i * kTileBytes);
+#pragma unroll
+        for (int i = 0; i < Q; ++i) e[i] = lds_s8(se + i * kTileExps);
+        const int s = (int)((unsigned)u / (unsigned)RG);
+        const float acc = loads_only ? unit_xor<Q>(w, e)   // experiment: the ring without lookups
+                                     : s == s_first ? unit_dot<Q, 0, 0u>(w, e, cst) : unit_dot<Q, 0, 128u>(w, e, cst);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + 8 * j);   // the unit's bytes are consumed
+        c.rg_base = (long long)s * RG;
+        emit<Q, 0>(acc, c, s, u, r, h);
+      } else {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + 8 * j);
+      }
+    }
+  }
+  if (S == 1) return;
+  // a5 as in gemv_tiled_kernel: one fence per CTA, relaxed arrivals per unit, owners poll
+  // their row groups' counters, sum the S partials in slice order, store fp16, re-arm.
+  const int own0 = (int)(((long long)blockIdx.x * RG) / G);
+  const int own1 = (int)(((long long)(blockIdx.x + 1) * RG) / G);
+  const int n0 = own0 * kTileRows;
+  const int R = (own1 - own0) * kTileRows;
+  __syncthreads();
+  if (tid == 0) __threadfence();
+  __syncthreads();
+  for (long long uq = u0 + tid; uq < u1; uq += NT)
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(cnt + ((unsigned)uq % (unsigned)RG)) : "memory");
+  for (int rg = own0 + tid; rg < own1; rg += NT)
+    while (ld_acquire_gpu(cnt + rg) < (unsigned)S) {
+    }
+  __syncthreads();
+  int T = 1;
+  while (T < 32 && 2 * T <= S && (R * 2 * T <= NT || S > 16 * T)) T *= 2;
+  const int items = R * T;
+  const int items_pad = (items + 31) & ~31;
+  for (int it = tid; it < items_pad; it += NT) {
+    const bool live = it < items;
+    const int n = n0 + it / T;
+    const int part = it & (T - 1);
+    float sum = 0.f;
+    if (live) {
+      const float* p = partial + n;
+      for (int s = part; s < S; s += 16 * T) {
+        float v[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k] = s + k * T < S ? __ldcg(p + (size_t)(s + k * T) * Npad) : 0.f;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) sum += v[k];
+      }
+    }
+    for (int off = T >> 1; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+    if (live && part == 0 && n < N) y[n] = __float2half_rn(sum);
+  }
+  for (int rg = own0 + tid; rg < own1; rg += NT) cnt[rg] = 0u;   // for the next call
+}
+
+template <int Q>
+cudaError_t launch_stream_q(const GemmArgs& a, const LaunchPlan& p) {
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(gemv_stream_kernel<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    StreamSmem<Q>::total);
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  const int S = a.K / kTileK;
+  const int RG = (a.N + kTileRows - 1) / kTileRows;
+  const long long U = (long long)S * RG;
+  unsigned* sync = reinterpret_cast<unsigned*>(a.workspace);
+  float* partial = reinterpret_cast<float*>(reinterpret_cast<char*>(a.workspace) + kCounterBytes);
+  const int pdl = (a.flags & SHIFTADD_FLAG_PDL) ? 1 : 0;
+  static const int npre = [] {
+    const char* e = std::getenv("SHIFTADD_STREAM_PRE");
+    return e ? std::atoi(e) : 2;
+  }();
+  static const int loads_only = [] {
+    const char* e = std::getenv("SHIFTADD_STREAM_LOADS_ONLY");
+    return e ? std::atoi(e) : 0;
+  }();
+  cudaLaunchConfig_t c = {};
+  c.gridDim = dim3(p.grid);
+  c.blockDim = dim3(p.threads);
+  c.dynamicSmemBytes = p.smem;
+  c.stream = a.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  c.attrs = attr;
+  c.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&c, gemv_stream_kernel<Q>, a.x, a.planes, a.exps, a.N, S, RG, U, a.y, partial, sync,
+                            pdl, npre, loads_only);
+}
+
+int stream_smem(int q) {
+  switch (q) {
+    case 1: return StreamSmem<1>::total;
+    case 2: return StreamSmem<2>::total;
+    case 3: return StreamSmem<3>::total;
+    default: return StreamSmem<4>::total;
+  }
+}
+
 }  // namespace
 
 LaunchPlan plan_gemv_tiled(int N, int K, int q, int sms) {
@@ -540,6 +781,24 @@ LaunchPlan plan_gemv_tiled(int N, int K, int q, int sms) {
   return LaunchPlan{(int)grid, kVariants[cfg().variant].nw * 32, kDynSmem, 1};
 }
 
+// Large layers (more than ~64 units per SM, chunks within two slices) stream through the
+// TMA ring (kernel 4); SHIFTADD_STREAM=0 keeps them on the register-ring kernel.
+bool stream_applicable(int N, int K, int q, int sms) {
+  static const int on = [] {
+    const char* e = std::getenv("SHIFTADD_STREAM");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (!on || q < 1 || q > 4) return false;
+  const long long S = K / kTileK;
+  const long long RG = (N + kTileRows - 1) / kTileRows;
+  return S > 1 && S < sms && S * RG >= 64LL * sms;
+}
+
+LaunchPlan plan_gemv_stream(int N, int K, int q, int sms) {
+  (void)N; (void)K;
+  return LaunchPlan{sms, (kStreamNWC + 1) * 32, stream_smem(q), 4};
+}
+
 size_t workspace_gemv_tiled(int N, int K) {
   const size_t S = K / kTileK;
   if (S <= 1) return 0;
@@ -548,6 +807,15 @@ size_t workspace_gemv_tiled(int N, int K) {
 }
 
 cudaError_t launch_gemv_tiled(const GemmArgs& a, const LaunchPlan& p) {
+  if (p.kernel == 4) {
+    switch (a.q) {
+      case 1: return launch_stream_q<1>(a, p);
+      case 2: return launch_stream_q<2>(a, p);
+      case 3: return launch_stream_q<3>(a, p);
+      case 4: return launch_stream_q<4>(a, p);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (a.q) {
     case 1: return launch_q<1>(a, p);
     case 2: return launch_q<2>(a, p);

@@ -102,6 +102,10 @@ SHAPES = [
     (1, 4000, 3072, 128),  # cluster kernel, C = 3 (12 slices)
     (1, 12000, 4096, 128), # cluster kernel, C = 4, 23 row groups per band
     (3, 1000, 11008, 128), # cluster kernel, 43 slices over clusters of 11 (uneven split)
+    (3, 4736, 8192, 128),  # TMA-ring kernel: 64 units per CTA, chunks straddle slices
+    (2, 4700, 8448, 128),  # TMA-ring kernel, ragged rows, 33 slices
+    (4, 2400, 16384, 128), # TMA-ring kernel, q = 4 (4-stage ring)
+    (1, 9500, 4096, 128),  # cluster kernel; forced split-K -> TMA ring, q = 1 (8 stages)
 ]
 # (layout, force split-K): the tiled M = 1 path has two decompositions
 KERNELS = [(1, False), (1, True), (0, False)]
@@ -164,14 +168,16 @@ def test_mixed_bit_dispatch_interleaved(sa):
 # ------------------------------------------------------------ full-size config parity
 def test_m1_kernel_choice(sa):
     """Cluster split-K for K <= 4096 (and larger K up to 12 MB of planes, clusters of <= 16)
-    with <= 128 row groups per band; grid split-K otherwise."""
+    with <= 128 row groups per band; else grid split-K through the TMA ring for >= 64 units
+    per SM and S < #SMs, the register-ring split-K otherwise."""
     def kid(N, K, M=1, q=1):
         signs, alpha = synth.gen_layer(q, N, K, 128, seed=1, device=DEV)
         return sa.gemm_plan(sa.pack(signs, alpha, 128, layout=sa.LAYOUT_TILED), M)[3]
     assert kid(4096, 4096) == 3 and kid(16384, 4096) == 3 and kid(256, 256) == 3 and kid(768, 768) == 3
-    assert kid(2048, 8192) == 3 and kid(28672, 8192, q=3) == 1
+    assert kid(2048, 8192) == 3 and kid(28672, 8192, q=3) == 4   # 70B gate/up: TMA ring
     assert kid(4096, 11008, q=1) == 3                     # 5.6 MB: clusters of 11 (non-portable)
-    assert kid(4096, 11008, q=3) == 1 and kid(80000, 4096) == 1
+    assert kid(4096, 11008, q=3) == 4 and kid(80000, 4096) == 4
+    assert kid(8192, 2048 * 20) == 1                      # S = 160 >= #SMs: register ring
     assert kid(4096, 4096, M=2) == 2
 
 
@@ -317,3 +323,21 @@ def test_gpu_rejects_bad_arguments(sa):
         sa.lut_gemm(x, layer)
     with pytest.raises(ValueError):
         sa.lut_gemm(x[:1, :256], layer)
+
+
+def test_tma_ring_kernel_exact_invariants(sa):
+    """Kernel 4 (TMA weight ring, chunks straddling two slices): y(-x) = -y(x) bit-exactly,
+    run-to-run bit-identical with and without PDL, counters left zeroed."""
+    q, N, K, g = 3, 4736, 8192, 128
+    signs, alpha = synth.gen_layer(q, N, K, g, seed=synth.seed_for(6, 4), device=DEV)
+    layer = sa.pack(signs, alpha, g, layout=sa.LAYOUT_TILED)
+    assert sa.gemm_plan(layer, 1)[3] == 4
+    ws = sa.Workspace(DEV)
+    x = synth.gen_x(1, K, seed=11).to(DEV)
+    ys = [sa.lut_gemm(x, layer, workspace=ws, pdl=bool(i & 1)).clone() for i in range(4)]
+    yn = sa.lut_gemm(-x, layer, workspace=ws)
+    torch.cuda.synchronize()
+    for y in ys[1:]:
+        assert torch.equal(y, ys[0])
+    assert torch.equal(yn.float(), -ys[0].float())
+    assert int(ws.buf[:65536 * 4].count_nonzero()) == 0
