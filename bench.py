@@ -51,7 +51,8 @@ def alg_bytes(M, q, N, K, g=G):
 
 
 KERNEL_NAMES = {0: "gemm_generic_kernel", 1: "gemv_tiled_kernel (grid split-K)", 2: "gemm_tiled_mb_kernel",
-                3: "gemv_cluster_kernel (cluster split-K)"}
+                3: "gemv_cluster_ring_kernel (cluster split-K, TMA weight ring)",
+                4: "gemv_stream_kernel (grid split-K, TMA weight ring)"}
 
 
 def kernel_names(layers):

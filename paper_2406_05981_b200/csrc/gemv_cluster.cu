@@ -105,8 +105,9 @@ __device__ __forceinline__ void mbar_init1(uint32_t bar) {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 __device__ __forceinline__ void bulk_load_x(uint32_t dst, const void* src, uint32_t bytes, uint32_t xbar,
-                                            uint64_t pol) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(xbar), "r"(bytes) : "memory");
+                                            uint64_t pol, bool expect = true) {
+  if (expect)
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(xbar), "r"(bytes) : "memory");
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
       ::"r"(dst), "l"(src), "r"(bytes), "r"(xbar), "l"(pol) : "memory");
@@ -502,6 +503,201 @@ gemv_cluster_kernel(const __half* __restrict__ x, const uint4* __restrict__ plan
   }
 }
 
+
+// ------------------------------------------------------------------------------------------
+// TMA-ring variant of the 2-slot cluster kernel (the default for K <= 4096).  Same items,
+// LUT slots, lookups, in-loop DSMEM push and owner reduction as gemv_cluster_kernel; the
+// weights reach shared memory through the bulk-copy engine instead of a per-warp register
+// ring of LDGs.  Measured on the register ring: with ~96 KB of weight loads in the LSU queue
+// when griddepcontrol.wait returns, x (and so the LUT build) waited ~1 us behind them on
+// FC1, and shrinking the ring left HBM idle during the wait.  Here one producer thread
+// (warp 16) streams the CTA's items -- for each of its slices a contiguous range of units --
+// in stages of 16 items (one per consumer warp) into a ring of NST stages, completing on the
+// stage's "full" mbarrier, from kernel start on (weights never depend on the upstream
+// kernel); the 16 consumer warps fetch x with nothing ahead of it, build the LUTs and take
+// one item per stage (LDS.128 of the lane's 16 key bytes per plane, conflict-free), then
+// release the stage on its "empty" mbarrier.
+constexpr int kRingNW = 16;                       // consumer warps
+constexpr int kRingBytes = 124 * 1024;            // stages + their 2 x 8 mbarriers
+constexpr int kRingBase = (Smem<2>::total + 127) & ~127;
+static_assert(kRingBase + kRingBytes <= 227 * 1024, "ring must fit");
+
+template <int Q>
+struct RingCfg {
+  static constexpr int stage_planes = kRingNW * Q * kTileBytes;
+  static constexpr int stage = kRingNW * Q * (kTileBytes + kTileExps);
+  static constexpr int nst = (kRingBytes - 128) / stage > 8 ? 8 : (kRingBytes - 128) / stage;
+  static constexpr int bars = nst * stage;          // full[j] at +8j, empty[j] at +64+8j
+  static constexpr int smem = kRingBase + kRingBytes;
+};
+
+__device__ __forceinline__ void rmbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void rmbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+  } while (!done);
+}
+
+template <int Q>
+__global__ void __launch_bounds__((kRingNW + 1) * 32, 1)
+gemv_cluster_ring_kernel(const __half* __restrict__ x, const uint8_t* __restrict__ planes,
+                         const int8_t* __restrict__ exps, int N, int S, int RG, int C, __half* __restrict__ y,
+                         int flags, unsigned long long* __restrict__ trace, GatherArgs ga) {
+  using RC = RingCfg<Q>;
+  constexpr int NW = kRingNW, NST = RC::nst;
+  const bool pdl = flags & kFlagPdl;
+  if (threadIdx.x == 0) check_dyn_base();
+  unsigned long long* tr = trace ? trace + 32 * blockIdx.x : nullptr;   // dev trace
+  if (tr && threadIdx.x == 0) tr[0] = gtimer_ns();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NT = (NW + 1) * 32;
+  const int r = lane >> 1, h = lane & 1;
+  const uint32_t rank = cluster_rank();
+  const unsigned Cu = (unsigned)C, ncl = gridDim.x / Cu, cl = blockIdx.x / Cu;
+  const int rg0 = (int)((cl * (unsigned)RG) / ncl);
+  const int RGb = (int)(((cl + 1) * (unsigned)RG) / ncl) - rg0;
+  const int s0 = (int)((rank * (unsigned)S) / Cu);
+  const int Sc = (int)(((rank + 1) * (unsigned)S) / Cu) - s0;   // <= 2
+  const int Mc = Sc * RGb;                                        // items: i = t * RGb + rgl
+  if (pdl) pdl_launch_dependents();
+
+  const uint32_t base = dyn_smem_base_cluster();   // kDynBase | rank << 24
+  const uint32_t xs = base + Smem<2>::lut;
+  const uint32_t recv = xs + Smem<2>::xstage;
+  const uint32_t bar = recv + Smem<2>::recv + Smem<2>::part;
+  const uint32_t ring = base + (uint32_t)kRingBase;
+  const uint32_t full = ring + RC::bars, empty = full + 64;
+  // a5 set-up as in gemv_cluster_kernel (in-loop push of every (slice, row) partial)
+  const int chunk_rg = (RGb + C - 1) / C;
+  const int chunk = chunk_rg * kTileRows;
+  const int rows = RGb * kTileRows;
+  const int own_lo = (int)rank * chunk;
+  const int cnt = rows - own_lo < chunk ? (rows - own_lo > 0 ? rows - own_lo : 0) : chunk;
+  const float inv_chunk_rg = 1.f / (float)chunk_rg;
+  if (tid == 0) {
+    mbar_init_expect(bar, (uint32_t)((S - Sc) * cnt * 4));
+    for (int j = 0; j < NST; ++j) {
+      rmbar_init(full + 8 * j, 1);
+      rmbar_init(empty + 8 * j, NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  cluster_arrive_relaxed();
+  const int nstages = (Mc + NW - 1) / NW;
+
+  if (warp == NW) {
+    // producer: stage t = items [16t, 16t + 16), one contiguous unit range per slice
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      for (int t = 0; t < nstages; ++t) {
+        const int j = t % NST;
+        if (t >= NST) rmbar_wait(empty + 8 * j, (uint32_t)((t / NST - 1) & 1));
+        const int i0 = t * NW, i1 = i0 + NW < Mc ? i0 + NW : Mc;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full + 8 * j),
+                     "r"((uint32_t)((i1 - i0) * Q * (kTileBytes + kTileExps))) : "memory");
+        for (int a = i0; a < i1;) {
+          const int ts = a >= RGb ? 1 : 0;
+          const int b = (ts + 1) * RGb < i1 ? (ts + 1) * RGb : i1;
+          const long long u = (long long)(s0 + ts) * RG + rg0 + (a - ts * RGb);
+          const uint32_t dst = ring + (uint32_t)(j * RC::stage);
+          bulk_load_x(dst + (uint32_t)((a - i0) * Q * kTileBytes), planes + u * Q * kTileBytes,
+                      (uint32_t)((b - a) * Q * kTileBytes), full + 8 * j, pol, false);
+          bulk_load_x(dst + (uint32_t)(RC::stage_planes + (a - i0) * Q * kTileExps), exps + u * Q * kTileExps,
+                      (uint32_t)((b - a) * Q * kTileExps), full + 8 * j, pol, false);
+          a = b;
+        }
+      }
+    }
+  } else {
+    if (pdl) pdl_wait();
+    if (tr && tid == 0) tr[8] = gtimer_ns();
+    if (tid < Sc * (kTileK / 8)) {   // one 16-B chunk of x per thread
+      const uint4 xv = ldg_keep(reinterpret_cast<const uint4*>(x + (size_t)s0 * kTileK) + tid, policy_evict_last());
+      asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(xs + 16 * tid), "r"(xv.x), "r"(xv.y), "r"(xv.z),
+                   "r"(xv.w) : "memory");
+      if (tr && tid == 0) tr[9] = gtimer_ns();
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");   // consumer warps only
+    if (tr && tid == 0) tr[1] = gtimer_ns();
+    for (int t = 0; t < 2; ++t)
+      if (t < Sc) build_lut_slot<NW>(base + (uint32_t)t * 128u, xs + t * (kTileK * 2), warp, lane);
+    asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+    if (tr && tid == 0) tr[2] = gtimer_ns();
+    cluster_wait();   // every peer's receive mbarrier is initialised
+    uint32_t cstE[8], cstO[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint32_t c0 = 4u * (uint32_t)(16 * h + ((2 * c + r) & 15));
+      const uint32_t c1 = 4u * (uint32_t)(16 * h + ((2 * c + 1 + r) & 15));
+      cstE[c] = c0 | (c1 << 8) | (rank << 16);
+      cstO[c] = cstE[c] + 0x8080u;
+    }
+    for (int t = 0; t < nstages; ++t) {
+      const int j = t % NST;
+      const int i = t * NW + warp;
+      rmbar_wait(full + 8 * j, (uint32_t)((t / NST) & 1));
+      if (i < Mc) {
+        uint4 w[Q];
+        int e[Q];
+        const uint32_t sp = ring + (uint32_t)(j * RC::stage + warp * Q * kTileBytes + 16 * lane);
+        const uint32_t se = ring + (uint32_t)(j * RC::stage + RC::stage_planes + warp * Q * kTileExps + lane);
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+          asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(w[k].x), "=r"(w[k].y), "=r"(w[k].z),
+                       "=r"(w[k].w) : "r"(sp + (uint32_t)(k * kTileBytes)));
+          asm volatile("ld.shared.s8 %0, [%1];" : "=r"(e[k]) : "r"(se + (uint32_t)(k * kTileExps)));
+        }
+        const int ts = i >= RGb ? 1 : 0, rgl = i - ts * RGb;
+        float v = ts ? unit_dot_c<Q, kDynBase, false>(w, e, e, cstO) : unit_dot_c<Q, kDynBase, false>(w, e, e, cstE);
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty + 8 * j) : "memory");
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        if (h == 0) {   // a5 push, as in gemv_cluster_kernel
+          const int o = (int)(((float)rgl + 0.5f) * inv_chunk_rg);
+          const uint32_t dst = recv + 4u * (uint32_t)((s0 + ts) * chunk + (rgl - o * chunk_rg) * kTileRows + r);
+          if (o == (int)rank) sts_f32(dst, v);
+          else st_async_f32(dst, bar, (uint32_t)o, v);
+        }
+      } else {
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty + 8 * j) : "memory");
+      }
+    }
+  }
+  __syncthreads();         // the CTA's own partials
+  if (tr && threadIdx.x == 0) tr[3] = gtimer_ns();
+  mbar_wait_parity0(bar);  // the peers' partials
+  if (tr && threadIdx.x == 0) tr[4] = gtimer_ns();
+  for (int jj = tid; jj < cnt; jj += NT) {
+    float v = lds_f32(recv + 4u * (uint32_t)jj);
+    for (int s = 1; s < S; ++s) v += lds_f32(recv + 4u * (uint32_t)(s * chunk + jj));
+    const int n = rg0 * kTileRows + own_lo + jj;
+    if (n < N) {
+      const __half hv = __float2half_rn(v);
+      if (ga.P == 0) {
+        y[n] = hv;
+      } else {   // NEXT-f3: store straight into every rank's gathered y (peer memory)
+        const int b = (int)((*ga.epoch + 1u) & 1u);
+        for (int rr = 0; rr < ga.P; ++rr) ga.y_peers[b * ga.P + rr][(size_t)ga.rank * N + n] = hv;
+      }
+    }
+  }
+  if (ga.P > 0) gather_signal(ga);
+  if (tr && threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    tr[5] = gtimer_ns();
+    tr[6] = smid;
+    tr[7] = (unsigned long long)nstages;
+  }
+}
+
 int env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
   return e ? std::atoi(e) : dflt;
@@ -520,7 +716,7 @@ int cluster_trace() {
 // stream takes its place and, under PDL, prefetches its weights while this kernel's tail
 // (cluster barrier, reduction) runs.  FULL4: 16 warps, 4 slots (170 KB, one CTA per SM),
 // for K up to 8192 with clusters of <= 8.
-enum Variant { kHalf = 0, kFull2 = 1, kFull4 = 2, kColw = 3 };
+enum Variant { kHalf = 0, kFull2 = 1, kFull4 = 2, kColw = 3, kRing = 4 };
 struct ClusterShape {
   int variant;
   int sc;   // max slices per CTA
@@ -534,12 +730,47 @@ ClusterShape cluster_shape(int N, int K, int q) {
   const int S = K / kTileK;
   const int sc = forced_sc > 0 ? (forced_sc > kMaxSc ? kMaxSc : forced_sc) : ((S + 1) / 2 <= kMaxC ? 2 : kMaxSc);
   // (S + sc - 1) / sc may exceed the portable 8: clusters of up to 16 are non-portable
-  const int variant = sc > 2 ? kFull4 : (half ? kHalf : kFull2);
+  static const int ring = env_int("SHIFTADD_RING", 1);
+  const int variant = sc > 2 ? kFull4 : (half ? kHalf : (ring ? kRing : kFull2));
   return ClusterShape{variant, sc, (S + sc - 1) / sc};
 }
 
-int variant_threads(int v) { return v == kHalf ? 8 * 32 : 16 * 32; }
-int variant_smem(int v) { return v == kFull4 ? Smem<4>::total : Smem<2>::total; }
+int variant_threads(int v) { return v == kHalf ? 8 * 32 : v == kRing ? (kRingNW + 1) * 32 : 16 * 32; }
+int variant_smem(int v) { return v == kFull4 ? Smem<4>::total : v == kRing ? RingCfg<1>::smem : Smem<2>::total; }
+
+template <int Q>
+cudaError_t set_ring_attrs() {
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [] {
+    err = cudaFuncSetAttribute(gemv_cluster_ring_kernel<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               RingCfg<Q>::smem);
+    if (err == cudaSuccess)
+      err = cudaFuncSetAttribute(gemv_cluster_ring_kernel<Q>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  });
+  return err;
+}
+
+int occupancy_ring_clusters(int C) {
+  if (set_ring_attrs<2>() != cudaSuccess) return 0;
+  cudaLaunchConfig_t c = {};
+  c.gridDim = dim3(C * 64);
+  c.blockDim = dim3((kRingNW + 1) * 32);
+  c.dynamicSmemBytes = RingCfg<2>::smem;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = C;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  c.attrs = &attr;
+  c.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, gemv_cluster_ring_kernel<2>, &c) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  return n;
+}
 
 template <int Q, int SCM, int NW, int REGS, bool COLW = false, bool AP2 = false>
 cudaError_t set_attrs() {
@@ -579,7 +810,7 @@ int occupancy_clusters(int C) {
 
 // Max co-resident clusters of size C for a variant (cached).
 int max_clusters(int variant, int C) {
-  static int cache[4][kMaxCColw + 1] = {};
+  static int cache[5][kMaxCColw + 1] = {};
   static std::mutex mu;
   std::lock_guard<std::mutex> g(mu);
   int& slot = cache[variant][C];
@@ -587,6 +818,7 @@ int max_clusters(int variant, int C) {
   const int n = variant == kHalf    ? occupancy_clusters<2, 8>(C)
                 : variant == kFull2 ? occupancy_clusters<2, 16>(C)
                 : variant == kFull4 ? occupancy_clusters<4, 16>(C)
+                : variant == kRing  ? occupancy_ring_clusters(C)
                                     : occupancy_clusters<4, 16, true>(C);
   slot = n > 0 ? n : -1;
   return slot;
@@ -642,6 +874,34 @@ cudaError_t launch_cluster_q(const GemmArgs& a, const LaunchPlan& p, int C) {
   return cudaLaunchKernelEx(&c, gemv_cluster_kernel<Q, SCM, NW, REGS, COLW, AP2>, a.x,
                             reinterpret_cast<const uint4*>(a.planes), a.exps, a.N, S, RG, C, a.y, flags, trace,
                             a.exps2, a.gather);
+}
+
+template <int Q>
+cudaError_t launch_ring_q(const GemmArgs& a, const LaunchPlan& p, int C) {
+  const cudaError_t ae = set_ring_attrs<Q>();
+  if (ae != cudaSuccess) return ae;
+  const int S = a.K / kTileK;
+  const int RG = (a.N + kTileRows - 1) / kTileRows;
+  const int pdl = (a.flags & SHIFTADD_FLAG_PDL) ? 1 : 0;
+  cudaLaunchConfig_t c = {};
+  c.gridDim = dim3(p.grid);
+  c.blockDim = dim3((kRingNW + 1) * 32);
+  c.dynamicSmemBytes = RingCfg<Q>::smem;
+  c.stream = a.stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  c.attrs = attr;
+  c.numAttrs = pdl ? 2 : 1;
+  unsigned long long* trace = nullptr;
+  if (cluster_trace() && a.workspace && a.workspace_bytes >= kCounterBytes + (size_t)p.grid * 256)
+    trace = reinterpret_cast<unsigned long long*>(static_cast<char*>(a.workspace) + kCounterBytes);
+  return cudaLaunchKernelEx(&c, gemv_cluster_ring_kernel<Q>, a.x, a.planes, a.exps, a.N, S, RG, C, a.y,
+                            pdl ? kFlagPdl : 0, trace, a.gather);
 }
 
 template <int SCM, int NW, bool AP2 = false>
@@ -757,12 +1017,31 @@ cudaError_t launch_gemv_colwise(const GemmArgs& a) {
 
 cudaError_t launch_gemv_cluster(const GemmArgs& a, const LaunchPlan& p) {
   const ClusterShape cs = cluster_shape(a.N, a.K, a.q);
+  if (cs.variant == kRing && !a.exps2 && !(reinterpret_cast<uintptr_t>(a.exps) & 15)) {
+    switch (a.q) {   // the TMA ring (its bulk copies need 16-B aligned exponent tiles)
+      case 1: return launch_ring_q<1>(a, p, cs.C);
+      case 2: return launch_ring_q<2>(a, p, cs.C);
+      case 3: return launch_ring_q<3>(a, p, cs.C);
+      case 4: return launch_ring_q<4>(a, p, cs.C);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  LaunchPlan pp = p;
+  if (cs.variant == kRing) {   // register-ring kernel instead: its own launch shape
+    const int RG = (a.N + kTileRows - 1) / kTileRows;
+    const int ncl = max_clusters(kFull2, cs.C);
+    if (ncl <= 0) return cudaErrorNotSupported;
+    const int bands = ncl < RG ? ncl : RG;
+    if ((RG + bands - 1) / bands > kMaxRGb) return cudaErrorNotSupported;
+    pp = LaunchPlan{bands * cs.C, variant_threads(kFull2), variant_smem(kFull2), 3};
+  }
   if (a.exps2)   // NEXT-f2: additive PoT K = 2 (16-warp variants only)
-    return cs.sc <= 2 ? launch_cluster_v<2, 16, true>(a, p, cs.C) : launch_cluster_v<4, 16, true>(a, p, cs.C);
+    return cs.sc <= 2 ? launch_cluster_v<2, 16, true>(a, pp, cs.C) : launch_cluster_v<4, 16, true>(a, pp, cs.C);
   switch (cs.variant) {
-    case kHalf: return launch_cluster_v<2, 8>(a, p, cs.C);
-    case kFull2: return launch_cluster_v<2, 16>(a, p, cs.C);
-    default: return launch_cluster_v<4, 16>(a, p, cs.C);
+    case kHalf: return launch_cluster_v<2, 8>(a, pp, cs.C);
+    case kFull2:
+    case kRing: return launch_cluster_v<2, 16>(a, pp, cs.C);
+    default: return launch_cluster_v<4, 16>(a, pp, cs.C);
   }
 }
 

@@ -367,7 +367,7 @@ gemv_tiled_kernel(const __half* __restrict__ x, const uint4* __restrict__ planes
   if (dyn_kc == 0) {
     if (!unit_release) {
       __syncthreads();
-      if (tid == 0) __threadfence();
+      if (tid == 0) asm volatile("fence.acq_rel.gpu;" ::: "memory");   // release: the CTA's partials before its arrivals
       __syncthreads();
       for (long long uq = u0 + tid; uq < u1; uq += NW * 32)
         asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(cnt + ((unsigned)uq % (unsigned)RG)) : "memory");
@@ -579,8 +579,10 @@ __global__ void __launch_bounds__((kStreamNWC + 1) * 32, 1)
 gemv_stream_kernel(const __half* __restrict__ x, const uint8_t* __restrict__ planes,
                    const int8_t* __restrict__ exps, int N, int S, int RG, long long U,
                    __half* __restrict__ y, float* __restrict__ partial, unsigned* __restrict__ cnt, int pdl,
-                   int npre, int loads_only) {
+                   int npre, int loads_only, unsigned long long* __restrict__ trace) {
   using SM = StreamSmem<Q>;
+  unsigned long long* tr = trace ? trace + 16 * blockIdx.x : nullptr;   // dev trace
+  if (tr && threadIdx.x == 0) tr[0] = gtimer();
   constexpr int NST = SM::nst;
   constexpr int NWC = kStreamNWC;
   if (threadIdx.x == 0) check_dyn_base();
@@ -629,12 +631,14 @@ gemv_stream_kernel(const __half* __restrict__ x, const uint8_t* __restrict__ pla
     const int s_last = u1 > u0 ? (int)((unsigned)(u1 - 1) / (unsigned)RG) : s_first;
     const uint64_t pol_keep = policy_evict_last();
     if (pdl) pdl_wait();
+    if (tr && tid == 0) tr[1] = gtimer();
     const uint4 xa = ldg_keep(x + (size_t)s_first * kTileK + 8 * lane, pol_keep);
     uint4 xb = xa;
     if (s_last != s_first) xb = ldg_keep(x + (size_t)s_last * kTileK + 8 * lane, pol_keep);
     build_lut<NWC>(xa, 0u, warp, lane);
     if (s_last != s_first) build_lut<NWC>(xb, 128u, warp, lane);
     asm volatile("bar.sync 1, %0;" ::"r"(NWC * 32) : "memory");   // consumer warps only
+    if (tr && tid == 0) tr[2] = gtimer();
     const int r = lane >> 1, h = lane & 1;
     uint32_t cst[4];
 #pragma unroll
@@ -649,6 +653,7 @@ gemv_stream_kernel(const __half* __restrict__ x, const uint8_t* __restrict__ pla
       const int j = t % NST;
       const long long u = u0 + (long long)t * kStageUnits + warp;
       mbar_wait(full + 8 * j, (uint32_t)((t / NST) & 1));
+      if (tr && tid == 0 && t == 0) tr[3] = gtimer();
       if (u < u1) {
         uint4 w[Q];
         int e[Q];
@@ -671,6 +676,7 @@ gemv_stream_kernel(const __half* __restrict__ x, const uint8_t* __restrict__ pla
       }
     }
   }
+  if (tr && tid == 0) tr[4] = gtimer();
   if (S == 1) return;
   // a5 as in gemv_tiled_kernel: one fence per CTA, relaxed arrivals per unit, owners poll
   // their row groups' counters, sum the S partials in slice order, store fp16, re-arm.
@@ -679,14 +685,16 @@ gemv_stream_kernel(const __half* __restrict__ x, const uint8_t* __restrict__ pla
   const int n0 = own0 * kTileRows;
   const int R = (own1 - own0) * kTileRows;
   __syncthreads();
-  if (tid == 0) __threadfence();
+  if (tid == 0) asm volatile("fence.acq_rel.gpu;" ::: "memory");   // release: the CTA's partials before its arrivals
   __syncthreads();
   for (long long uq = u0 + tid; uq < u1; uq += NT)
     asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(cnt + ((unsigned)uq % (unsigned)RG)) : "memory");
+  if (tr && tid == 0) tr[5] = gtimer();
   for (int rg = own0 + tid; rg < own1; rg += NT)
     while (ld_acquire_gpu(cnt + rg) < (unsigned)S) {
     }
   __syncthreads();
+  if (tr && tid == 0) tr[6] = gtimer();
   int T = 1;
   while (T < 32 && 2 * T <= S && (R * 2 * T <= NT || S > 16 * T)) T *= 2;
   const int items = R * T;
@@ -710,6 +718,10 @@ gemv_stream_kernel(const __half* __restrict__ x, const uint8_t* __restrict__ pla
     if (live && part == 0 && n < N) y[n] = __float2half_rn(sum);
   }
   for (int rg = own0 + tid; rg < own1; rg += NT) cnt[rg] = 0u;   // for the next call
+  if (tr) {
+    __syncthreads();
+    if (tid == 0) tr[7] = gtimer();
+  }
 }
 
 template <int Q>
@@ -729,8 +741,17 @@ cudaError_t launch_stream_q(const GemmArgs& a, const LaunchPlan& p) {
   const int pdl = (a.flags & SHIFTADD_FLAG_PDL) ? 1 : 0;
   static const int npre = [] {
     const char* e = std::getenv("SHIFTADD_STREAM_PRE");
-    return e ? std::atoi(e) : 2;
+    return e ? std::atoi(e) : 1;
   }();
+  // dev trace (SHIFTADD_STREAM_TRACE=1): 16 words per CTA after the partials
+  static const int trace_on = [] {
+    const char* e = std::getenv("SHIFTADD_STREAM_TRACE");
+    return e ? std::atoi(e) : 0;
+  }();
+  unsigned long long* trace = nullptr;
+  const size_t part_bytes = (size_t)S * RG * kTileRows * sizeof(float);
+  if (trace_on && a.workspace_bytes >= kCounterBytes + part_bytes + (size_t)p.grid * 128)
+    trace = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(a.workspace) + kCounterBytes + part_bytes);
   static const int loads_only = [] {
     const char* e = std::getenv("SHIFTADD_STREAM_LOADS_ONLY");
     return e ? std::atoi(e) : 0;
@@ -746,7 +767,7 @@ cudaError_t launch_stream_q(const GemmArgs& a, const LaunchPlan& p) {
   c.attrs = attr;
   c.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&c, gemv_stream_kernel<Q>, a.x, a.planes, a.exps, a.N, S, RG, U, a.y, partial, sync,
-                            pdl, npre, loads_only);
+                            pdl, npre, loads_only, trace);
 }
 
 int stream_smem(int q) {
