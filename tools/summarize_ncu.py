@@ -55,7 +55,7 @@ def launches(path, tag):
            "Cold-cache, serialised per-launch times (`--metrics gpu__time_duration.sum --clock-control none`):",
            "compare SHARES, not absolutes.  The list covers the whole process: layer synthesis (torch",
            "RNG/elementwise kernels) and packing (`pack_*`, one-time per layer) precede the timed region;",
-           "a bench step launches only the LUT-GEMV kernel (`gemv_cluster_kernel` for the K = 4096",
+           "a bench step launches only the LUT-GEMV kernel (`gemv_cluster_ring_kernel` for the K = 4096",
            "bench layers; `gemv_tiled_kernel` is the grid split-K kernel), one per layer, so within",
            "the step the LUT-GEMV is 100% of device time.", "",
            "| kernel | launches | total us | share of whole process |", "|---|---|---|---|"]
