@@ -81,8 +81,10 @@ size_t tiled_rows(int N) { return (size_t)((N + kTileRows - 1) / kTileRows); }
 LaunchPlan make_plan(int layout, int M, int N, int K, int q, int g, int sms, unsigned flags) {
   if (layout == SHIFTADD_LAYOUT_CANONICAL) return plan_generic(M, N, K, q, g, sms);
   if (M == 1) {
-    if (!(flags & SHIFTADD_FLAG_SPLITK) && cluster_applicable(N, K, q, sms)) return plan_gemv_cluster(N, K, q, sms);
-    if (stream_applicable(N, K, q, sms)) return plan_gemv_stream(N, K, q, sms);
+    const bool stream = stream_applicable(N, K, q, sms);
+    if (!(flags & SHIFTADD_FLAG_SPLITK) && cluster_applicable(N, K, q, sms) && !(stream && cluster_is_4slot(N, K, q)))
+      return plan_gemv_cluster(N, K, q, sms);
+    if (stream) return plan_gemv_stream(N, K, q, sms);
     return plan_gemv_tiled(N, K, q, sms);
   }
   return plan_gemm_tiled_mb(M, N, K, q, sms);

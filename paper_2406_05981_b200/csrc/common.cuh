@@ -227,6 +227,7 @@ cudaError_t launch_gemm_generic(const GemmArgs& a, const LaunchPlan& p);
 
 LaunchPlan plan_gemv_tiled(int N, int K, int q, int sms);
 bool stream_applicable(int N, int K, int q, int sms);
+bool cluster_is_4slot(int N, int K, int q);
 LaunchPlan plan_gemv_stream(int N, int K, int q, int sms);
 size_t workspace_gemv_tiled(int N, int K);
 cudaError_t launch_gemv_tiled(const GemmArgs& a, const LaunchPlan& p);

@@ -978,6 +978,10 @@ bool cluster_applicable(int N, int K, int q, int sms) {
   return (RG + bands - 1) / bands <= kMaxRGb;
 }
 
+// 4-slot (K > 4096) cluster shapes: the TMA-ring grid split-K kernel is faster where it
+// applies (measured: LLaMA-2-7B down 4096x11008 q=2 8.5 vs 11.3 us).
+bool cluster_is_4slot(int N, int K, int q) { return cluster_shape(N, K, q).variant == kFull4; }
+
 LaunchPlan plan_gemv_cluster(int N, int K, int q, int sms) {
   (void)sms;
   const ClusterShape cs = cluster_shape(N, K, q);

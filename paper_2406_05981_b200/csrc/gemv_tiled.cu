@@ -579,7 +579,7 @@ __global__ void __launch_bounds__((kStreamNWC + 1) * 32, 1)
 gemv_stream_kernel(const __half* __restrict__ x, const uint8_t* __restrict__ planes,
                    const int8_t* __restrict__ exps, int N, int S, int RG, long long U,
                    __half* __restrict__ y, float* __restrict__ partial, unsigned* __restrict__ cnt, int pdl,
-                   int npre, int loads_only, unsigned long long* __restrict__ trace) {
+                   int npre, int loads_only, unsigned long long* __restrict__ trace, int nown) {
   using SM = StreamSmem<Q>;
   unsigned long long* tr = trace ? trace + 16 * blockIdx.x : nullptr;   // dev trace
   if (tr && threadIdx.x == 0) tr[0] = gtimer();
@@ -680,8 +680,12 @@ gemv_stream_kernel(const __half* __restrict__ x, const uint8_t* __restrict__ pla
   if (S == 1) return;
   // a5 as in gemv_tiled_kernel: one fence per CTA, relaxed arrivals per unit, owners poll
   // their row groups' counters, sum the S partials in slice order, store fp16, re-arm.
-  const int own0 = (int)(((long long)blockIdx.x * RG) / G);
-  const int own1 = (int)(((long long)(blockIdx.x + 1) * RG) / G);
+  // Only the first nown CTAs own row groups: the others leave right after their arrivals, and
+  // their SMs take the next kernel's CTAs (PDL), whose weight streams then overlap this
+  // kernel's reduction.
+  const bool owner = (int)blockIdx.x < nown;
+  const int own0 = owner ? (int)(((long long)blockIdx.x * RG) / nown) : 0;
+  const int own1 = owner ? (int)(((long long)(blockIdx.x + 1) * RG) / nown) : 0;
   const int n0 = own0 * kTileRows;
   const int R = (own1 - own0) * kTileRows;
   __syncthreads();
@@ -690,6 +694,7 @@ gemv_stream_kernel(const __half* __restrict__ x, const uint8_t* __restrict__ pla
   for (long long uq = u0 + tid; uq < u1; uq += NT)
     asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(cnt + ((unsigned)uq % (unsigned)RG)) : "memory");
   if (tr && tid == 0) tr[5] = gtimer();
+  if (!owner) return;
   for (int rg = own0 + tid; rg < own1; rg += NT)
     while (ld_acquire_gpu(cnt + rg) < (unsigned)S) {
     }
@@ -752,6 +757,11 @@ cudaError_t launch_stream_q(const GemmArgs& a, const LaunchPlan& p) {
   const size_t part_bytes = (size_t)S * RG * kTileRows * sizeof(float);
   if (trace_on && a.workspace_bytes >= kCounterBytes + part_bytes + (size_t)p.grid * 128)
     trace = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(a.workspace) + kCounterBytes + part_bytes);
+  static const int owners = [] {
+    const char* e = std::getenv("SHIFTADD_STREAM_OWNERS");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int nown = owners > 0 && owners < p.grid ? owners : p.grid;
   static const int loads_only = [] {
     const char* e = std::getenv("SHIFTADD_STREAM_LOADS_ONLY");
     return e ? std::atoi(e) : 0;
@@ -767,7 +777,7 @@ cudaError_t launch_stream_q(const GemmArgs& a, const LaunchPlan& p) {
   c.attrs = attr;
   c.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&c, gemv_stream_kernel<Q>, a.x, a.planes, a.exps, a.N, S, RG, U, a.y, partial, sync,
-                            pdl, npre, loads_only, trace);
+                            pdl, npre, loads_only, trace, nown);
 }
 
 int stream_smem(int q) {

@@ -175,7 +175,8 @@ def test_m1_kernel_choice(sa):
         return sa.gemm_plan(sa.pack(signs, alpha, 128, layout=sa.LAYOUT_TILED), M)[3]
     assert kid(4096, 4096) == 3 and kid(16384, 4096) == 3 and kid(256, 256) == 3 and kid(768, 768) == 3
     assert kid(2048, 8192) == 3 and kid(28672, 8192, q=3) == 4   # 70B gate/up: TMA ring
-    assert kid(4096, 11008, q=1) == 3                     # 5.6 MB: clusters of 11 (non-portable)
+    assert kid(2048, 8192, q=3) == 3                      # 4-slot clusters where the TMA ring split-K
+    assert kid(4096, 11008, q=1) == 4                     # does not apply; it wins where it does
     assert kid(4096, 11008, q=3) == 4 and kid(80000, 4096) == 4
     assert kid(8192, 2048 * 20) == 1                      # S = 160 >= #SMs: register ring
     assert kid(4096, 4096, M=2) == 2

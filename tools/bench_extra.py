@@ -5,6 +5,8 @@
   llama7b_decode   config 2: all 224 LLaMA-2-7B projections with the synthetic 2.2-bit Eq. 4
                    allocation (synth.llama2_7b_allocation), one batch-1 GEMV each, in model
                    order in one CUDA graph (PDL on): us per token and achieved GB/s.
+  llama7b_decode_fused  config 2 with same-q q/k/v and gate/up fused by rows (shared x: one
+                   LUT build and one launch per group), same bytes per token.
   llama7b_batch    config 2, M in {1,2,4,8,16}: one decoder block (7 projections), M rows.
   llama70b_mlp     config 3 on one GPU: gate/up/down 3-bit, us per call.
   opt66b_decode    config 4 on one GPU: 64 x 6 OPT-66B projections at q in {2,3}, us per token.
@@ -84,6 +86,46 @@ def llama7b_decode(dev, M=1):
             "g=128, M=%d" % (avg_bits, M), "us_per_token": round(us, 1), "GBps": round(nbytes / us * 1e-3, 1),
             "frac_of_peak": round(nbytes / us * 1e-3 / PEAK, 4), "bytes_per_token": nbytes,
             "us_per_call_avg": round(us / len(packed), 3)}
+
+
+def llama7b_decode_fused(dev, M=1):
+    """Config 2 with the usual fused projections: in every block the projections that read the
+    same activations (q/k/v; gate/up) and got the same bit width are one packed layer with
+    their rows concatenated (one LUT build and one launch for the group; y is split by views).
+    Same bytes per token as llama7b_decode."""
+    layers = synth.llama2_7b_layers()
+    qs = synth.llama2_7b_allocation()
+    share = {"q_proj": "attn_in", "k_proj": "attn_in", "v_proj": "attn_in", "gate_proj": "mlp_in", "up_proj": "mlp_in"}
+    groups = {}
+    order = []
+    for i, ((blk, name, N, K), q) in enumerate(zip(layers, qs)):
+        key = (blk, share.get(name, name), q, K)
+        if key not in groups:
+            groups[key] = 0
+            order.append(key)
+        groups[key] += N
+    packed = []
+    nbytes = 0
+    for j, key in enumerate(order):
+        blk, _, q, K = key
+        N = groups[key]
+        packed.append(pack_layer(q, N, K, synth.seed_for(2, 1000 + j), dev))
+        nbytes += alg(M, q, N, K)
+    xs = {K: synth.gen_x(M, K, seed=5, device=dev) for K in (4096, 11008)}
+    outs = [torch.empty((M, L.N), dtype=torch.float16, device=dev) for L in packed]
+    ws = sa.Workspace(dev)
+    ws.get(max(sa.workspace_bytes(L, M) for L in packed))
+
+    def run():
+        for L, o in zip(packed, outs):
+            sa.lut_gemm(xs[L.K], L, out=o, workspace=ws, pdl=True)
+
+    us = time_graph(run)
+    return {"name": "llama7b_decode_fused", "config": "LLaMA-2-7B 224 projections as %d launches (same-q q/k/v and "
+            "gate/up fused by rows), synthetic Eq.4 allocation, g=128, M=%d" % (len(packed), M),
+            "us_per_token": round(us, 1), "GBps": round(nbytes / us * 1e-3, 1),
+            "frac_of_peak": round(nbytes / us * 1e-3 / PEAK, 4), "bytes_per_token": nbytes,
+            "launches_per_token": len(packed)}
 
 
 def llama7b_batch(dev):
@@ -211,6 +253,7 @@ def main():
     jobs = {
         "config0": lambda: [config0(dev)],
         "llama7b_decode": lambda: [llama7b_decode(dev)],
+        "llama7b_decode_fused": lambda: [llama7b_decode_fused(dev)],
         "llama7b_batch": lambda: llama7b_batch(dev),
         "llama70b_mlp": lambda: llama70b_mlp(dev),
         "opt66b_decode": lambda: [opt66b_decode(dev, 2), opt66b_decode(dev, 3)],
