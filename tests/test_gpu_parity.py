@@ -342,3 +342,25 @@ def test_tma_ring_kernel_exact_invariants(sa):
         assert torch.equal(y, ys[0])
     assert torch.equal(yn.float(), -ys[0].float())
     assert int(ws.buf[:65536 * 4].count_nonzero()) == 0
+
+
+@pytest.mark.parametrize("q,N,K", [(3, 4096, 4096), (2, 4736, 8192)])
+def test_misaligned_exponents_use_register_ring(sa, q, N, K):
+    """The TMA rings copy exponent tiles with 16-B bulk copies; an exponent array that is not
+    16-B aligned takes the register-ring kernels (own launch shape) and gives the same y."""
+    g = 128
+    signs, alpha = synth.gen_layer(q, N, K, g, seed=synth.seed_for(6, 7, q), device=DEV)
+    layer = sa.pack(signs, alpha, g, layout=sa.LAYOUT_TILED)
+    buf = torch.empty(layer.exps.numel() + 16, dtype=torch.int8, device=DEV)
+    ex = buf[3:3 + layer.exps.numel()]
+    ex.copy_(layer.exps)
+    assert ex.data_ptr() % 16 != 0
+    moved = sa.PackedLayer(layer.planes, ex, q, N, K, g, layer.layout, layer.counts)
+    x = synth.gen_x(1, K, seed=12).to(DEV)
+    y0 = sa.lut_gemm(x, layer)
+    y1 = sa.lut_gemm(x, moved, pdl=True)
+    torch.cuda.synchronize()
+    planes, exps, _ = oracle.pack_canonical(signs.cpu().numpy(), alpha.cpu().numpy(), g)
+    y_ref = oracle.gemm(x.cpu().numpy(), planes, exps, g)
+    for y in (y0, y1):
+        assert oracle.err_floor(y.float().cpu().numpy(), y_ref) <= TOL
