@@ -201,15 +201,17 @@ __device__ __forceinline__ float unit_dot_c(const uint4 (&w)[Q], const int (&e)[
   float acc = 0.f;
 #pragma unroll
   for (int i = 0; i < Q; ++i) {
-    float p0 = 0.f, p1 = 0.f;
+    // 4 chains seeded with the first 4 lookups (no 0 + v adds), summed as a fixed tree
+    float p[4];
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       const uint32_t word = (j < 4) ? w[i].x : (j < 8) ? w[i].y : (j < 12) ? w[i].z : w[i].w;
       const float v = lds_f32(IMM + prmt(word, cst[j >> 1], step_sel_c(j)));
-      if (j & 1) p1 += v; else p0 += v;
+      p[j & 3] = j < 4 ? v : p[j & 3] + v;
     }
-    const float v1 = shift_pow2(p0 + p1, e[i]);
-    acc += AP2 ? v1 + shift_apot2(v1, e2[i]) : v1;   // NEXT-f2: second additive-PoT term
+    const float v1 = shift_pow2((p[0] + p[1]) + (p[2] + p[3]), e[i]);
+    const float vt = AP2 ? v1 + shift_apot2(v1, e2[i]) : v1;   // NEXT-f2: second additive-PoT term
+    acc = i == 0 ? vt : acc + vt;
   }
   return acc;
 }
@@ -519,17 +521,91 @@ gemv_cluster_kernel(const __half* __restrict__ x, const uint4* __restrict__ plan
 // release the stage on its "empty" mbarrier.
 constexpr int kRingNW = 16;                       // consumer warps
 constexpr int kRingBytes = 124 * 1024;            // stages + their 2 x 8 mbarriers
-constexpr int kRingBase = (Smem<2>::total + 127) & ~127;
+// Map below the ring: one 64 KB LUT slab -- 2 slices of fp32 entries, or (H16) 4 slices of
+// fp16 entries, two slices per 32-bit word -- staged x of up to 4 slices, receive buffer
+// recv[slice][row] for up to 4 slices per CTA, the owner's receive mbarrier.
+struct RingMap {
+  static constexpr int lut = kLutBytes;
+  static constexpr int xstage = 4 * kTileK * 2;
+  static constexpr int recv = 4 * (4 * (kMaxRGb + kMaxC) * kTileRows);
+  static constexpr int bar = lut + xstage + recv;
+  static constexpr int total = bar + 16;
+};
+constexpr int kRingBase = (RingMap::total + 127) & ~127;
 static_assert(kRingBase + kRingBytes <= 227 * 1024, "ring must fit");
+
+// a2 for the fp16-pair LUT (H16): word (key, col) of column half `hoff` holds slice ta's entry
+// in its low half and slice tb's in its high half (fp32 sums rounded once to fp16, RNE), so a
+// 64 KB slab holds 4 slices and a build stores half the bytes (store-bandwidth bound:
+// tools/lutbuild.cu, 310 vs 595 cycles per 2 slices).  A lookup of slice t reads the 16-bit
+// half 2*(t&1) of the fp32 layout's address -- an LDS.U16 immediate -- and converts it.
+template <int NW>
+__device__ __forceinline__ void build_lut_pair16(uint32_t slot_base, uint32_t xa, uint32_t xb, bool has_b,
+                                                 int warp, int lane) {
+  float L[2][16], H[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    uint4 xv = make_uint4(0, 0, 0, 0);
+    if (u == 0 || has_b)
+      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(xv.x), "=r"(xv.y), "=r"(xv.z), "=r"(xv.w)
+                   : "r"((u ? xb : xa) + 16 * lane));
+    const float2 f01 = __half22float2(*reinterpret_cast<const __half2*>(&xv.x));
+    const float2 f23 = __half22float2(*reinterpret_cast<const __half2*>(&xv.y));
+    const float2 f45 = __half22float2(*reinterpret_cast<const __half2*>(&xv.z));
+    const float2 f67 = __half22float2(*reinterpret_cast<const __half2*>(&xv.w));
+    const float A[4] = {-f01.x - f01.y, f01.x - f01.y, f01.y - f01.x, f01.x + f01.y};
+    const float B[4] = {-f23.x - f23.y, f23.x - f23.y, f23.y - f23.x, f23.x + f23.y};
+#pragma unroll
+    for (int lo = 0; lo < 16; ++lo) L[u][lo] = A[lo & 3] + B[lo >> 2];
+    const int hi = warp;   // NW == 16: one hi nibble per warp
+    H[u] = ((hi & 1 ? f45.x : -f45.x) + (hi & 2 ? f45.y : -f45.y)) +
+           ((hi & 4 ? f67.x : -f67.x) + (hi & 8 ? f67.y : -f67.y));
+  }
+  static_assert(NW == 16, "one hi nibble per warp");
+  const uint32_t col = slot_base + 4 * lane;
+#pragma unroll
+  for (int lo = 0; lo < 16; ++lo) {
+    const __half2 v = __floats2half2_rn(L[0][lo] + H[0], L[1][lo] + H[1]);
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"(col + ((warp * 16 + lo) << 8)),
+                 "r"(*reinterpret_cast<const uint32_t*>(&v)) : "memory");
+  }
+}
+
+__device__ __forceinline__ float lds_h16(uint32_t addr) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+  return __half2float(__ushort_as_half(v));
+}
+
+// a3 + a4 with fp16 LUT entries: slice half `IMM2` (0 or 2 bytes) of the words addressed as
+// in unit_dot_c.
+template <int Q, uint32_t IMM>
+__device__ __forceinline__ float unit_dot_h16(const uint4 (&w)[Q], const int (&e)[Q], const uint32_t (&cst)[8]) {
+  float acc = 0.f;
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    float p0 = 0.f, p1 = 0.f;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const uint32_t word = (j < 4) ? w[i].x : (j < 8) ? w[i].y : (j < 12) ? w[i].z : w[i].w;
+      const float v = lds_h16(IMM + prmt(word, cst[j >> 1], step_sel_c(j)));
+      if (j & 1) p1 += v; else p0 += v;
+    }
+    acc += shift_pow2(p0 + p1, e[i]);
+  }
+  return acc;
+}
 
 template <int Q>
 struct RingCfg {
-  static constexpr int stage_planes = kRingNW * Q * kTileBytes;
-  static constexpr int stage = kRingNW * Q * (kTileBytes + kTileExps);
+  static constexpr int items = kRingNW;              // items per stage: one per consumer warp
+  static constexpr int stage_planes = items * Q * kTileBytes;
+  static constexpr int stage = items * Q * (kTileBytes + kTileExps);
   static constexpr int nst = (kRingBytes - 128) / stage > 8 ? 8 : (kRingBytes - 128) / stage;
   static constexpr int bars = nst * stage;          // full[j] at +8j, empty[j] at +64+8j
   static constexpr int smem = kRingBase + kRingBytes;
 };
+static_assert(kRingBase + kRingBytes <= 227 * 1024, "ring must fit");
 
 __device__ __forceinline__ void rmbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
@@ -542,13 +618,13 @@ __device__ __forceinline__ void rmbar_wait(uint32_t bar, uint32_t parity) {
   } while (!done);
 }
 
-template <int Q>
+template <int Q, bool H16>
 __global__ void __launch_bounds__((kRingNW + 1) * 32, 1)
 gemv_cluster_ring_kernel(const __half* __restrict__ x, const uint8_t* __restrict__ planes,
                          const int8_t* __restrict__ exps, int N, int S, int RG, int C, __half* __restrict__ y,
                          int flags, unsigned long long* __restrict__ trace, GatherArgs ga) {
   using RC = RingCfg<Q>;
-  constexpr int NW = kRingNW, NST = RC::nst;
+  constexpr int NW = kRingNW, NST = RC::nst, SI = RC::items;
   const bool pdl = flags & kFlagPdl;
   if (threadIdx.x == 0) check_dyn_base();
   unsigned long long* tr = trace ? trace + 32 * blockIdx.x : nullptr;   // dev trace
@@ -561,14 +637,14 @@ gemv_cluster_ring_kernel(const __half* __restrict__ x, const uint8_t* __restrict
   const int rg0 = (int)((cl * (unsigned)RG) / ncl);
   const int RGb = (int)(((cl + 1) * (unsigned)RG) / ncl) - rg0;
   const int s0 = (int)((rank * (unsigned)S) / Cu);
-  const int Sc = (int)(((rank + 1) * (unsigned)S) / Cu) - s0;   // <= 2
+  const int Sc = (int)(((rank + 1) * (unsigned)S) / Cu) - s0;   // <= 2 (H16: <= 4)
   const int Mc = Sc * RGb;                                        // items: i = t * RGb + rgl
   if (pdl) pdl_launch_dependents();
 
   const uint32_t base = dyn_smem_base_cluster();   // kDynBase | rank << 24
-  const uint32_t xs = base + Smem<2>::lut;
-  const uint32_t recv = xs + Smem<2>::xstage;
-  const uint32_t bar = recv + Smem<2>::recv + Smem<2>::part;
+  const uint32_t xs = base + RingMap::lut;
+  const uint32_t recv = xs + RingMap::xstage;
+  const uint32_t bar = base + RingMap::bar;
   const uint32_t ring = base + (uint32_t)kRingBase;
   const uint32_t full = ring + RC::bars, empty = full + 64;
   // a5 set-up as in gemv_cluster_kernel (in-loop push of every (slice, row) partial)
@@ -589,7 +665,7 @@ gemv_cluster_ring_kernel(const __half* __restrict__ x, const uint8_t* __restrict
   }
   __syncthreads();
   cluster_arrive_relaxed();
-  const int nstages = (Mc + NW - 1) / NW;
+  const int nstages = (Mc + SI - 1) / SI;
 
   if (warp == NW) {
     // producer: stage t = items [16t, 16t + 16), one contiguous unit range per slice
@@ -598,11 +674,11 @@ gemv_cluster_ring_kernel(const __half* __restrict__ x, const uint8_t* __restrict
       for (int t = 0; t < nstages; ++t) {
         const int j = t % NST;
         if (t >= NST) rmbar_wait(empty + 8 * j, (uint32_t)((t / NST - 1) & 1));
-        const int i0 = t * NW, i1 = i0 + NW < Mc ? i0 + NW : Mc;
+        const int i0 = t * SI, i1 = i0 + SI < Mc ? i0 + SI : Mc;
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full + 8 * j),
                      "r"((uint32_t)((i1 - i0) * Q * (kTileBytes + kTileExps))) : "memory");
         for (int a = i0; a < i1;) {
-          const int ts = a >= RGb ? 1 : 0;
+          const int ts = a / RGb;
           const int b = (ts + 1) * RGb < i1 ? (ts + 1) * RGb : i1;
           const long long u = (long long)(s0 + ts) * RG + rg0 + (a - ts * RGb);
           const uint32_t dst = ring + (uint32_t)(j * RC::stage);
@@ -625,8 +701,14 @@ gemv_cluster_ring_kernel(const __half* __restrict__ x, const uint8_t* __restrict
     }
     asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");   // consumer warps only
     if (tr && tid == 0) tr[1] = gtimer_ns();
-    for (int t = 0; t < 2; ++t)
-      if (t < Sc) build_lut_slot<NW>(base + (uint32_t)t * 128u, xs + t * (kTileK * 2), warp, lane);
+    if (H16) {   // slices (0,1) in column half 0, (2,3) in half 1
+      for (int t = 0; t < Sc; t += 2)
+        build_lut_pair16<NW>(base + (uint32_t)(t >> 1) * 128u, xs + t * (kTileK * 2), xs + (t + 1) * (kTileK * 2),
+                             t + 1 < Sc, warp, lane);
+    } else {
+      for (int t = 0; t < 2; ++t)
+        if (t < Sc) build_lut_slot<NW>(base + (uint32_t)t * 128u, xs + t * (kTileK * 2), warp, lane);
+    }
     asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
     if (tr && tid == 0) tr[2] = gtimer_ns();
     cluster_wait();   // every peer's receive mbarrier is initialised
@@ -653,8 +735,19 @@ gemv_cluster_ring_kernel(const __half* __restrict__ x, const uint8_t* __restrict
                        "=r"(w[k].w) : "r"(sp + (uint32_t)(k * kTileBytes)));
           asm volatile("ld.shared.s8 %0, [%1];" : "=r"(e[k]) : "r"(se + (uint32_t)(k * kTileExps)));
         }
-        const int ts = i >= RGb ? 1 : 0, rgl = i - ts * RGb;
-        float v = ts ? unit_dot_c<Q, kDynBase, false>(w, e, e, cstO) : unit_dot_c<Q, kDynBase, false>(w, e, e, cstE);
+        const int ts = H16 ? (i >= RGb) + (i >= 2 * RGb) + (i >= 3 * RGb) : (i >= RGb ? 1 : 0);
+        const int rgl = i - ts * RGb;
+        float v;
+        if (H16) {
+          switch (ts) {   // column half ts >> 1 (constant set), word half ts & 1 (LDS immediate)
+            case 0: v = unit_dot_h16<Q, kDynBase>(w, e, cstE); break;
+            case 1: v = unit_dot_h16<Q, kDynBase + 2>(w, e, cstE); break;
+            case 2: v = unit_dot_h16<Q, kDynBase>(w, e, cstO); break;
+            default: v = unit_dot_h16<Q, kDynBase + 2>(w, e, cstO); break;
+          }
+        } else {
+          v = ts ? unit_dot_c<Q, kDynBase, false>(w, e, e, cstO) : unit_dot_c<Q, kDynBase, false>(w, e, e, cstE);
+        }
         __syncwarp();
         if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty + 8 * j) : "memory");
         v += __shfl_xor_sync(0xffffffffu, v, 1);
@@ -716,14 +809,14 @@ int cluster_trace() {
 // stream takes its place and, under PDL, prefetches its weights while this kernel's tail
 // (cluster barrier, reduction) runs.  FULL4: 16 warps, 4 slots (170 KB, one CTA per SM),
 // for K up to 8192 with clusters of <= 8.
-enum Variant { kHalf = 0, kFull2 = 1, kFull4 = 2, kColw = 3, kRing = 4 };
+enum Variant { kHalf = 0, kFull2 = 1, kFull4 = 2, kColw = 3, kRing = 4, kRing16 = 5 };
 struct ClusterShape {
   int variant;
   int sc;   // max slices per CTA
   int C;    // cluster size
 };
 
-ClusterShape cluster_shape(int N, int K, int q) {
+ClusterShape cluster_shape(int N, int K, int q, bool allow16 = true) {
   (void)N; (void)q;
   static const int forced_sc = env_int("SHIFTADD_CLUSTER_SC", 0);
   static const int half = env_int("SHIFTADD_CLUSTER_HALF", 0);
@@ -731,22 +824,26 @@ ClusterShape cluster_shape(int N, int K, int q) {
   const int sc = forced_sc > 0 ? (forced_sc > kMaxSc ? kMaxSc : forced_sc) : ((S + 1) / 2 <= kMaxC ? 2 : kMaxSc);
   // (S + sc - 1) / sc may exceed the portable 8: clusters of up to 16 are non-portable
   static const int ring = env_int("SHIFTADD_RING", 1);
+  static const int lut16 = env_int("SHIFTADD_LUT16", 0);
+  if (allow16 && ring && lut16 && !forced_sc && !half && S <= 16)   // fp16-pair LUT: 4 slices per CTA
+    return ClusterShape{kRing16, 4, (S + 3) / 4};
   const int variant = sc > 2 ? kFull4 : (half ? kHalf : (ring ? kRing : kFull2));
   return ClusterShape{variant, sc, (S + sc - 1) / sc};
 }
 
-int variant_threads(int v) { return v == kHalf ? 8 * 32 : v == kRing ? (kRingNW + 1) * 32 : 16 * 32; }
-int variant_smem(int v) { return v == kFull4 ? Smem<4>::total : v == kRing ? RingCfg<1>::smem : Smem<2>::total; }
+int variant_threads(int v) { return v == kHalf ? 8 * 32 : v >= kRing ? (kRingNW + 1) * 32 : 16 * 32; }
+int variant_smem(int v) { return v == kFull4 ? Smem<4>::total : v >= kRing ? RingCfg<1>::smem : Smem<2>::total; }
 
-template <int Q>
+template <int Q, bool H16 = false>
 cudaError_t set_ring_attrs() {
   static std::once_flag once;
   static cudaError_t err = cudaSuccess;
   std::call_once(once, [] {
-    err = cudaFuncSetAttribute(gemv_cluster_ring_kernel<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    err = cudaFuncSetAttribute(gemv_cluster_ring_kernel<Q, H16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                RingCfg<Q>::smem);
     if (err == cudaSuccess)
-      err = cudaFuncSetAttribute(gemv_cluster_ring_kernel<Q>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      err = cudaFuncSetAttribute(gemv_cluster_ring_kernel<Q, H16>,
+                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   });
   return err;
 }
@@ -765,7 +862,7 @@ int occupancy_ring_clusters(int C) {
   c.attrs = &attr;
   c.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, gemv_cluster_ring_kernel<2>, &c) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&n, gemv_cluster_ring_kernel<2, false>, &c) != cudaSuccess) {
     cudaGetLastError();
     n = 0;
   }
@@ -810,7 +907,7 @@ int occupancy_clusters(int C) {
 
 // Max co-resident clusters of size C for a variant (cached).
 int max_clusters(int variant, int C) {
-  static int cache[5][kMaxCColw + 1] = {};
+  static int cache[6][kMaxCColw + 1] = {};
   static std::mutex mu;
   std::lock_guard<std::mutex> g(mu);
   int& slot = cache[variant][C];
@@ -818,7 +915,7 @@ int max_clusters(int variant, int C) {
   const int n = variant == kHalf    ? occupancy_clusters<2, 8>(C)
                 : variant == kFull2 ? occupancy_clusters<2, 16>(C)
                 : variant == kFull4 ? occupancy_clusters<4, 16>(C)
-                : variant == kRing  ? occupancy_ring_clusters(C)
+                : variant >= kRing  ? occupancy_ring_clusters(C)
                                     : occupancy_clusters<4, 16, true>(C);
   slot = n > 0 ? n : -1;
   return slot;
@@ -876,9 +973,9 @@ cudaError_t launch_cluster_q(const GemmArgs& a, const LaunchPlan& p, int C) {
                             a.exps2, a.gather);
 }
 
-template <int Q>
+template <int Q, bool H16>
 cudaError_t launch_ring_q(const GemmArgs& a, const LaunchPlan& p, int C) {
-  const cudaError_t ae = set_ring_attrs<Q>();
+  const cudaError_t ae = set_ring_attrs<Q, H16>();
   if (ae != cudaSuccess) return ae;
   const int S = a.K / kTileK;
   const int RG = (a.N + kTileRows - 1) / kTileRows;
@@ -900,7 +997,7 @@ cudaError_t launch_ring_q(const GemmArgs& a, const LaunchPlan& p, int C) {
   unsigned long long* trace = nullptr;
   if (cluster_trace() && a.workspace && a.workspace_bytes >= kCounterBytes + (size_t)p.grid * 256)
     trace = reinterpret_cast<unsigned long long*>(static_cast<char*>(a.workspace) + kCounterBytes);
-  return cudaLaunchKernelEx(&c, gemv_cluster_ring_kernel<Q>, a.x, a.planes, a.exps, a.N, S, RG, C, a.y,
+  return cudaLaunchKernelEx(&c, gemv_cluster_ring_kernel<Q, H16>, a.x, a.planes, a.exps, a.N, S, RG, C, a.y,
                             pdl ? kFlagPdl : 0, trace, a.gather);
 }
 
@@ -1020,17 +1117,19 @@ cudaError_t launch_gemv_colwise(const GemmArgs& a) {
 }
 
 cudaError_t launch_gemv_cluster(const GemmArgs& a, const LaunchPlan& p) {
-  const ClusterShape cs = cluster_shape(a.N, a.K, a.q);
-  if (cs.variant == kRing && !a.exps2 && !(reinterpret_cast<uintptr_t>(a.exps) & 15)) {
+  ClusterShape cs = cluster_shape(a.N, a.K, a.q);
+  if ((cs.variant == kRing || cs.variant == kRing16) && !a.exps2 && !(reinterpret_cast<uintptr_t>(a.exps) & 15)) {
+    const bool h16 = cs.variant == kRing16;
     switch (a.q) {   // the TMA ring (its bulk copies need 16-B aligned exponent tiles)
-      case 1: return launch_ring_q<1>(a, p, cs.C);
-      case 2: return launch_ring_q<2>(a, p, cs.C);
-      case 3: return launch_ring_q<3>(a, p, cs.C);
-      case 4: return launch_ring_q<4>(a, p, cs.C);
+      case 1: return h16 ? launch_ring_q<1, true>(a, p, cs.C) : launch_ring_q<1, false>(a, p, cs.C);
+      case 2: return h16 ? launch_ring_q<2, true>(a, p, cs.C) : launch_ring_q<2, false>(a, p, cs.C);
+      case 3: return h16 ? launch_ring_q<3, true>(a, p, cs.C) : launch_ring_q<3, false>(a, p, cs.C);
+      case 4: return h16 ? launch_ring_q<4, true>(a, p, cs.C) : launch_ring_q<4, false>(a, p, cs.C);
       default: return cudaErrorInvalidValue;
     }
   }
   LaunchPlan pp = p;
+  if (cs.variant == kRing16) cs = cluster_shape(a.N, a.K, a.q, false);
   if (cs.variant == kRing) {   // register-ring kernel instead: its own launch shape
     const int RG = (a.N + kTileRows - 1) / kTileRows;
     const int ncl = max_clusters(kFull2, cs.C);

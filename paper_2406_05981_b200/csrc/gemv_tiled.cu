@@ -86,15 +86,17 @@ __device__ __forceinline__ float unit_dot(const uint4 (&w)[Q], const int (&e)[Q]
   float acc = 0.f;
 #pragma unroll
   for (int i = 0; i < Q; ++i) {
-    float p0 = 0.f, p1 = 0.f;
+    // 4 chains seeded with the first 4 lookups (no 0 + v adds), summed as a fixed tree
+    float p[4];
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       const uint32_t word = (j < 4) ? w[i].x : (j < 8) ? w[i].y : (j < 12) ? w[i].z : w[i].w;
       const uint32_t off = prmt(word, cst[j >> 2], step_sel(j));
       const float v = lds_f32(kDynBase + HOFF + off);
-      if (j & 1) p1 += v; else p0 += v;
+      p[j & 3] = j < 4 ? v : p[j & 3] + v;
     }
-    acc += shift_pow2(p0 + p1, e[i]);
+    const float vt = shift_pow2((p[0] + p[1]) + (p[2] + p[3]), e[i]);
+    acc = i == 0 ? vt : acc + vt;
   }
   return acc;
 }
