@@ -426,7 +426,10 @@ def main():
 
     def e2e_step(t):
         cur = copies[t % R]
-        xd_all.copy_(xh_all, non_blocking=True)
+        # the step's inputs host -> device and outputs device -> host by shiftadd_copy (a kernel
+        # reading / writing the pinned buffers over PCIe inside the PDL chain; copy-engine
+        # memcpy nodes cost ~10 us of latency each for these kilobytes)
+        sa.copy(xd_all, xh_all, pdl=pdl, src_ready=True, stream=stream)
         for li in range(len(shard)):
             xv = xd_all[xoff[li]:xoff[li + 1]].view(1, -1)
             yv = yd_all[yoff[li]:yoff[li + 1]].view(1, -1)
@@ -437,7 +440,7 @@ def main():
                 torch.distributed.all_gather_into_tensor(yv.view(-1), ys[li].view(-1), group=group)
             else:
                 sa.lut_gemm(xv, cur[li], out=yv, workspace=wsp, pdl=pdl)
-        yh_all.copy_(yd_all, non_blocking=True)
+        sa.copy(yh_all, yd_all, pdl=pdl, stream=stream)
 
     e2e_rounds = max(2, min(args.steps, 500) // R)
     e2e_steps = e2e_rounds * R

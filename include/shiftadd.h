@@ -213,10 +213,26 @@ shiftadd_status shiftadd_lut_gemv_gather(const uint16_t* x, const uint8_t* plane
                                          void* workspace, size_t workspace_bytes, unsigned flags, void* stream);
 shiftadd_status shiftadd_gather_wait(const uint32_t* flags_local, int P, uint32_t* epoch, void* stream);
 
+/* §8(d) e2e -- stream-ordered copy between device memory and pinned (page-locked, UVA-mapped)
+ * host memory done by a small kernel instead of the copy engine: a decode step's inputs
+ * host->device and its outputs device->host are kilobytes, where a copy-engine memcpy node
+ * costs ~10 us of latency; the kernel reads or writes the host buffer over PCIe directly and
+ * joins the PDL chain of the step's GEMV launches.
+ *   dst, src: device or pinned host pointers (either direction, or device to device),
+ *   16-B aligned; bytes: any multiple of 16 (INVALID otherwise).
+ *   flags: SHIFTADD_FLAG_PDL launches with programmatic dependent launch: the copy writes dst
+ *   only after griddepcontrol.wait (the preceding kernel has finished reading dst);
+ *   SHIFTADD_COPY_SRC_READY additionally lets it read src before that wait (src is not
+ *   written by the preceding kernel, e.g. host inputs), so the PCIe read overlaps it.
+ * No allocation; asynchronous faults surface at the next sync. */
+#define SHIFTADD_COPY_SRC_READY 4u
+shiftadd_status shiftadd_copy(void* dst, const void* src, size_t bytes, unsigned flags, void* stream);
+
 /* Launch geometry the gemm call would use (for measurement/reporting; host only):
  * out[0] = grid CTAs, out[1] = threads per CTA, out[2] = dynamic smem bytes,
  * out[3] = kernel id (0 generic, 1 tiled M=1 split-K, 2 tiled small-batch, 3 tiled M=1
- * cluster split-K), for flags = 0.  Needs a device. */
+ * cluster split-K, 4 tiled M=1 split-K with the TMA weight ring), for flags = 0.  Needs a
+ * device. */
 shiftadd_status shiftadd_gemm_plan(int layout, int M, int N, int K, int q, int g, int out[4]);
 
 #ifdef __cplusplus

@@ -87,6 +87,8 @@ def lib():
                                                vp, vp, c_size, ctypes.c_uint, vp]
         L.shiftadd_gather_wait.restype = c_int
         L.shiftadd_gather_wait.argtypes = [vp, c_int, vp, vp]
+        L.shiftadd_copy.restype = c_int
+        L.shiftadd_copy.argtypes = [vp, vp, c_size, ctypes.c_uint, vp]
         L.shiftadd_gemm_plan.restype = c_int
         L.shiftadd_gemm_plan.argtypes = [c_int] * 6 + [ctypes.POINTER(c_int * 4)]
         v = L.shiftadd_abi_version()
@@ -361,6 +363,27 @@ def lut_gemm(x: torch.Tensor, layer: PackedLayer, out: torch.Tensor | None = Non
 def lut_gemv(x: torch.Tensor, layer: PackedLayer, **kw) -> torch.Tensor:
     """Batch-1 form: x fp16 [K] -> y fp16 [N]."""
     return lut_gemm(x.reshape(-1), layer, **kw)
+
+
+COPY_SRC_READY = 4
+
+
+def copy(dst: torch.Tensor, src: torch.Tensor, pdl: bool = False, src_ready: bool = False, stream=None):
+    """Kernel copy between device memory and pinned host memory (shiftadd_copy): the e2e
+    host<->device transfers of a decode step inside its PDL chain.  src_ready: src is not
+    written by the preceding kernel on the stream (it may be read before the PDL wait)."""
+    nbytes = src.numel() * src.element_size()
+    if dst.numel() * dst.element_size() != nbytes:
+        raise ValueError("copy: size mismatch")
+    for t in (dst, src):
+        if not (t.is_cuda or t.is_pinned()):
+            raise ValueError("copy: tensors must be on the device or in pinned host memory")
+        if not t.is_contiguous():
+            raise ValueError("copy: tensors must be contiguous")
+    dev = dst.device if dst.is_cuda else src.device
+    flags = (FLAG_PDL if pdl else 0) | (COPY_SRC_READY if src_ready else 0)
+    _check(lib().shiftadd_copy(_ptr(dst), _ptr(src), nbytes, flags, _stream_ptr(stream, dev)), "shiftadd_copy")
+    return dst
 
 
 def gemm_plan(layer: PackedLayer, M: int):

@@ -330,6 +330,20 @@ shiftadd_status shiftadd_gather_wait(const uint32_t* flags_local, int P, uint32_
   return SHIFTADD_OK;
 }
 
+shiftadd_status shiftadd_copy(void* dst, const void* src, size_t bytes, unsigned flags, void* stream) {
+  if (!dst || !src) return fail(SHIFTADD_ERR_INVALID, "null pointer argument");
+  if (bytes % 16 || !aligned(dst, 16) || !aligned(src, 16))
+    return fail(SHIFTADD_ERR_INVALID, "copy needs 16-B aligned pointers and a multiple of 16 bytes (%zu)", bytes);
+  if (flags & ~(SHIFTADD_FLAG_PDL | SHIFTADD_COPY_SRC_READY)) return fail(SHIFTADD_ERR_INVALID, "unknown flags 0x%x", flags);
+  DevInfo di;
+  shiftadd_status st;
+  if ((st = device_info(&di)) != SHIFTADD_OK) return st;
+  const cudaError_t e = launch_copy(dst, src, bytes, flags & SHIFTADD_FLAG_PDL, flags & SHIFTADD_COPY_SRC_READY,
+                                    reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "copy launch");
+  return SHIFTADD_OK;
+}
+
 size_t shiftadd_workspace_bytes(int layout, int M, int N, int K, int q, int g) {
   if (check_shape(q, N, K, g, 4) != SHIFTADD_OK || check_layout(layout, K, g) != SHIFTADD_OK) return 0;
   if (M < 1 || M > 16) return 0;

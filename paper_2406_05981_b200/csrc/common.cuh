@@ -227,6 +227,7 @@ cudaError_t launch_gemm_generic(const GemmArgs& a, const LaunchPlan& p);
 
 LaunchPlan plan_gemv_tiled(int N, int K, int q, int sms);
 bool stream_applicable(int N, int K, int q, int sms);
+cudaError_t launch_copy(void* dst, const void* src, size_t bytes, bool pdl, bool src_ready, cudaStream_t stream);
 bool cluster_is_4slot(int N, int K, int q);
 LaunchPlan plan_gemv_stream(int N, int K, int q, int sms);
 size_t workspace_gemv_tiled(int N, int K);

@@ -171,3 +171,13 @@ def test_gather_validation_happens_before_any_launch(L):
     assert L.shiftadd_lut_gemv_gather(*args, p, p, 2, 0, p, p, 1024, 0, None) == 2        # workspace
     assert L.shiftadd_lut_gemv_gather(p, p, p, 0, 4096, 4096, 3, 128, p, p, 2, 0, p, p, 1 << 19, 0, None) == 6
     assert L.shiftadd_gather_wait(None, 2, p, None) == 2
+
+
+def test_copy_validation_happens_before_any_launch(L):
+    _r1, p = _buf(1 << 16)
+    q = ctypes.c_void_p(p.value + 8)
+    assert L.shiftadd_copy(None, p, 256, 0, None) == 2          # null pointer
+    assert L.shiftadd_copy(p, p, 100, 0, None) == 2             # not a multiple of 16
+    assert L.shiftadd_copy(q, p, 256, 0, None) == 2             # misaligned
+    assert L.shiftadd_copy(p, p, 256, 8, None) == 2             # unknown flag
+    assert L.shiftadd_copy(p, p, 256, 1 | 4, None) == 7         # valid: no GPU here
