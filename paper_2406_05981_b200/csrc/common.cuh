@@ -205,7 +205,7 @@ struct LaunchPlan {
   int threads;
   int smem;
   int kernel;  // 0 generic, 1 tiled M=1 split-K, 2 tiled small batch, 3 tiled M=1 cluster split-K,
-              // 4 tiled M=1 split-K with the TMA weight ring
+              // 4 tiled M=1 split-K with the TMA weight ring, 5 tiled M=2 cluster TMA ring
 };
 
 // Implemented in the kernel translation units.
@@ -229,6 +229,9 @@ LaunchPlan plan_gemv_tiled(int N, int K, int q, int sms);
 bool stream_applicable(int N, int K, int q, int sms);
 cudaError_t launch_copy(void* dst, const void* src, size_t bytes, bool pdl, bool src_ready, cudaStream_t stream);
 bool cluster_is_4slot(int N, int K, int q);
+bool m2_applicable(int N, int K, int q, int sms);
+LaunchPlan plan_gemm_m2(int N, int K, int q, int sms);
+cudaError_t launch_gemm_m2(const GemmArgs& a, const LaunchPlan& p);
 LaunchPlan plan_gemv_stream(int N, int K, int q, int sms);
 size_t workspace_gemv_tiled(int N, int K);
 cudaError_t launch_gemv_tiled(const GemmArgs& a, const LaunchPlan& p);

@@ -791,6 +791,268 @@ gemv_cluster_ring_kernel(const __half* __restrict__ x, const uint8_t* __restrict
   }
 }
 
+
+// ------------------------------------------------------------------------------------------
+// §8 a7, M = 2 on the cluster TMA ring (kernel id 5).  The batch-1 ring kernel's
+// decomposition, weight ring and DSMEM reduction, with float2 LUT entries holding the
+// partial sums of both batch rows: one key byte from HBM, one LDS.64, two FADDs.  A slot is
+// 256 keys x 32 groups x 8 B = 64 KB; group g of a slice sits at physical column
+// pcol(g) = 16*(g>>4) + ((g & 15) ^ 8*(g>>4)), so each 16-lane LDS.64 phase (rows r..r+7,
+// halves 0/1) covers all 32 banks (the XOR sends half 1 to the complementary 8 columns).
+// Two slots (slices) per CTA -> 128 KB of LUT and a 60 KB weight ring.
+constexpr int kM2RingBytes = 60 * 1024;
+struct M2Map {
+  static constexpr int lut = 2 * kLutBytes;
+  static constexpr int xstage = 2 * 2 * kTileK * 2;                        // [row][slice][256] fp16
+  static constexpr int recv = 4 * (2 * 2 * (kMaxRGb + kMaxC) * kTileRows);  // [row][slice][chunk row]
+  static constexpr int bar = lut + xstage + recv;
+  static constexpr int base = (bar + 16 + 127) & ~127;                      // the ring
+  static constexpr int total = base + kM2RingBytes;
+};
+static_assert(M2Map::total <= 227 * 1024, "M = 2 ring kernel must fit");
+
+template <int Q>
+struct M2Cfg {
+  static constexpr int stage_planes = kRingNW * Q * kTileBytes;
+  static constexpr int stage = kRingNW * Q * (kTileBytes + kTileExps);
+  static constexpr int nst = (kM2RingBytes - 128) / stage > 8 ? 8 : (kM2RingBytes - 128) / stage;
+  static constexpr int bars = nst * stage;
+};
+
+__host__ __device__ constexpr int pcol2(int g) { return 16 * (g >> 4) + ((g & 15) ^ (8 * (g >> 4))); }
+
+// a2 for M = 2: slot at slot_base from x rows 0/1 of one slice (xa, xb: shared addresses of
+// the 256 activations of each row); warp = hi nibble, lane = group.
+__device__ __forceinline__ void build_lut_slot_m2(uint32_t slot_base, uint32_t xa, uint32_t xb, int warp, int lane) {
+  float L[2][16], H[2];
+#pragma unroll
+  for (int m = 0; m < 2; ++m) {
+    uint4 xv;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(xv.x), "=r"(xv.y), "=r"(xv.z), "=r"(xv.w)
+                 : "r"((m ? xb : xa) + 16 * lane));
+    const float2 f01 = __half22float2(*reinterpret_cast<const __half2*>(&xv.x));
+    const float2 f23 = __half22float2(*reinterpret_cast<const __half2*>(&xv.y));
+    const float2 f45 = __half22float2(*reinterpret_cast<const __half2*>(&xv.z));
+    const float2 f67 = __half22float2(*reinterpret_cast<const __half2*>(&xv.w));
+    const float A[4] = {-f01.x - f01.y, f01.x - f01.y, f01.y - f01.x, f01.x + f01.y};
+    const float B[4] = {-f23.x - f23.y, f23.x - f23.y, f23.y - f23.x, f23.x + f23.y};
+#pragma unroll
+    for (int lo = 0; lo < 16; ++lo) L[m][lo] = A[lo & 3] + B[lo >> 2];
+    const int hi = warp;
+    H[m] = ((hi & 1 ? f45.x : -f45.x) + (hi & 2 ? f45.y : -f45.y)) +
+           ((hi & 4 ? f67.x : -f67.x) + (hi & 8 ? f67.y : -f67.y));
+  }
+  const uint32_t col = slot_base + 8u * (uint32_t)pcol2(lane);
+#pragma unroll
+  for (int lo = 0; lo < 16; ++lo)
+    asm volatile("st.shared.v2.f32 [%0], {%1,%2};" ::"r"(col + ((warp * 16 + lo) << 8)), "f"(L[0][lo] + H[0]),
+                 "f"(L[1][lo] + H[1]) : "memory");
+}
+
+__device__ __forceinline__ float2 lds_f32x2(uint32_t addr) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+  return v;
+}
+
+// a3 + a4 for both rows of one unit; IMM = the slot's LUT base.
+template <int Q, uint32_t IMM>
+__device__ __forceinline__ float2 unit_dot_m2(const uint4 (&w)[Q], const int (&e)[Q], const uint32_t (&cst)[8]) {
+  float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    float2 p[2];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const uint32_t word = (j < 4) ? w[i].x : (j < 8) ? w[i].y : (j < 12) ? w[i].z : w[i].w;
+      const float2 v = lds_f32x2(IMM + prmt(word, cst[j >> 1], step_sel_c(j)));
+      if (j < 2) {
+        p[j & 1] = v;
+      } else {
+        p[j & 1].x += v.x;
+        p[j & 1].y += v.y;
+      }
+    }
+    const float v0 = shift_pow2(p[0].x + p[1].x, e[i]), v1 = shift_pow2(p[0].y + p[1].y, e[i]);
+    acc.x = i == 0 ? v0 : acc.x + v0;
+    acc.y = i == 0 ? v1 : acc.y + v1;
+  }
+  return acc;
+}
+
+template <int Q>
+__global__ void __launch_bounds__((kRingNW + 1) * 32, 1)
+gemm_cluster_ring_m2_kernel(const __half* __restrict__ x, int ldx, const uint8_t* __restrict__ planes,
+                            const int8_t* __restrict__ exps, int N, int S, int RG, int C, __half* __restrict__ y,
+                            int ldy, int flags) {
+  using RC = M2Cfg<Q>;
+  constexpr int NW = kRingNW, NST = RC::nst;
+  const bool pdl = flags & kFlagPdl;
+  if (threadIdx.x == 0) check_dyn_base();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NT = (NW + 1) * 32;
+  const int r = lane >> 1, h = lane & 1;
+  const uint32_t rank = cluster_rank();
+  const unsigned Cu = (unsigned)C, ncl = gridDim.x / Cu, cl = blockIdx.x / Cu;
+  const int rg0 = (int)((cl * (unsigned)RG) / ncl);
+  const int RGb = (int)(((cl + 1) * (unsigned)RG) / ncl) - rg0;
+  const int s0 = (int)((rank * (unsigned)S) / Cu);
+  const int Sc = (int)(((rank + 1) * (unsigned)S) / Cu) - s0;   // <= 2
+  const int Mc = Sc * RGb;
+  if (pdl) pdl_launch_dependents();
+
+  const uint32_t base = dyn_smem_base_cluster();
+  const uint32_t xs = base + M2Map::lut;
+  const uint32_t recv = xs + M2Map::xstage;
+  const uint32_t bar = base + M2Map::bar;
+  const uint32_t ring = base + (uint32_t)M2Map::base;
+  const uint32_t full = ring + RC::bars, empty = full + 64;
+  const int chunk_rg = (RGb + C - 1) / C;
+  const int chunk = chunk_rg * kTileRows;
+  const int rows = RGb * kTileRows;
+  const int own_lo = (int)rank * chunk;
+  const int cnt = rows - own_lo < chunk ? (rows - own_lo > 0 ? rows - own_lo : 0) : chunk;
+  const float inv_chunk_rg = 1.f / (float)chunk_rg;
+  if (tid == 0) {
+    mbar_init_expect(bar, (uint32_t)(2 * (S - Sc) * cnt * 4));
+    for (int j = 0; j < NST; ++j) {
+      rmbar_init(full + 8 * j, 1);
+      rmbar_init(empty + 8 * j, NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  cluster_arrive_relaxed();
+  const int nstages = (Mc + NW - 1) / NW;
+
+  if (warp == NW) {
+    if (lane == 0) {   // producer, as in gemv_cluster_ring_kernel
+      const uint64_t pol = policy_evict_first();
+      for (int t = 0; t < nstages; ++t) {
+        const int j = t % NST;
+        if (t >= NST) rmbar_wait(empty + 8 * j, (uint32_t)((t / NST - 1) & 1));
+        const int i0 = t * NW, i1 = i0 + NW < Mc ? i0 + NW : Mc;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full + 8 * j),
+                     "r"((uint32_t)((i1 - i0) * Q * (kTileBytes + kTileExps))) : "memory");
+        for (int a = i0; a < i1;) {
+          const int ts = a / RGb;
+          const int b = (ts + 1) * RGb < i1 ? (ts + 1) * RGb : i1;
+          const long long u = (long long)(s0 + ts) * RG + rg0 + (a - ts * RGb);
+          const uint32_t dst = ring + (uint32_t)(j * RC::stage);
+          bulk_load_x(dst + (uint32_t)((a - i0) * Q * kTileBytes), planes + u * Q * kTileBytes,
+                      (uint32_t)((b - a) * Q * kTileBytes), full + 8 * j, pol, false);
+          bulk_load_x(dst + (uint32_t)(RC::stage_planes + (a - i0) * Q * kTileExps), exps + u * Q * kTileExps,
+                      (uint32_t)((b - a) * Q * kTileExps), full + 8 * j, pol, false);
+          a = b;
+        }
+      }
+    }
+  } else {
+    if (pdl) pdl_wait();
+    if (tid < 2 * Sc * (kTileK / 8)) {   // x rows 0/1 of the CTA's slices -> xs[row][slice][256]
+      const int m = tid / (Sc * 32), c = tid - m * (Sc * 32);
+      const uint4 xv = ldg_keep(reinterpret_cast<const uint4*>(x + (size_t)m * ldx + (size_t)s0 * kTileK) + c,
+                                policy_evict_last());
+      asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(xs + (uint32_t)(m * 2 * kTileK * 2 + 16 * c)),
+                   "r"(xv.x), "r"(xv.y), "r"(xv.z), "r"(xv.w) : "memory");
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+    for (int t = 0; t < Sc; ++t)
+      build_lut_slot_m2(base + (uint32_t)t * kLutBytes, xs + (uint32_t)(t * kTileK * 2),
+                        xs + (uint32_t)(2 * kTileK * 2 + t * kTileK * 2), warp, lane);
+    asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+    cluster_wait();
+    uint32_t cst[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint32_t c0 = 8u * (uint32_t)pcol2(16 * h + ((2 * c + r) & 15));
+      const uint32_t c1 = 8u * (uint32_t)pcol2(16 * h + ((2 * c + 1 + r) & 15));
+      cst[c] = c0 | (c1 << 8) | (rank << 16);
+    }
+    for (int t = 0; t < nstages; ++t) {
+      const int j = t % NST;
+      const int i = t * NW + warp;
+      rmbar_wait(full + 8 * j, (uint32_t)((t / NST) & 1));
+      if (i < Mc) {
+        uint4 w[Q];
+        int e[Q];
+        const uint32_t sp = ring + (uint32_t)(j * RC::stage + warp * Q * kTileBytes + 16 * lane);
+        const uint32_t se = ring + (uint32_t)(j * RC::stage + RC::stage_planes + warp * Q * kTileExps + lane);
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+          asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(w[k].x), "=r"(w[k].y), "=r"(w[k].z),
+                       "=r"(w[k].w) : "r"(sp + (uint32_t)(k * kTileBytes)));
+          asm volatile("ld.shared.s8 %0, [%1];" : "=r"(e[k]) : "r"(se + (uint32_t)(k * kTileExps)));
+        }
+        const int ts = i >= RGb ? 1 : 0, rgl = i - ts * RGb;
+        float2 v = ts ? unit_dot_m2<Q, kDynBase + kLutBytes>(w, e, cst) : unit_dot_m2<Q, kDynBase>(w, e, cst);
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty + 8 * j) : "memory");
+        v.x += __shfl_xor_sync(0xffffffffu, v.x, 1);
+        v.y += __shfl_xor_sync(0xffffffffu, v.y, 1);
+        if (h == 0) {   // a5 push of both rows' partials: recv[m][slice][row - o*chunk] of owner o
+          const int o = (int)(((float)rgl + 0.5f) * inv_chunk_rg);
+          const uint32_t d0 = recv + 4u * (uint32_t)((s0 + ts) * chunk + (rgl - o * chunk_rg) * kTileRows + r);
+          const uint32_t d1 = d0 + 4u * (uint32_t)(S * chunk);
+          if (o == (int)rank) {
+            sts_f32(d0, v.x);
+            sts_f32(d1, v.y);
+          } else {
+            st_async_f32(d0, bar, (uint32_t)o, v.x);
+            st_async_f32(d1, bar, (uint32_t)o, v.y);
+          }
+        }
+      } else {
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty + 8 * j) : "memory");
+      }
+    }
+  }
+  __syncthreads();
+  mbar_wait_parity0(bar);
+  for (int it = tid; it < 2 * cnt; it += NT) {   // the owner: rows 0/1 of its chunk, slices in order
+    const int m = it >= cnt ? 1 : 0, jj = it - m * cnt;
+    const uint32_t rb = recv + 4u * (uint32_t)(m * S * chunk + jj);
+    float v = lds_f32(rb);
+    for (int s = 1; s < S; ++s) v += lds_f32(rb + 4u * (uint32_t)(s * chunk));
+    const int n = rg0 * kTileRows + own_lo + jj;
+    if (n < N) y[(size_t)m * ldy + n] = __float2half_rn(v);
+  }
+}
+
+template <int Q>
+cudaError_t launch_m2_q(const GemmArgs& a, const LaunchPlan& p, int C) {
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [] {
+    err = cudaFuncSetAttribute(gemm_cluster_ring_m2_kernel<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               M2Map::total);
+    if (err == cudaSuccess)
+      err = cudaFuncSetAttribute(gemm_cluster_ring_m2_kernel<Q>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  });
+  if (err != cudaSuccess) return err;
+  const int S = a.K / kTileK;
+  const int RG = (a.N + kTileRows - 1) / kTileRows;
+  const int pdl = (a.flags & SHIFTADD_FLAG_PDL) ? 1 : 0;
+  cudaLaunchConfig_t c = {};
+  c.gridDim = dim3(p.grid);
+  c.blockDim = dim3((kRingNW + 1) * 32);
+  c.dynamicSmemBytes = M2Map::total;
+  c.stream = a.stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  c.attrs = attr;
+  c.numAttrs = pdl ? 2 : 1;
+  return cudaLaunchKernelEx(&c, gemm_cluster_ring_m2_kernel<Q>, a.x, a.ldx, a.planes, a.exps, a.N, S, RG, C, a.y,
+                            a.ldy, pdl ? kFlagPdl : 0);
+}
+
 int env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
   return e ? std::atoi(e) : dflt;
@@ -1112,6 +1374,39 @@ cudaError_t launch_gemv_colwise(const GemmArgs& a) {
     case 2: return launch_cluster_q<2, 4, 16, 128, true>(a, p, S);
     case 3: return launch_cluster_q<3, 4, 16, 128, true>(a, p, S);
     case 4: return launch_cluster_q<4, 4, 16, 128, true>(a, p, S);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// §8 a7, M = 2 (kernel id 5): tiled layout, K <= 4096, q <= 3 (a 60 KB ring holds >= 2 stages).
+bool m2_applicable(int N, int K, int q, int sms) {
+  (void)sms;
+  static const int on = env_int("SHIFTADD_M2_RING", 1);
+  const int S = K / kTileK;
+  if (!on || S < 1 || S > 2 * kMaxC || q < 1 || q > 3) return false;
+  const int C = (S + 1) / 2;
+  const int ncl = max_clusters(kRing, C);
+  if (ncl <= 0) return false;
+  const int RG = (N + kTileRows - 1) / kTileRows;
+  const int bands = ncl < RG ? ncl : RG;
+  return (RG + bands - 1) / bands <= kMaxRGb;
+}
+
+LaunchPlan plan_gemm_m2(int N, int K, int q, int sms) {
+  (void)q; (void)sms;
+  const int S = K / kTileK, C = (S + 1) / 2;
+  const int RG = (N + kTileRows - 1) / kTileRows;
+  const int ncl = max_clusters(kRing, C);
+  const int bands = ncl < RG ? ncl : RG;
+  return LaunchPlan{bands * C, (kRingNW + 1) * 32, M2Map::total, 5};
+}
+
+cudaError_t launch_gemm_m2(const GemmArgs& a, const LaunchPlan& p) {
+  const int C = (a.K / kTileK + 1) / 2;
+  switch (a.q) {
+    case 1: return launch_m2_q<1>(a, p, C);
+    case 2: return launch_m2_q<2>(a, p, C);
+    case 3: return launch_m2_q<3>(a, p, C);
     default: return cudaErrorInvalidValue;
   }
 }

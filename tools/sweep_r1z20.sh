@@ -1,0 +1,7 @@
+#!/bin/bash
+cd "$(dirname "$0")/.."
+timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -4
+B="4096:4096:2 11008:4096:3 4096:4096:3 22016:4096:3 768:768:3"
+echo "== M=2 cluster ring"; timeout 300 python tools/time_gemv.py --pdl --m 2 $B 2>&1 | grep -v Warn
+echo "== M=2 small-batch split-K"; SHIFTADD_M2_RING=0 timeout 300 python tools/time_gemv.py --pdl --m 2 $B 2>&1 | grep -v Warn
+timeout 300 python tools/bench_extra.py --only llama7b_batch 2>&1 | grep -v Warn | head -3
