@@ -88,6 +88,8 @@ LaunchPlan make_plan(int layout, int M, int N, int K, int q, int g, int sms, uns
     return plan_gemv_tiled(N, K, q, sms);
   }
   if (M == 2 && !(flags & SHIFTADD_FLAG_SPLITK) && m2_applicable(N, K, q, sms)) return plan_gemm_m2(N, K, q, sms);
+  if ((M == 3 || M == 4) && !(flags & SHIFTADD_FLAG_SPLITK) && m4_applicable(N, K, q, sms))
+    return plan_gemm_m4(N, K, q, sms);
   return plan_gemm_tiled_mb(M, N, K, q, sms);
 }
 
@@ -405,11 +407,12 @@ shiftadd_status shiftadd_lut_gemm(const uint16_t* x, int ldx, const uint8_t* pla
   LaunchPlan p = make_plan(layout, M, N, K, q, g, di.sms, flags);
   // the TMA ring copies exponent tiles with 16-B bulk copies
   if (p.kernel == 4 && !aligned(exps, 16)) p = plan_gemv_tiled(N, K, q, di.sms);
-  if (p.kernel == 5 && !aligned(exps, 16)) p = plan_gemm_tiled_mb(M, N, K, q, di.sms);
+  if ((p.kernel == 5 || p.kernel == 6) && !aligned(exps, 16)) p = plan_gemm_tiled_mb(M, N, K, q, di.sms);
   cudaError_t e;
   if (layout == SHIFTADD_LAYOUT_CANONICAL) e = launch_gemm_generic(a, p);
   else if (p.kernel == 3) e = launch_gemv_cluster(a, p);
   else if (p.kernel == 5) e = launch_gemm_m2(a, p);
+  else if (p.kernel == 6) e = launch_gemm_m4(a, p);
   else if (M == 1) e = launch_gemv_tiled(a, p);
   else e = launch_gemm_tiled_mb(a, p);
   if (e == cudaErrorNotSupported) return fail(SHIFTADD_ERR_UNSUPPORTED, "no kernel for this configuration");

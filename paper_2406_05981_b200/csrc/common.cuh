@@ -205,7 +205,8 @@ struct LaunchPlan {
   int threads;
   int smem;
   int kernel;  // 0 generic, 1 tiled M=1 split-K, 2 tiled small batch, 3 tiled M=1 cluster split-K,
-              // 4 tiled M=1 split-K with the TMA weight ring, 5 tiled M=2 cluster TMA ring
+              // 4 tiled M=1 split-K with the TMA weight ring, 5 tiled M=2 cluster TMA ring,
+              // 6 tiled M=3..4 cluster TMA ring
 };
 
 // Implemented in the kernel translation units.
@@ -232,6 +233,9 @@ bool cluster_is_4slot(int N, int K, int q);
 bool m2_applicable(int N, int K, int q, int sms);
 LaunchPlan plan_gemm_m2(int N, int K, int q, int sms);
 cudaError_t launch_gemm_m2(const GemmArgs& a, const LaunchPlan& p);
+bool m4_applicable(int N, int K, int q, int sms);
+LaunchPlan plan_gemm_m4(int N, int K, int q, int sms);
+cudaError_t launch_gemm_m4(const GemmArgs& a, const LaunchPlan& p);
 LaunchPlan plan_gemv_stream(int N, int K, int q, int sms);
 size_t workspace_gemv_tiled(int N, int K);
 cudaError_t launch_gemv_tiled(const GemmArgs& a, const LaunchPlan& p);

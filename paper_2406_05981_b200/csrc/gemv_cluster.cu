@@ -1053,6 +1053,248 @@ cudaError_t launch_m2_q(const GemmArgs& a, const LaunchPlan& p, int C) {
                             a.ldy, pdl ? kFlagPdl : 0);
 }
 
+
+// ------------------------------------------------------------------------------------------
+// §8 a7, M = 3..4 on the cluster TMA ring (kernel id 6).  float4 LUT entries (4 rows per
+// lookup: one LDS.128, four FADDs).  A slot is 256 keys x 32 groups x 16 B = 128 KB in two
+// 64 KB regions (group half h = g >> 4); group g sits at region h, key*256 + ((g & 15) ^ 4h)*16,
+// so each 8-lane LDS.128 phase covers 8 distinct 16-B bank groups.  One slot (slice) per CTA:
+// clusters of S (K <= 4096).  The PRMT forms the whole address from the key byte and a
+// per-step constant (column byte, region byte, rank byte).
+struct M4Map {
+  static constexpr int lut = 2 * kLutBytes;
+  static constexpr int xstage = 4 * kTileK * 2;                            // [row][256] fp16
+  static constexpr int recv = 4 * (4 * (kMaxRGb + 2 * kMaxC) * kTileRows);  // [row][slice][chunk row]
+  static constexpr int bar = lut + xstage + recv;
+  static constexpr int base = (bar + 16 + 127) & ~127;
+  static constexpr int total = base + kM2RingBytes;
+};
+static_assert(M4Map::total <= 227 * 1024, "M = 4 ring kernel must fit");
+
+// step j: byte0 <- cst byte 0 (column), byte1 <- key byte j&3, byte2 <- cst byte 2 (region),
+// byte3 <- cst byte 3 (rank)
+__host__ __device__ constexpr uint32_t step_sel_m4(int j) { return (7u << 12) | (6u << 8) | ((uint32_t)(j & 3) << 4) | 4u; }
+
+__device__ __forceinline__ void build_lut_slot_m4(uint32_t slot_base, uint32_t xs, int warp, int lane) {
+  float L[4][16], H[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    uint4 xv;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(xv.x), "=r"(xv.y), "=r"(xv.z), "=r"(xv.w)
+                 : "r"(xs + (uint32_t)(m * kTileK * 2) + 16 * lane));
+    const float2 f01 = __half22float2(*reinterpret_cast<const __half2*>(&xv.x));
+    const float2 f23 = __half22float2(*reinterpret_cast<const __half2*>(&xv.y));
+    const float2 f45 = __half22float2(*reinterpret_cast<const __half2*>(&xv.z));
+    const float2 f67 = __half22float2(*reinterpret_cast<const __half2*>(&xv.w));
+    const float A[4] = {-f01.x - f01.y, f01.x - f01.y, f01.y - f01.x, f01.x + f01.y};
+    const float B[4] = {-f23.x - f23.y, f23.x - f23.y, f23.y - f23.x, f23.x + f23.y};
+#pragma unroll
+    for (int lo = 0; lo < 16; ++lo) L[m][lo] = A[lo & 3] + B[lo >> 2];
+    const int hi = warp;
+    H[m] = ((hi & 1 ? f45.x : -f45.x) + (hi & 2 ? f45.y : -f45.y)) +
+           ((hi & 4 ? f67.x : -f67.x) + (hi & 8 ? f67.y : -f67.y));
+  }
+  const int hh = lane >> 4;
+  const uint32_t col = slot_base + (uint32_t)hh * 65536u + 16u * (uint32_t)((lane & 15) ^ (4 * hh));
+#pragma unroll
+  for (int lo = 0; lo < 16; ++lo)
+    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(col + ((warp * 16 + lo) << 8)), "f"(L[0][lo] + H[0]),
+                 "f"(L[1][lo] + H[1]), "f"(L[2][lo] + H[2]), "f"(L[3][lo] + H[3]) : "memory");
+}
+
+template <int Q>
+__device__ __forceinline__ float4 unit_dot_m4(const uint4 (&w)[Q], const int (&e)[Q], const uint32_t (&cst)[16]) {
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const uint32_t word = (j < 4) ? w[i].x : (j < 8) ? w[i].y : (j < 12) ? w[i].z : w[i].w;
+      const float4 v = lds_f32x4(kDynBase + prmt(word, cst[j], step_sel_m4(j)));
+      if (j == 0) {
+        p = v;
+      } else {
+        p.x += v.x; p.y += v.y; p.z += v.z; p.w += v.w;
+      }
+    }
+    const float v0 = shift_pow2(p.x, e[i]), v1 = shift_pow2(p.y, e[i]);
+    const float v2 = shift_pow2(p.z, e[i]), v3 = shift_pow2(p.w, e[i]);
+    if (i == 0) {
+      acc = make_float4(v0, v1, v2, v3);
+    } else {
+      acc.x += v0; acc.y += v1; acc.z += v2; acc.w += v3;
+    }
+  }
+  return acc;
+}
+
+template <int Q>
+__global__ void __launch_bounds__((kRingNW + 1) * 32, 1)
+gemm_cluster_ring_m4_kernel(const __half* __restrict__ x, int ldx, int M, const uint8_t* __restrict__ planes,
+                            const int8_t* __restrict__ exps, int N, int S, int RG, int C, __half* __restrict__ y,
+                            int ldy, int flags) {
+  using RC = M2Cfg<Q>;
+  constexpr int NW = kRingNW, NST = RC::nst;
+  const bool pdl = flags & kFlagPdl;
+  if (threadIdx.x == 0) check_dyn_base();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NT = (NW + 1) * 32;
+  const int r = lane >> 1, h = lane & 1;
+  const uint32_t rank = cluster_rank();
+  const unsigned Cu = (unsigned)C, ncl = gridDim.x / Cu, cl = blockIdx.x / Cu;
+  const int rg0 = (int)((cl * (unsigned)RG) / ncl);
+  const int RGb = (int)(((cl + 1) * (unsigned)RG) / ncl) - rg0;
+  const int s0 = (int)((rank * (unsigned)S) / Cu);
+  const int Sc = (int)(((rank + 1) * (unsigned)S) / Cu) - s0;   // 1 (C = S)
+  const int Mc = Sc * RGb;
+  if (pdl) pdl_launch_dependents();
+
+  const uint32_t base = dyn_smem_base_cluster();
+  const uint32_t xs = base + M4Map::lut;
+  const uint32_t recv = xs + M4Map::xstage;
+  const uint32_t bar = base + M4Map::bar;
+  const uint32_t ring = base + (uint32_t)M4Map::base;
+  const uint32_t full = ring + RC::bars, empty = full + 64;
+  const int chunk_rg = (RGb + C - 1) / C;
+  const int chunk = chunk_rg * kTileRows;
+  const int rows = RGb * kTileRows;
+  const int own_lo = (int)rank * chunk;
+  const int cnt = rows - own_lo < chunk ? (rows - own_lo > 0 ? rows - own_lo : 0) : chunk;
+  const float inv_chunk_rg = 1.f / (float)chunk_rg;
+  if (tid == 0) {
+    mbar_init_expect(bar, (uint32_t)(4 * (S - Sc) * cnt * 4));
+    for (int j = 0; j < NST; ++j) {
+      rmbar_init(full + 8 * j, 1);
+      rmbar_init(empty + 8 * j, NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  cluster_arrive_relaxed();
+  const int nstages = (Mc + NW - 1) / NW;
+
+  if (warp == NW) {
+    if (lane == 0) {   // producer: one slice, contiguous units
+      const uint64_t pol = policy_evict_first();
+      for (int t = 0; t < nstages; ++t) {
+        const int j = t % NST;
+        if (t >= NST) rmbar_wait(empty + 8 * j, (uint32_t)((t / NST - 1) & 1));
+        const int i0 = t * NW, i1 = i0 + NW < Mc ? i0 + NW : Mc;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full + 8 * j),
+                     "r"((uint32_t)((i1 - i0) * Q * (kTileBytes + kTileExps))) : "memory");
+        const long long u = (long long)s0 * RG + rg0 + i0;
+        const uint32_t dst = ring + (uint32_t)(j * RC::stage);
+        bulk_load_x(dst, planes + u * Q * kTileBytes, (uint32_t)((i1 - i0) * Q * kTileBytes), full + 8 * j, pol,
+                    false);
+        bulk_load_x(dst + (uint32_t)RC::stage_planes, exps + u * Q * kTileExps, (uint32_t)((i1 - i0) * Q * kTileExps),
+                    full + 8 * j, pol, false);
+      }
+    }
+  } else {
+    if (pdl) pdl_wait();
+    if (tid < 4 * (kTileK / 8)) {   // x rows 0..3 of the slice (rows >= M are zero)
+      const int m = tid >> 5, c = tid & 31;
+      uint4 xv = make_uint4(0, 0, 0, 0);
+      if (m < M)
+        xv = ldg_keep(reinterpret_cast<const uint4*>(x + (size_t)m * ldx + (size_t)s0 * kTileK) + c,
+                      policy_evict_last());
+      asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(xs + (uint32_t)(m * kTileK * 2 + 16 * c)),
+                   "r"(xv.x), "r"(xv.y), "r"(xv.z), "r"(xv.w) : "memory");
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+    build_lut_slot_m4(base, xs, warp, lane);
+    asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+    cluster_wait();
+    uint32_t cst[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      cst[j] = (16u * (uint32_t)(((j + r) & 15) ^ (4 * h))) | ((uint32_t)h << 16) | (rank << 24);
+    for (int t = 0; t < nstages; ++t) {
+      const int j = t % NST;
+      const int i = t * NW + warp;
+      rmbar_wait(full + 8 * j, (uint32_t)((t / NST) & 1));
+      if (i < Mc) {
+        uint4 w[Q];
+        int e[Q];
+        const uint32_t sp = ring + (uint32_t)(j * RC::stage + warp * Q * kTileBytes + 16 * lane);
+        const uint32_t se = ring + (uint32_t)(j * RC::stage + RC::stage_planes + warp * Q * kTileExps + lane);
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+          asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(w[k].x), "=r"(w[k].y), "=r"(w[k].z),
+                       "=r"(w[k].w) : "r"(sp + (uint32_t)(k * kTileBytes)));
+          asm volatile("ld.shared.s8 %0, [%1];" : "=r"(e[k]) : "r"(se + (uint32_t)(k * kTileExps)));
+        }
+        float4 v = unit_dot_m4<Q>(w, e, cst);
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty + 8 * j) : "memory");
+        v.x += __shfl_xor_sync(0xffffffffu, v.x, 1);
+        v.y += __shfl_xor_sync(0xffffffffu, v.y, 1);
+        v.z += __shfl_xor_sync(0xffffffffu, v.z, 1);
+        v.w += __shfl_xor_sync(0xffffffffu, v.w, 1);
+        if (h == 0) {   // a5 push of the 4 rows' partials: recv[m][slice][row - o*chunk] of owner o
+          const int rgl = i;
+          const int o = (int)(((float)rgl + 0.5f) * inv_chunk_rg);
+          const uint32_t d0 = recv + 4u * (uint32_t)(s0 * chunk + (rgl - o * chunk_rg) * kTileRows + r);
+          const uint32_t ds = 4u * (uint32_t)(S * chunk);
+          const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            if (o == (int)rank) sts_f32(d0 + m * ds, vv[m]);
+            else st_async_f32(d0 + m * ds, bar, (uint32_t)o, vv[m]);
+          }
+        }
+      } else {
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty + 8 * j) : "memory");
+      }
+    }
+  }
+  __syncthreads();
+  mbar_wait_parity0(bar);
+  for (int it = tid; it < M * cnt; it += NT) {   // the owner: rows 0..M-1 of its chunk, slices in order
+    const int m = it / cnt, jj = it - m * cnt;
+    const uint32_t rb = recv + 4u * (uint32_t)(m * S * chunk + jj);
+    float v = lds_f32(rb);
+    for (int s = 1; s < S; ++s) v += lds_f32(rb + 4u * (uint32_t)(s * chunk));
+    const int n = rg0 * kTileRows + own_lo + jj;
+    if (n < N) y[(size_t)m * ldy + n] = __float2half_rn(v);
+  }
+}
+
+template <int Q>
+cudaError_t launch_m4_q(const GemmArgs& a, const LaunchPlan& p, int C) {
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [] {
+    err = cudaFuncSetAttribute(gemm_cluster_ring_m4_kernel<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               M4Map::total);
+    if (err == cudaSuccess)
+      err = cudaFuncSetAttribute(gemm_cluster_ring_m4_kernel<Q>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  });
+  if (err != cudaSuccess) return err;
+  const int S = a.K / kTileK;
+  const int RG = (a.N + kTileRows - 1) / kTileRows;
+  const int pdl = (a.flags & SHIFTADD_FLAG_PDL) ? 1 : 0;
+  cudaLaunchConfig_t c = {};
+  c.gridDim = dim3(p.grid);
+  c.blockDim = dim3((kRingNW + 1) * 32);
+  c.dynamicSmemBytes = M4Map::total;
+  c.stream = a.stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  c.attrs = attr;
+  c.numAttrs = pdl ? 2 : 1;
+  return cudaLaunchKernelEx(&c, gemm_cluster_ring_m4_kernel<Q>, a.x, a.ldx, a.M, a.planes, a.exps, a.N, S, RG, C,
+                            a.y, a.ldy, pdl ? kFlagPdl : 0);
+}
+
 int env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
   return e ? std::atoi(e) : dflt;
@@ -1407,6 +1649,38 @@ cudaError_t launch_gemm_m2(const GemmArgs& a, const LaunchPlan& p) {
     case 1: return launch_m2_q<1>(a, p, C);
     case 2: return launch_m2_q<2>(a, p, C);
     case 3: return launch_m2_q<3>(a, p, C);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// §8 a7, M = 3..4 (kernel id 6): tiled layout, K <= 4096 (one slice per CTA), q <= 3.
+bool m4_applicable(int N, int K, int q, int sms) {
+  (void)sms;
+  static const int on = env_int("SHIFTADD_M4_RING", 1);
+  const int S = K / kTileK;
+  if (!on || S < 1 || S > kMaxCColw || q < 1 || q > 3) return false;
+  const int ncl = max_clusters(kRing, S);
+  if (ncl <= 0) return false;
+  const int RG = (N + kTileRows - 1) / kTileRows;
+  const int bands = ncl < RG ? ncl : RG;
+  return (RG + bands - 1) / bands <= kMaxRGb;
+}
+
+LaunchPlan plan_gemm_m4(int N, int K, int q, int sms) {
+  (void)q; (void)sms;
+  const int S = K / kTileK;
+  const int RG = (N + kTileRows - 1) / kTileRows;
+  const int ncl = max_clusters(kRing, S);
+  const int bands = ncl < RG ? ncl : RG;
+  return LaunchPlan{bands * S, (kRingNW + 1) * 32, M4Map::total, 6};
+}
+
+cudaError_t launch_gemm_m4(const GemmArgs& a, const LaunchPlan& p) {
+  const int C = a.K / kTileK;
+  switch (a.q) {
+    case 1: return launch_m4_q<1>(a, p, C);
+    case 2: return launch_m4_q<2>(a, p, C);
+    case 3: return launch_m4_q<3>(a, p, C);
     default: return cudaErrorInvalidValue;
   }
 }

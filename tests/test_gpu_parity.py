@@ -156,6 +156,25 @@ def test_m2_cluster_ring_parity(sa, q, N, K, splitk):
     assert bool((ybuf[:, N:] == 7.0).all())
 
 
+@pytest.mark.parametrize("M,q,N,K", [(4, 2, 4096, 4096), (3, 3, 11008, 4096), (4, 1, 1000, 3072),
+                                     (3, 3, 40, 512), (4, 3, 768, 768)])
+@pytest.mark.parametrize("splitk", [False, True])
+def test_m4_cluster_ring_parity(sa, M, q, N, K, splitk):
+    """a7 at M = 3..4 on the cluster TMA ring (kernel 6, float4 entries; splitk forces the
+    small-batch split-K kernel), output written into a wider buffer (ldy > N)."""
+    g = 128
+    signs, alpha, planes, exps = _layer(q, N, K, g, synth.seed_for(2, 40 + q, N % 13))
+    layer = _gpu(sa, signs, alpha, g, sa.LAYOUT_TILED)
+    assert sa.gemm_plan(layer, M)[3] == 6
+    x = synth.gen_x(M, K, seed=synth.seed_for(2, 6, M))
+    ybuf = torch.full((M, N + 40), 7.0, dtype=torch.float16, device=DEV)
+    y = sa.lut_gemm(x.to(DEV), layer, out=ybuf[:, :N], pdl=True, splitk=splitk)
+    torch.cuda.synchronize()
+    err = oracle.err_floor(y.float().cpu().numpy(), oracle.gemm(x.numpy(), planes, exps, g))
+    assert err <= TOL, err
+    assert bool((ybuf[:, N:] == 7.0).all())
+
+
 @pytest.mark.parametrize("g", [8, 32, 64])
 def test_canonical_small_scale_groups(sa, g):
     q, N, K = 2, 70, 576
@@ -199,7 +218,8 @@ def test_m1_kernel_choice(sa):
     assert kid(4096, 11008, q=3) == 4 and kid(80000, 4096) == 4
     assert kid(8192, 2048 * 20) == 1                      # S = 160 >= #SMs: register ring
     assert kid(4096, 4096, M=2, q=3) == 5 and kid(4096, 4096, M=2, q=4) == 2   # M = 2 cluster ring: q <= 3
-    assert kid(4096, 8192, M=2) == 2 and kid(4096, 4096, M=3) == 2
+    assert kid(4096, 8192, M=2) == 2 and kid(4096, 4096, M=3) == 6 and kid(4096, 4096, M=4, q=4) == 2
+    assert kid(4096, 4096, M=5) == 2
 
 
 @pytest.mark.parametrize("splitk", [False, True])
