@@ -53,7 +53,8 @@ def alg_bytes(M, q, N, K, g=G):
 KERNEL_NAMES = {0: "gemm_generic_kernel", 1: "gemv_tiled_kernel (grid split-K)", 2: "gemm_tiled_mb_kernel",
                 3: "gemv_cluster_ring_kernel (cluster split-K, TMA weight ring)",
                 4: "gemv_stream_kernel (grid split-K, TMA weight ring)",
-                5: "gemm_cluster_ring_m2_kernel (M = 2)", 6: "gemm_cluster_ring_m4_kernel (M = 3..4)"}
+                5: "gemm_cluster_ring_m2_kernel (M = 2)", 6: "gemm_cluster_ring_m4_kernel (M = 3..4)",
+                7: "gemm_cluster_ring_m2/m4 kernels (M > 4, row chunks)"}
 
 
 def kernel_names(layers):

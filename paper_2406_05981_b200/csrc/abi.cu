@@ -90,6 +90,11 @@ LaunchPlan make_plan(int layout, int M, int N, int K, int q, int g, int sms, uns
   if (M == 2 && !(flags & SHIFTADD_FLAG_SPLITK) && m2_applicable(N, K, q, sms)) return plan_gemm_m2(N, K, q, sms);
   if ((M == 3 || M == 4) && !(flags & SHIFTADD_FLAG_SPLITK) && m4_applicable(N, K, q, sms))
     return plan_gemm_m4(N, K, q, sms);
+  if (M > 4 && !(flags & SHIFTADD_FLAG_SPLITK) && m2_applicable(N, K, q, sms) && m4_applicable(N, K, q, sms)) {
+    LaunchPlan p = plan_gemm_m4(N, K, q, sms);   // row chunks of 2..4 through kernels 5/6
+    p.kernel = 7;
+    return p;
+  }
   return plan_gemm_tiled_mb(M, N, K, q, sms);
 }
 
@@ -407,12 +412,28 @@ shiftadd_status shiftadd_lut_gemm(const uint16_t* x, int ldx, const uint8_t* pla
   LaunchPlan p = make_plan(layout, M, N, K, q, g, di.sms, flags);
   // the TMA ring copies exponent tiles with 16-B bulk copies
   if (p.kernel == 4 && !aligned(exps, 16)) p = plan_gemv_tiled(N, K, q, di.sms);
-  if ((p.kernel == 5 || p.kernel == 6) && !aligned(exps, 16)) p = plan_gemm_tiled_mb(M, N, K, q, di.sms);
+  if ((p.kernel >= 5 && p.kernel <= 7) && !aligned(exps, 16)) p = plan_gemm_tiled_mb(M, N, K, q, di.sms);
   cudaError_t e;
   if (layout == SHIFTADD_LAYOUT_CANONICAL) e = launch_gemm_generic(a, p);
   else if (p.kernel == 3) e = launch_gemv_cluster(a, p);
   else if (p.kernel == 5) e = launch_gemm_m2(a, p);
   else if (p.kernel == 6) e = launch_gemm_m4(a, p);
+  else if (p.kernel == 7) {
+    // M > 4: row chunks of 4 (the last two 3 + 2 when M % 4 == 1), each one pass over the
+    // weights with 2- or 4-wide LUT entries (measured faster than one 16-row pass re-walking
+    // the weights per 4-row chunk on the split-K kernel)
+    e = cudaSuccess;
+    for (int m0 = 0; m0 < M && e == cudaSuccess;) {
+      const int left = M - m0;
+      const int mc = left >= 6 || left == 4 ? 4 : (left == 5 ? 3 : left);
+      GemmArgs c = a;
+      c.x = a.x + (size_t)m0 * ldx;
+      c.y = a.y + (size_t)m0 * ldy;
+      c.M = mc;
+      e = mc == 2 ? launch_gemm_m2(c, plan_gemm_m2(N, K, q, di.sms)) : launch_gemm_m4(c, plan_gemm_m4(N, K, q, di.sms));
+      m0 += mc;
+    }
+  }
   else if (M == 1) e = launch_gemv_tiled(a, p);
   else e = launch_gemm_tiled_mb(a, p);
   if (e == cudaErrorNotSupported) return fail(SHIFTADD_ERR_UNSUPPORTED, "no kernel for this configuration");

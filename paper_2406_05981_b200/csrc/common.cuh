@@ -206,7 +206,7 @@ struct LaunchPlan {
   int smem;
   int kernel;  // 0 generic, 1 tiled M=1 split-K, 2 tiled small batch, 3 tiled M=1 cluster split-K,
               // 4 tiled M=1 split-K with the TMA weight ring, 5 tiled M=2 cluster TMA ring,
-              // 6 tiled M=3..4 cluster TMA ring
+              // 6 tiled M=3..4 cluster TMA ring, 7 tiled M>4 as row chunks through 5/6
 };
 
 // Implemented in the kernel translation units.

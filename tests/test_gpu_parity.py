@@ -219,7 +219,7 @@ def test_m1_kernel_choice(sa):
     assert kid(8192, 2048 * 20) == 1                      # S = 160 >= #SMs: register ring
     assert kid(4096, 4096, M=2, q=3) == 5 and kid(4096, 4096, M=2, q=4) == 2   # M = 2 cluster ring: q <= 3
     assert kid(4096, 8192, M=2) == 2 and kid(4096, 4096, M=3) == 6 and kid(4096, 4096, M=4, q=4) == 2
-    assert kid(4096, 4096, M=5) == 2
+    assert kid(4096, 4096, M=5) == 7 and kid(4096, 4096, M=16, q=4) == 2   # M > 4: row chunks
 
 
 @pytest.mark.parametrize("splitk", [False, True])
