@@ -64,10 +64,12 @@ typedef enum { SHIFTADD_LAYOUT_CANONICAL = 0, SHIFTADD_LAYOUT_TILED = 1 } shifta
 #define SHIFTADD_FLAG_PDL 1u /* launch with programmatic dependent launch: the kernel's weight
                                 prefetch may overlap the previous kernel on the stream; x,
                                 y and the workspace are touched only after it completes. */
-#define SHIFTADD_FLAG_SPLITK 2u /* M = 1, tiled layout: always use the grid-wide split-K
-                                   decomposition (one K-slice per CTA, partials in the
-                                   workspace) instead of the cluster kernel chosen for
-                                   K <= 4096 (K-split reduced over distributed shared memory).
+#define SHIFTADD_FLAG_SPLITK 2u /* tiled layout: always use the grid-wide split-K
+                                   decompositions (K-slices per CTA, partials in the
+                                   workspace) -- for M = 1 the TMA-ring split-K kernel where
+                                   it applies, else the register-ring one; for M >= 2 the
+                                   small-batch split-K kernel -- instead of the cluster
+                                   kernels (K-split reduced over distributed shared memory).
                                    For testing and measurement; results agree within
                                    rounding order. */
 
@@ -231,8 +233,9 @@ shiftadd_status shiftadd_copy(void* dst, const void* src, size_t bytes, unsigned
 /* Launch geometry the gemm call would use (for measurement/reporting; host only):
  * out[0] = grid CTAs, out[1] = threads per CTA, out[2] = dynamic smem bytes,
  * out[3] = kernel id (0 generic, 1 tiled M=1 split-K, 2 tiled small-batch, 3 tiled M=1
- * cluster split-K, 4 tiled M=1 split-K with the TMA weight ring), for flags = 0.  Needs a
- * device. */
+ * cluster split-K (TMA weight ring), 4 tiled M=1 split-K with the TMA weight ring, 5 tiled M=2
+ * cluster TMA ring, 6 tiled M=3..4 cluster TMA ring, 7 tiled M>4 as row chunks of <= 4
+ * through 5/6), for flags = 0.  Needs a device. */
 shiftadd_status shiftadd_gemm_plan(int layout, int M, int N, int K, int q, int g, int out[4]);
 
 #ifdef __cplusplus
