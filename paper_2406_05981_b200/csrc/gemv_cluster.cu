@@ -724,6 +724,7 @@ gemv_cluster_ring_kernel(const __half* __restrict__ x, const uint8_t* __restrict
       const int j = t % NST;
       const int i = t * NW + warp;
       rmbar_wait(full + 8 * j, (uint32_t)((t / NST) & 1));
+      if (tr && tid == 0 && (t == 0 || t == nstages - 1)) tr[t == 0 ? 10 : 11] = gtimer_ns();
       if (i < Mc) {
         uint4 w[Q];
         int e[Q];

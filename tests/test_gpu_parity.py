@@ -404,3 +404,24 @@ def test_misaligned_exponents_use_register_ring(sa, q, N, K):
     y_ref = oracle.gemm(x.cpu().numpy(), planes, exps, g)
     for y in (y0, y1):
         assert oracle.err_floor(y.float().cpu().numpy(), y_ref) <= TOL
+
+
+@pytest.mark.parametrize("M,kid", [(2, 5), (3, 6), (4, 6), (7, 7)])
+def test_small_batch_ring_exact_invariants(sa, M, kid):
+    """The small-batch cluster-ring kernels (float2 / float4 entries, row chunks): row m of x
+    set to the basis vector e_{j_m} gives the fp16-rounded column j_m exactly, and
+    y(-x) = -y(x) bit-exactly."""
+    layer, planes, exps, (q, N, K, g) = _exact_layer(sa, 1, q=3, N=80, K=1024)
+    assert sa.gemm_plan(layer, M)[3] == kid
+    W = oracle.dequant(planes, exps, g, K)
+    js = [0, 7, 256, 300, 511, 1000, K - 1][:M]
+    x = torch.zeros((M, K), dtype=torch.float16)
+    for m, j in enumerate(js):
+        x[m, j] = 1.0
+    y = _run(sa, x, layer).cpu().numpy()
+    for m, j in enumerate(js):
+        assert np.array_equal(y[m], oracle.to_fp16(W[:, j])), (m, j)
+    xr = synth.gen_x(M, K, seed=21)
+    y1 = _run(sa, xr, layer).float().cpu()
+    y2 = _run(sa, -xr, layer).float().cpu()
+    assert torch.equal(y2, -y1)

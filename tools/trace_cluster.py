@@ -30,7 +30,8 @@ assert kid == 3, kid
 tr = ws.buf[need:need + G * 256].cpu().numpy().view(np.uint64).reshape(G, 32).astype(np.int64)
 t0 = tr[:, 0].min()
 print("N=%d K=%d q=%d G=%d pdl=%d  (us from first CTA start)" % (N, K, q, G, PDL))
-for nm, c in [("start", 0), ("pre_x", 8), ("x_arrived", 9), ("x_staged", 1), ("luts_built", 2), ("loop_end", 3), ("cl_sync", 4), ("end", 5)]:
+for nm, c in [("start", 0), ("pre_x", 8), ("x_arrived", 9), ("x_staged", 1), ("luts_built", 2), ("stage0_full", 10),
+              ("last_full", 11), ("loop_end", 3), ("cl_sync", 4), ("end", 5)]:
     v = (tr[:, c] - t0) / 1000.0
     print("  %-10s min %7.2f  med %7.2f  max %7.2f" % (nm, v.min(), np.median(v), v.max()))
 le = (tr[:, 3] - t0) / 1000.0
