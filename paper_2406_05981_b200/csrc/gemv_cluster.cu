@@ -654,25 +654,21 @@ gemv_cluster_ring_kernel(const __half* __restrict__ x, const uint8_t* __restrict
   const int own_lo = (int)rank * chunk;
   const int cnt = rows - own_lo < chunk ? (rows - own_lo > 0 ? rows - own_lo : 0) : chunk;
   const float inv_chunk_rg = 1.f / (float)chunk_rg;
-  // The producer initialises its own stage barriers and starts streaming at once; the
-  // consumers meet it on named barrier 2 (producer: bar.arrive) only before their first stage
-  // wait.  (A CTA-wide barrier after all the inits put ~0.5 us in front of the first request.)
-  if (tid == 0) mbar_init_expect(bar, (uint32_t)((S - Sc) * cnt * 4));   // peers' pushes
+  if (tid == 0) {
+    mbar_init_expect(bar, (uint32_t)((S - Sc) * cnt * 4));
+    for (int j = 0; j < NST; ++j) {
+      rmbar_init(full + 8 * j, 1);
+      rmbar_init(empty + 8 * j, NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
   cluster_arrive_relaxed();
   const int nstages = (Mc + SI - 1) / SI;
 
   if (warp == NW) {
     // producer: stage t = items [16t, 16t + 16), one contiguous unit range per slice
-    if (lane == 0) {
-      for (int j = 0; j < NST; ++j) {
-        rmbar_init(full + 8 * j, 1);
-        rmbar_init(empty + 8 * j, NW);
-      }
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-    __syncwarp();
-    asm volatile("bar.arrive 2, %0;" ::"r"(NT) : "memory");
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
       for (int t = 0; t < nstages; ++t) {
@@ -715,7 +711,6 @@ gemv_cluster_ring_kernel(const __half* __restrict__ x, const uint8_t* __restrict
     }
     asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
     if (tr && tid == 0) tr[2] = gtimer_ns();
-    asm volatile("bar.sync 2, %0;" ::"r"(NT) : "memory");   // the producer's stage barriers exist
     cluster_wait();   // every peer's receive mbarrier is initialised
     uint32_t cstE[8], cstO[8];
 #pragma unroll
