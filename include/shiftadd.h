@@ -66,12 +66,11 @@ typedef enum { SHIFTADD_LAYOUT_CANONICAL = 0, SHIFTADD_LAYOUT_TILED = 1 } shifta
                                 y and the workspace are touched only after it completes. */
 #define SHIFTADD_FLAG_SPLITK 2u /* tiled layout: always use the grid-wide split-K
                                    decompositions (K-slices per CTA, partials in the
-                                   workspace) -- for M = 1 the TMA-ring split-K kernel where
-                                   it applies, else the register-ring one; for M >= 2 the
-                                   small-batch split-K kernel -- instead of the cluster
-                                   kernels (K-split reduced over distributed shared memory).
-                                   For testing and measurement; results agree within
-                                   rounding order. */
+                                   workspace) -- for M = 1 the all-SM streaming kernel (id 8)
+                                   where K <= 256 x #SMs; for M >= 2 the small-batch split-K
+                                   kernel -- instead of the cluster kernels (K-split reduced
+                                   over distributed shared memory).  For testing and
+                                   measurement; results agree within rounding order. */
 
 int shiftadd_abi_version(void);
 const char* shiftadd_status_string(int status);
@@ -122,6 +121,30 @@ shiftadd_status shiftadd_lut_gemm(const uint16_t* x, int ldx, const uint8_t* pla
                                   const int8_t* exps, int layout, int M, int N, int K, int q,
                                   int g, uint16_t* y, int ldy, void* workspace,
                                   size_t workspace_bytes, unsigned flags, void* stream);
+
+/* Fused projections (§8 a3/a6; BASELINE north_star "mixed 2/3/4-bit per-layer dispatch"):
+ * several output segments that read the same activations x -- LLaMA q/k/v, or gate/up --
+ * in ONE launch, each with its own packed weights and bit width (PAPER.md:286-292 allocates
+ * q per layer, so the k_proj of a block may carry 3 bits while q/v carry 2).  Segment i:
+ *   y_i[n] = fp16_rne( sum_j sum_G 2^{e_i[j][n][G]} sum_{k in G} s_i(j,n,k) x[k] ), n < N_i.
+ * Equivalent to nseg shiftadd_lut_gemv calls; the one launch builds each K-slice's LUT once
+ * for all segments and streams their weights as one byte range per slice (all-SM streaming
+ * kernel, id 8).  Batch 1 (M = 1), tiled layout only, K % 256 == 0, K <= 256 x #SMs,
+ * 1 <= nseg <= 4, each segment 1 <= q <= 4 with planes / exps 16-B aligned (packed by
+ * shiftadd_pack with the same K and g), y_i fp16 [N_i].  Workspace: shiftadd_workspace_bytes_fused
+ * bytes (same zero-once contract as shiftadd_lut_gemm; calls of either kind may share it, not
+ * concurrently).  flags: 0 or SHIFTADD_FLAG_PDL. */
+typedef struct {
+  const uint8_t* planes; /* tiled planes of segment i            */
+  const int8_t* exps;    /* tiled exponents of segment i         */
+  int N;                 /* output rows of segment i             */
+  int q;                 /* bit width of segment i (1..4)        */
+  uint16_t* y;           /* fp16 [N] output of segment i         */
+} shiftadd_segment;
+size_t shiftadd_workspace_bytes_fused(int layout, int M, int K, int g, int nseg, const shiftadd_segment* segs);
+shiftadd_status shiftadd_lut_gemv_fused(const uint16_t* x, int K, int g, int layout, int nseg,
+                                        const shiftadd_segment* segs, void* workspace, size_t workspace_bytes,
+                                        unsigned flags, void* stream);
 
 /* Batch-1 convenience: shiftadd_lut_gemm with M = 1, ldx = K, ldy = N. */
 shiftadd_status shiftadd_lut_gemv(const uint16_t* x, const uint8_t* planes, const int8_t* exps,
@@ -235,7 +258,7 @@ shiftadd_status shiftadd_copy(void* dst, const void* src, size_t bytes, unsigned
  * out[3] = kernel id (0 generic, 1 tiled M=1 split-K, 2 tiled small-batch, 3 tiled M=1
  * cluster split-K (TMA weight ring), 4 tiled M=1 split-K with the TMA weight ring, 5 tiled M=2
  * cluster TMA ring, 6 tiled M=3..4 cluster TMA ring, 7 tiled M>4 as row chunks of <= 4
- * through 5/6), for flags = 0.  Needs a device. */
+ * through 5/6, 8 tiled all-SM streaming LUT-GEMV), for flags = 0.  Needs a device. */
 shiftadd_status shiftadd_gemm_plan(int layout, int M, int N, int K, int q, int g, int out[4]);
 
 #ifdef __cplusplus

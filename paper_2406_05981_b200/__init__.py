@@ -23,6 +23,7 @@ __all__ = [
     "LAYOUT_CANONICAL", "LAYOUT_TILED", "FLAG_PDL", "FLAG_SPLITK", "EXP_ZERO", "ShiftAddError", "lib",
     "PackedLayer", "packed_bytes", "pack", "lut_gemm", "lut_gemv", "workspace_bytes",
     "gemm_plan", "Workspace", "pack_colwise", "lut_gemv_colwise", "pack_apot2", "bcq_quantize",
+    "lut_gemv_fused", "workspace_bytes_fused",
 ]
 
 LAYOUT_CANONICAL = 0
@@ -39,6 +40,12 @@ _lib_lock = threading.Lock()
 
 class ShiftAddError(RuntimeError):
     pass
+
+
+class _Segment(ctypes.Structure):
+    """shiftadd_segment (include/shiftadd.h)."""
+    _fields_ = [("planes", ctypes.c_void_p), ("exps", ctypes.c_void_p), ("N", ctypes.c_int), ("q", ctypes.c_int),
+                ("y", ctypes.c_void_p)]
 
 
 def lib():
@@ -89,6 +96,11 @@ def lib():
         L.shiftadd_gather_wait.argtypes = [vp, c_int, vp, vp]
         L.shiftadd_copy.restype = c_int
         L.shiftadd_copy.argtypes = [vp, vp, c_size, ctypes.c_uint, vp]
+        L.shiftadd_workspace_bytes_fused.restype = c_size
+        L.shiftadd_workspace_bytes_fused.argtypes = [c_int, c_int, c_int, c_int, c_int, ctypes.POINTER(_Segment)]
+        L.shiftadd_lut_gemv_fused.restype = c_int
+        L.shiftadd_lut_gemv_fused.argtypes = [vp, c_int, c_int, c_int, c_int, ctypes.POINTER(_Segment), vp, c_size,
+                                              ctypes.c_uint, vp]
         L.shiftadd_gemm_plan.restype = c_int
         L.shiftadd_gemm_plan.argtypes = [c_int] * 6 + [ctypes.POINTER(c_int * 4)]
         v = L.shiftadd_abi_version()
@@ -299,8 +311,11 @@ class Workspace:
 _default_ws = {}
 
 
-def _workspace_for(device):
-    key = (device.index, torch.cuda.current_stream(device).cuda_stream)
+def _workspace_for(device, stream=None):
+    """Default workspace of (device, launch stream): calls on different streams never share
+    one (their split-K partials / epoch counters would race)."""
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    key = (device.index, s.cuda_stream)
     ws = _default_ws.get(key)
     if ws is None:
         ws = _default_ws[key] = Workspace(device)
@@ -312,7 +327,8 @@ def lut_gemm(x: torch.Tensor, layer: PackedLayer, out: torch.Tensor | None = Non
              splitk: bool = False) -> torch.Tensor:
     """§8 a2-a7: y[M][N] = x[M][K] (.) the packed layer, fp16 in/out (shiftadd_lut_gemm).
 
-    splitk forces the split-K decomposition for M = 1 (SHIFTADD_FLAG_SPLITK)."""
+    splitk forces the grid-wide split-K decompositions (SHIFTADD_FLAG_SPLITK), for testing and
+    measurement."""
     squeeze = x.dim() == 1
     x2 = x.unsqueeze(0) if squeeze else x
     if x2.dtype != torch.float16 or not x2.is_cuda or x2.device != layer.device:
@@ -346,7 +362,7 @@ def lut_gemm(x: torch.Tensor, layer: PackedLayer, out: torch.Tensor | None = Non
     need = layer._ws_bytes.get(M)
     if need is None:
         need = layer._ws_bytes[M] = workspace_bytes(layer, M)
-    ws = (workspace or _workspace_for(dev)).get(need)
+    ws = (workspace or _workspace_for(dev, stream)).get(need)
     if torch.cuda.current_device() != dev.index:
         torch.cuda.set_device(dev)
     sptr = (stream if stream is not None else torch.cuda.current_stream(dev)).cuda_stream
@@ -358,6 +374,53 @@ def lut_gemm(x: torch.Tensor, layer: PackedLayer, out: torch.Tensor | None = Non
     if st:
         _check(st, "shiftadd_lut_gemm")
     return out[0] if squeeze else out
+
+
+def _segments(layers, outs):
+    arr = (_Segment * len(layers))()
+    for i, (L, y) in enumerate(zip(layers, outs)):
+        arr[i].planes = L.planes.data_ptr()
+        arr[i].exps = L.exps.data_ptr()
+        arr[i].N = L.N
+        arr[i].q = L.q
+        arr[i].y = y.data_ptr() if y is not None else None
+    return arr
+
+
+def workspace_bytes_fused(layers, M: int = 1) -> int:
+    L0 = layers[0]
+    return int(lib().shiftadd_workspace_bytes_fused(L0.layout, M, L0.K, L0.g, len(layers),
+                                                    _segments(layers, [None] * len(layers))))
+
+
+def lut_gemv_fused(x: torch.Tensor, layers, outs=None, workspace: Workspace | None = None, pdl: bool = False,
+                   stream=None):
+    """Fused projections sharing x (shiftadd_lut_gemv_fused): one launch computes
+    y_i = x (.) layers[i] for every segment i, each with its own bit width.  x: fp16 [K];
+    layers: tiled PackedLayers with the same K and g; returns the list of y_i (fp16 [N_i])."""
+    x = x.reshape(-1)
+    if x.dtype != torch.float16 or not x.is_cuda:
+        raise ValueError("x must be fp16 on the device")
+    if not 1 <= len(layers) <= 4:
+        raise ValueError("1..4 segments")
+    dev = layers[0].device
+    if outs is None:
+        outs = [torch.empty(L.N, dtype=torch.float16, device=dev) for L in layers]
+    for L, y in zip(layers, outs):
+        if L.K != x.numel() or L.g != layers[0].g or L.layout != LAYOUT_TILED or L.colwise or L.exps2 is not None:
+            raise ValueError("fused segments: tiled row-wise layers with the K and g of x")
+        if y.dtype != torch.float16 or y.numel() != L.N or not y.is_contiguous():
+            raise ValueError("outs must be contiguous fp16 [N_i]")
+    segs = _segments(layers, outs)
+    need = int(lib().shiftadd_workspace_bytes_fused(LAYOUT_TILED, 1, x.numel(), layers[0].g, len(layers), segs))
+    ws = (workspace or _workspace_for(dev, stream)).get(need)
+    if torch.cuda.current_device() != dev.index:
+        torch.cuda.set_device(dev)
+    sptr = (stream if stream is not None else torch.cuda.current_stream(dev)).cuda_stream
+    _check(lib().shiftadd_lut_gemv_fused(x.data_ptr(), x.numel(), layers[0].g, LAYOUT_TILED, len(layers), segs,
+                                         ws.data_ptr() if ws is not None else None, ws.numel() if ws is not None else 0,
+                                         FLAG_PDL if pdl else 0, sptr), "shiftadd_lut_gemv_fused")
+    return outs
 
 
 def lut_gemv(x: torch.Tensor, layer: PackedLayer, **kw) -> torch.Tensor:

@@ -76,15 +76,25 @@ shiftadd_status check_layout(int layout, int K, int g) {
   return SHIFTADD_OK;
 }
 
+// shared-memory budget of the streaming kernel's CTA (one per SM): LUT slab + weight ring
+constexpr int kStreamSmemBudget = 200 * 1024;
+
 size_t tiled_rows(int N) { return (size_t)((N + kTileRows - 1) / kTileRows); }
 
 LaunchPlan make_plan(int layout, int M, int N, int K, int q, int g, int sms, unsigned flags) {
   if (layout == SHIFTADD_LAYOUT_CANONICAL) return plan_generic(M, N, K, q, g, sms);
   if (M == 1) {
-    const bool stream = stream_applicable(N, K, q, sms);
-    if (!(flags & SHIFTADD_FLAG_SPLITK) && cluster_applicable(N, K, q, sms) && !(stream && cluster_is_4slot(N, K, q)))
+    // K <= 4096: the cluster kernel (K-split reduced over DSMEM, measured faster at these
+    // sizes); larger K (and SHIFTADD_FLAG_SPLITK): the all-SM streaming kernel (id 8), whose
+    // split-K goes through the workspace.  The register-ring / TMA-ring split-K kernels (ids
+    // 1, 4) remain for K > 256 x #SMs.
+    if (!(flags & SHIFTADD_FLAG_SPLITK) && K <= 4096 && cluster_applicable(N, K, q, sms))
       return plan_gemv_cluster(N, K, q, sms);
-    if (stream) return plan_gemv_stream(N, K, q, sms);
+    if (stream_shape_ok(K, sms)) {
+      const int nst = stream_stages(q, kStreamSmemBudget, 16);
+      return LaunchPlan{sms, 17 * 32, stream_smem_bytes(q, nst, 16), 8};
+    }
+    if (stream_applicable(N, K, q, sms)) return plan_gemv_stream(N, K, q, sms);
     return plan_gemv_tiled(N, K, q, sms);
   }
   if (M == 2 && !(flags & SHIFTADD_FLAG_SPLITK) && m2_applicable(N, K, q, sms)) return plan_gemm_m2(N, K, q, sms);
@@ -100,7 +110,11 @@ LaunchPlan make_plan(int layout, int M, int N, int K, int q, int g, int sms, uns
 
 size_t workspace_for(int layout, int M, int N, int K) {
   if (layout == SHIFTADD_LAYOUT_CANONICAL) return 0;
-  if (M == 1) return workspace_gemv_tiled(N, K);
+  if (M == 1) {
+    const size_t a = workspace_gemv_tiled(N, K);
+    const size_t b = stream_workspace_bytes(1, K / kTileK, (N + kTileRows - 1) / kTileRows);
+    return a > b ? a : b;
+  }
   return workspace_gemm_tiled_mb(M, N, K);
 }
 
@@ -352,6 +366,13 @@ shiftadd_status shiftadd_copy(void* dst, const void* src, size_t bytes, unsigned
   return SHIFTADD_OK;
 }
 
+#ifdef SHIFTADD_DEV_TRACE
+// development builds only: per-CTA phase timestamps of the streaming kernel into `buf`
+// (16 u64 per CTA), NULL to stop
+int shiftadd_dev_set_trace(void* buf) { return (int)dev_set_trace(buf); }
+void shiftadd_dev_set_variant(int v) { dev_set_variant(v); }
+#endif
+
 size_t shiftadd_workspace_bytes(int layout, int M, int N, int K, int q, int g) {
   if (check_shape(q, N, K, g, 4) != SHIFTADD_OK || check_layout(layout, K, g) != SHIFTADD_OK) return 0;
   if (M < 1 || M > 16) return 0;
@@ -411,10 +432,30 @@ shiftadd_status shiftadd_lut_gemm(const uint16_t* x, int ldx, const uint8_t* pla
   a.stream = reinterpret_cast<cudaStream_t>(stream);
   LaunchPlan p = make_plan(layout, M, N, K, q, g, di.sms, flags);
   // the TMA ring copies exponent tiles with 16-B bulk copies
-  if (p.kernel == 4 && !aligned(exps, 16)) p = plan_gemv_tiled(N, K, q, di.sms);
+  if ((p.kernel == 4 || p.kernel == 8) && !aligned(exps, 16)) p = plan_gemv_tiled(N, K, q, di.sms);
   if ((p.kernel >= 5 && p.kernel <= 7) && !aligned(exps, 16)) p = plan_gemm_tiled_mb(M, N, K, q, di.sms);
   cudaError_t e;
   if (layout == SHIFTADD_LAYOUT_CANONICAL) e = launch_gemm_generic(a, p);
+  else if (p.kernel == 8) {
+    StreamLaunch L = {};
+    L.x = a.x;
+    L.K = K;
+    L.nseg = 1;
+    L.seg[0] = StreamSeg{planes, exps, a.y, q, N};
+    L.workspace = workspace;
+    L.grid = p.grid;
+    L.su = 16;
+    L.nst = stream_stages(q, kStreamSmemBudget, L.su);
+    L.pdl = (flags & SHIFTADD_FLAG_PDL) ? 1 : 0;
+#ifdef SHIFTADD_DEV_TRACE
+    if (g_dev_variant & 1) {
+      L.half = 1;
+      L.nst = stream_stages(q, 112 * 1024, L.su);
+      if (L.nst < 2) L.half = 0, L.nst = stream_stages(q, kStreamSmemBudget, L.su);
+    }
+#endif
+    e = launch_lut_stream(L, a.stream);
+  }
   else if (p.kernel == 3) e = launch_gemv_cluster(a, p);
   else if (p.kernel == 5) e = launch_gemm_m2(a, p);
   else if (p.kernel == 6) e = launch_gemm_m4(a, p);
@@ -438,6 +479,62 @@ shiftadd_status shiftadd_lut_gemm(const uint16_t* x, int ldx, const uint8_t* pla
   else e = launch_gemm_tiled_mb(a, p);
   if (e == cudaErrorNotSupported) return fail(SHIFTADD_ERR_UNSUPPORTED, "no kernel for this configuration");
   if (e != cudaSuccess) return cuda_fail(e, "lut_gemm launch");
+  return SHIFTADD_OK;
+}
+
+size_t shiftadd_workspace_bytes_fused(int layout, int M, int K, int g, int nseg, const shiftadd_segment* segs) {
+  if (layout != SHIFTADD_LAYOUT_TILED || !segs || nseg < 1 || nseg > kMaxSegments || M < 1 || M > 16) return 0;
+  if (K < kTileK || K % kTileK || g < 128 || g % 128 || K % g) return 0;
+  int rg = 0;
+  for (int i = 0; i < nseg; ++i) {
+    if (segs[i].N < 1 || segs[i].N > kMaxRows) return 0;
+    rg += (segs[i].N + kTileRows - 1) / kTileRows;
+  }
+  return stream_workspace_bytes(M, K / kTileK, rg);
+}
+
+shiftadd_status shiftadd_lut_gemv_fused(const uint16_t* x, int K, int g, int layout, int nseg,
+                                        const shiftadd_segment* segs, void* workspace, size_t workspace_bytes,
+                                        unsigned flags, void* stream) {
+  if (!x || !segs) return fail(SHIFTADD_ERR_INVALID, "null pointer argument");
+  if (layout != SHIFTADD_LAYOUT_TILED) return fail(SHIFTADD_ERR_UNSUPPORTED, "fused segments need the tiled layout");
+  if (nseg < 1 || nseg > kMaxSegments) return fail(SHIFTADD_ERR_INVALID, "nseg=%d outside [1, %d]", nseg, kMaxSegments);
+  if (flags & ~SHIFTADD_FLAG_PDL) return fail(SHIFTADD_ERR_INVALID, "unknown flags 0x%x", flags);
+  if (!aligned(x, 16)) return fail(SHIFTADD_ERR_INVALID, "x must be 16-B aligned");
+  shiftadd_status st;
+  int rg = 0;
+  for (int i = 0; i < nseg; ++i) {
+    const shiftadd_segment& sg = segs[i];
+    if (!sg.planes || !sg.exps || !sg.y) return fail(SHIFTADD_ERR_INVALID, "segment %d: null pointer", i);
+    if ((st = check_shape(sg.q, sg.N, K, g, 4)) != SHIFTADD_OK) return st;
+    if (!aligned(sg.planes, 16) || !aligned(sg.exps, 16) || !aligned(sg.y, 2))
+      return fail(SHIFTADD_ERR_INVALID, "segment %d: planes / exps must be 16-B aligned", i);
+    rg += (sg.N + kTileRows - 1) / kTileRows;
+  }
+  if ((st = check_layout(layout, K, g)) != SHIFTADD_OK) return st;
+  DevInfo di;
+  if ((st = device_info(&di)) != SHIFTADD_OK) return st;
+  if (!stream_shape_ok(K, di.sms))
+    return fail(SHIFTADD_ERR_UNSUPPORTED, "fused segments: K=%d above 256 x %d SMs", K, di.sms);
+  const size_t need = stream_workspace_bytes(1, K / kTileK, rg);
+  if (!workspace || workspace_bytes < need || !aligned(workspace, 16))
+    return fail(SHIFTADD_ERR_INVALID, "workspace needs %zu bytes, 16-B aligned (got %zu)", need, workspace_bytes);
+  StreamLaunch L = {};
+  L.x = reinterpret_cast<const __half*>(x);
+  L.K = K;
+  L.nseg = nseg;
+  int qmax = 1;
+  for (int i = 0; i < nseg; ++i) {
+    L.seg[i] = StreamSeg{segs[i].planes, segs[i].exps, reinterpret_cast<__half*>(segs[i].y), segs[i].q, segs[i].N};
+    qmax = segs[i].q > qmax ? segs[i].q : qmax;
+  }
+  L.workspace = workspace;
+  L.grid = di.sms;
+  L.su = 16;
+  L.nst = stream_stages(qmax, kStreamSmemBudget, L.su);
+  L.pdl = (flags & SHIFTADD_FLAG_PDL) ? 1 : 0;
+  const cudaError_t e = launch_lut_stream(L, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "lut_gemv_fused launch");
   return SHIFTADD_OK;
 }
 

@@ -200,13 +200,35 @@ struct GemmArgs {
   cudaStream_t stream;
 };
 
+// The all-SM streaming LUT-GEMV (lut_stream.cu, kernel id 8): one launch covers one or several
+// output segments that share x (fused projections), each with its own packed weights and q.
+constexpr int kMaxSegments = 4;
+// its workspace region: after the split-K counters and the fused-gather launch counter
+constexpr size_t kStreamWsOff = kCounterBytes + 256;
+struct StreamSeg {
+  const uint8_t* planes;
+  const int8_t* exps;
+  __half* y;
+  int q, N;
+};
+struct StreamLaunch {
+  const __half* x;
+  int K;
+  int nseg;
+  StreamSeg seg[kMaxSegments];
+  void* workspace;
+  int grid, nst, su, pdl;
+  int half;   // 1: the co-resident variant (<= 113 KB shared memory, two CTAs fit one SM)
+};
+
 struct LaunchPlan {
   int grid;
   int threads;
   int smem;
   int kernel;  // 0 generic, 1 tiled M=1 split-K, 2 tiled small batch, 3 tiled M=1 cluster split-K,
               // 4 tiled M=1 split-K with the TMA weight ring, 5 tiled M=2 cluster TMA ring,
-              // 6 tiled M=3..4 cluster TMA ring, 7 tiled M>4 as row chunks through 5/6
+              // 6 tiled M=3..4 cluster TMA ring, 7 tiled M>4 as row chunks through 5/6,
+              // 8 tiled all-SM streaming LUT-GEMV (lut_stream.cu)
 };
 
 // Implemented in the kernel translation units.
@@ -247,6 +269,17 @@ cudaError_t launch_gemv_colwise(const GemmArgs& a);
 cudaError_t launch_gather_wait(const uint32_t* flags, int P, uint32_t* epoch, cudaStream_t stream);
 LaunchPlan plan_gemv_cluster(int N, int K, int q, int sms);
 cudaError_t launch_gemv_cluster(const GemmArgs& a, const LaunchPlan& p);
+
+int stream_smem_bytes(int qmax, int nst, int su);
+int stream_stages(int qmax, int budget, int su);
+size_t stream_workspace_bytes(int M, int S, int RGtot);
+bool stream_shape_ok(int K, int sms);
+cudaError_t launch_lut_stream(const StreamLaunch& L, cudaStream_t stream);
+#ifdef SHIFTADD_DEV_TRACE
+cudaError_t dev_set_trace(void* buf);
+extern int g_dev_variant;
+void dev_set_variant(int v);
+#endif
 
 LaunchPlan plan_gemm_tiled_mb(int M, int N, int K, int q, int sms);
 size_t workspace_gemm_tiled_mb(int M, int N, int K);

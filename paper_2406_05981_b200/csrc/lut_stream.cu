@@ -1,0 +1,602 @@
+// lut_stream.cu -- the all-SM streaming LUT-GEMV for the tiled layout (§8 a2-a6; kernel id 8).
+//
+// y = sum_i alpha_i (.) (B_i x) with LUT queries and exponent-add shifts,
+// for one or several output "segments" that share the activations x (fused projections:
+// LLaMA q/k/v or gate/up), each with its own bit width q (mixed 2/3/4-bit dispatch, §8 a6,
+// PAPER.md:286-292).
+//
+// Decomposition.  A unit is (256-k slice s, segment, 16-row group rg); units are numbered
+// slice-major.  A unit of a q-bit segment weighs q (its bytes).  The grid is one CTA per SM
+// and CTA c takes the units whose weight offset falls in [c W/G, (c+1) W/G): one contiguous
+// byte range per (slice, segment), at most two slices per CTA (S <= G), so the CTA builds at
+// most two LUTs (a2), once, in the two column halves of one 64 KB slab.
+//
+// Weights.  Warp 16 is a producer: one thread streams the CTA's units through a ring of
+// shared-memory stages with 1-D bulk copies (cp.async.bulk, the TMA engine), 16 units per
+// stage, each stage completing on its "full" mbarrier and released by the 16 consumer warps on
+// its "empty" one.  It starts at kernel entry, before griddepcontrol.wait: the weights never
+// depend on the upstream kernel (SHIFTADD_FLAG_PDL contract), so HBM is busy while the
+// previous call drains.  The consumers wait, fetch x, build the LUTs, then take one unit per
+// warp per stage: LDS.128 of the lane's 16 key bytes per plane (the tiled layout's rotation
+// makes every lookup step hit 32 different LUT columns: conflict-free), one PRMT + one
+// LDS [R+imm] + one FADD per key byte (a3), the chunk sum times 2^e by an exponent-field add
+// (a4).
+//
+// Split-K reduction (a5) without fences or counters.  Every (slice, row) partial goes to the
+// workspace as one 64-bit word {epoch, fp32 bits}, stored with a single relaxed store, so a
+// reader that sees the call's epoch sees the value.  CTA c owns an equal share of the row
+// groups; after its own units it polls the S words of each owned row until all carry this
+// call's epoch, sums them in slice order (deterministic) and stores fp16 (RNE).  The epoch is
+// the call count: a 64-bit counter in the workspace to which every call's CTAs add exactly
+// 2^32 in total (CTA 0 adds 2^32 - (G-1), the others 1, fire-and-forget at their end) -- any
+// proper subset of the adds stays below the next multiple of 2^32, so every CTA of a call,
+// reading it after griddepcontrol.wait, sees the same epoch (counter >> 32) + 1, and stale
+// words of earlier calls never match.
+#include <mutex>
+
+#include "common.cuh"
+
+namespace shiftadd {
+namespace {
+
+constexpr int kNWC = 16;                     // consumer warps
+constexpr int kNT = (kNWC + 1) * 32;         // + one producer warp
+constexpr int kLutSlab = kLutBytes;          // 64 KB: two slices' LUTs (column halves)
+constexpr int kBarBytes = 512;               // full[16] at +0, empty[16] at +128, epoch at +256
+
+#ifdef SHIFTADD_DEV_TRACE
+// development builds only (tools/dev_build.sh): per-CTA phase timestamps
+__device__ unsigned long long* g_trace = nullptr;
+__device__ __forceinline__ void trace_at(int k) {
+  if (g_trace && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_trace[16 * blockIdx.x + k] = t;
+  }
+}
+__device__ __forceinline__ void trace_clk(int k, long long c0) {   // cycles since c0 (same SM)
+  if (g_trace && threadIdx.x == 0) g_trace[16 * blockIdx.x + k] = (unsigned long long)(clock64() - c0);
+}
+#else
+__device__ __forceinline__ void trace_at(int) {}
+__device__ __forceinline__ void trace_clk(int, long long) {}
+#endif
+
+struct SegDev {
+  const uint8_t* planes;
+  const int8_t* exps;
+  __half* y;
+  int q, RG, N, rgoff, woff;
+};
+
+struct StreamParams {
+  const __half* x;
+  int S, nseg, RGtot, Ws;   // Ws = sum over segments of q * RG (weight of one slice)
+  SegDev seg[kMaxSegments];
+  unsigned long long* done;   // epoch counter (workspace)
+  unsigned long long* part;   // {epoch, fp32} [S][RGtot * 16]
+  int nst, slot, slot_planes;
+  int su;    // units per stage (16, 8 or 4); consumer warp w serves stages t with
+             // t % (16 / su) == w / su, unit w % su
+  int pdl;
+};
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      ::"r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(pol) : "memory");
+}
+__device__ __forceinline__ uint4 lds_u4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ int lds_s8(uint32_t addr) {
+  int v;
+  asm volatile("ld.shared.s8 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// a2: the 32 LUTs of one 256-k slice into column half `hoff` (0 or 128 B) of the slab at
+// kDynBase, from the 8 activations of group `lane` (xv).  T[key] = (A[lo&3] + B[lo>>2]) +
+// (C[hi&3] + D[hi>>2]): key bit b <-> +x_b if set, -x_b if clear;
+// warp w writes the keys with hi nibble w, 32 consecutive words per store (conflict-free).
+__device__ __forceinline__ void build_lut(const uint4 xv, uint32_t hoff, int warp, int lane) {
+  const float2 f01 = __half22float2(*reinterpret_cast<const __half2*>(&xv.x));
+  const float2 f23 = __half22float2(*reinterpret_cast<const __half2*>(&xv.y));
+  const float2 f45 = __half22float2(*reinterpret_cast<const __half2*>(&xv.z));
+  const float2 f67 = __half22float2(*reinterpret_cast<const __half2*>(&xv.w));
+  const float A[4] = {-f01.x - f01.y, f01.x - f01.y, f01.y - f01.x, f01.x + f01.y};
+  const float B[4] = {-f23.x - f23.y, f23.x - f23.y, f23.y - f23.x, f23.x + f23.y};
+  const int hi = warp;
+  const float H = ((hi & 1 ? f45.x : -f45.x) + (hi & 2 ? f45.y : -f45.y)) +
+                  ((hi & 4 ? f67.x : -f67.x) + (hi & 8 ? f67.y : -f67.y));
+  const uint32_t col = kDynBase + hoff + 4 * lane;
+#pragma unroll
+  for (int lo = 0; lo < 16; ++lo) sts_f32(col + ((hi * 16 + lo) << 8), (A[lo & 3] + B[lo >> 2]) + H);
+}
+
+// PRMT selector for step j: byte0 <- column byte (j&3) of cst[j>>2], byte1 <- key byte (j&3)
+// of the weight word, bytes 2,3 <- sign of the column byte (< 0x80, so 0x00).
+__host__ __device__ constexpr uint32_t step_sel(int j) {
+  return ((8u | (4u + (j & 3))) << 12) | ((8u | (4u + (j & 3))) << 8) | ((uint32_t)(j & 3) << 4) | (4u + (j & 3));
+}
+
+// a4 -- the shift: 2^e as the float whose exponent field is e plus the
+// bias, formed with one integer multiply-add on the bits of 1.0 (e << 23 + 0x3f800000); the
+// chunk sum is then scaled in the accumulating FFMA.  p * 2^e is exact here (|p| in
+// [2^-24, 2^24] or 0, e in [EXP_MIN, EXP_MAX]), so fma(p, 2^e, acc) rounds exactly like
+// acc + (the exponent-field add on p) -- bit-identical to shift_pow2 + FADD, 3 instructions
+// instead of 9.  EXP_ZERO (-128) is clamped to -127, whose bit pattern is +0.0: the group
+// contributes 0.
+__device__ __forceinline__ float pow2_bits(int e) {
+  return __int_as_float((e < -127 ? -127 : e) * (1 << 23) + 0x3f800000);
+}
+
+// a3 + a4 for one unit (16 rows x 256 k, Q planes) read from a ring stage: per plane the 16
+// lookups of the lane's 16 key bytes (4 chains, fixed tree), scaled by 2^e and accumulated.
+template <int Q, uint32_t HOFF>
+__device__ __forceinline__ float unit_dot(uint32_t sp, uint32_t se, const uint32_t (&cst)[4]) {
+  uint4 w[Q];
+  int e[Q];
+#pragma unroll
+  for (int i = 0; i < Q; ++i) w[i] = lds_u4(sp + i * kTileBytes);
+#pragma unroll
+  for (int i = 0; i < Q; ++i) e[i] = lds_s8(se + i * kTileExps);
+  float acc = 0.f;
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    float p[4];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const uint32_t word = (j < 4) ? w[i].x : (j < 8) ? w[i].y : (j < 12) ? w[i].z : w[i].w;
+      const float v = lds_f32(kDynBase + HOFF + prmt(word, cst[j >> 2], step_sel(j)));
+      p[j & 3] = j < 4 ? v : p[j & 3] + v;
+    }
+    acc = __fmaf_rn((p[0] + p[1]) + (p[2] + p[3]), pow2_bits(e[i]), acc);
+  }
+  return acc;
+}
+
+// Position in the unit order: slice s, segment g, row group rg of that segment.
+struct Pos {
+  int s, g, rg;
+};
+
+// First unit whose weight offset is >= w (units are assigned by their starting offset).
+__device__ __forceinline__ Pos pos_at(const StreamParams& p, long long w) {
+  Pos r;
+  r.s = (int)(w / p.Ws);
+  int wi = (int)(w - (long long)r.s * p.Ws);
+  r.g = 0;
+  while (r.g + 1 < p.nseg && p.seg[r.g + 1].woff <= wi) ++r.g;
+  const int q = p.seg[r.g].q;
+  r.rg = (wi - p.seg[r.g].woff + q - 1) / q;
+  if (r.rg >= p.seg[r.g].RG) {
+    r.rg = 0;
+    if (++r.g == p.nseg) { r.g = 0; ++r.s; }
+  }
+  return r;
+}
+__device__ __forceinline__ bool before(const Pos& a, const Pos& b) {
+  return a.s != b.s ? a.s < b.s : (a.g != b.g ? a.g < b.g : a.rg < b.rg);
+}
+// End (exclusive) row group of the run (a.s, a.g) inside [a, end); moving to the next run.
+__device__ __forceinline__ int run_end(const StreamParams& p, const Pos& a, const Pos& end) {
+  return (a.s == end.s && a.g == end.g) ? end.rg : p.seg[a.g].RG;
+}
+__device__ __forceinline__ void next_run(const StreamParams& p, Pos& a, int re) {
+  a.rg = re;
+  if (a.rg >= p.seg[a.g].RG) {
+    a.rg = 0;
+    if (++a.g == p.nseg) { a.g = 0; ++a.s; }
+  }
+}
+
+// Ring position: slot j and its use count k (the phase parity is k & 1).
+struct RingPos {
+  int j, k;
+  __device__ __forceinline__ void next(int nst) {
+    if (++j == nst) { j = 0; ++k; }
+  }
+};
+
+// a3 + a4 for two units at once (ILP: the two lookup streams interleave, hiding LDS latency
+// and the per-unit wait/emit of the other).  v1 = false: unit 1 absent (acc[1] = 0).
+template <int Q, uint32_t HOFF>
+__device__ __forceinline__ void unit_dot2(uint32_t sp0, uint32_t se0, uint32_t sp1, uint32_t se1, bool v1,
+                                          const uint32_t (&cst)[4], float (&acc)[2]) {
+  uint4 w[2][Q];
+  int e[2][Q];
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    w[0][i] = lds_u4(sp0 + i * kTileBytes);
+    e[0][i] = lds_s8(se0 + i * kTileExps);
+  }
+  if (v1) {
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+      w[1][i] = lds_u4(sp1 + i * kTileBytes);
+      e[1][i] = lds_s8(se1 + i * kTileExps);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+      w[1][i] = make_uint4(0, 0, 0, 0);
+      e[1][i] = SHIFTADD_EXP_ZERO;   // contributes +0
+    }
+  }
+  acc[0] = 0.f;
+  acc[1] = 0.f;
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    float p[2][4];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const uint32_t word = (j < 4) ? w[u][i].x : (j < 8) ? w[u][i].y : (j < 12) ? w[u][i].z : w[u][i].w;
+        const float v = lds_f32(kDynBase + HOFF + prmt(word, cst[j >> 2], step_sel(j)));
+        p[u][j & 3] = j < 4 ? v : p[u][j & 3] + v;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      acc[u] = __fmaf_rn((p[u][0] + p[u][1]) + (p[u][2] + p[u][3]), pow2_bits(e[u][i]), acc[u]);
+  }
+}
+
+// Consumer side of one run (slice s, segment sg, row groups [rga, re)): the run's stages of su
+// units, taken two at a time -- warp w processes unit w of stage t and unit w of stage t + 1
+// together, then releases both.
+template <int Q, uint32_t HOFF>
+__device__ __forceinline__ void consume_run(const StreamParams& p, const SegDev& sg, int s, int rga, int re,
+                                            RingPos& rp, int& t, uint32_t ring, uint32_t full, uint32_t empty,
+                                            const uint32_t (&cst)[4], int wu, int lane, unsigned long long ep) {
+  const int r = lane >> 1, h = lane & 1;
+  // partial words [flat row group][slice][16 rows]: a unit's 16 sums are one 128-B line, and an
+  // owner's (row group, all slices) block is S contiguous lines
+  unsigned long long* prow = p.part + ((size_t)sg.rgoff * p.S + s) * kTileRows + r;
+  for (int rg = rga; rg < re; rg += 2 * p.su) {
+    const int n0 = re - rg < p.su ? re - rg : p.su;
+    const int left = re - rg - n0;
+    const int n1 = left < p.su ? left : p.su;   // may be <= 0: no second stage in this run
+    const RingPos r0 = rp;
+    rp.next(p.nst);
+    const RingPos r1 = rp;
+    if (n1 > 0) rp.next(p.nst);
+    t += n1 > 0 ? 2 : 1;
+    const uint32_t slot0 = ring + (uint32_t)(r0.j * p.slot), slot1 = ring + (uint32_t)(r1.j * p.slot);
+    const long long c0 = clock64();
+    mbar_wait(full + 8 * r0.j, (uint32_t)(r0.k & 1));
+    if (n1 > 0) mbar_wait(full + 8 * r1.j, (uint32_t)(r1.k & 1));
+    if (rg == rga) trace_clk(8, c0);
+    const bool u0 = wu < n0, u1 = wu < n1;
+    float acc[2] = {0.f, 0.f};
+    if (u0)
+      unit_dot2<Q, HOFF>(slot0 + (uint32_t)(wu * Q * kTileBytes + 16 * lane),
+                         slot0 + (uint32_t)(p.slot_planes + wu * Q * kTileExps + lane),
+                         slot1 + (uint32_t)(wu * Q * kTileBytes + 16 * lane),
+                         slot1 + (uint32_t)(p.slot_planes + wu * Q * kTileExps + lane), u1, cst, acc);
+    if (rg == rga) trace_clk(9, c0);
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(empty + 8 * r0.j);
+      if (n1 > 0) mbar_arrive(empty + 8 * r1.j);
+    }
+    acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
+    acc[1] += __shfl_xor_sync(0xffffffffu, acc[1], 1);
+    if (h == 0) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        if (k == 0 ? u0 : u1) {
+          const int u = rg + k * p.su + wu;
+          if (p.S == 1) {
+            const int nl = u * kTileRows + r;
+            if (nl < sg.N) sg.y[nl] = __float2half_rn(acc[k]);
+          } else {
+            st_relaxed_u64(prow + (size_t)u * p.S * kTileRows, ep | __float_as_uint(acc[k]));
+          }
+        }
+      }
+    }
+    if (rg == rga) trace_clk(10, c0);
+  }
+}
+
+template <uint32_t HOFF>
+__device__ __forceinline__ void consume_run_q(const StreamParams& p, const SegDev& sg, int s, int rga, int re,
+                                              RingPos& rp, int& t, uint32_t ring, uint32_t full, uint32_t empty,
+                                              const uint32_t (&cst)[4], int wu, int lane, unsigned long long ep) {
+  switch (sg.q) {
+    case 1: consume_run<1, HOFF>(p, sg, s, rga, re, rp, t, ring, full, empty, cst, wu, lane, ep); break;
+    case 2: consume_run<2, HOFF>(p, sg, s, rga, re, rp, t, ring, full, empty, cst, wu, lane, ep); break;
+    case 3: consume_run<3, HOFF>(p, sg, s, rga, re, rp, t, ring, full, empty, cst, wu, lane, ep); break;
+    default: consume_run<4, HOFF>(p, sg, s, rga, re, rp, t, ring, full, empty, cst, wu, lane, ep); break;
+  }
+}
+
+// MINB = 2: registers capped so that two CTAs fit one SM -- with <= 113 KB of shared memory
+// the next call's CTA becomes resident (and streams its weights) while this one finishes.
+template <int MINB>
+__global__ void __launch_bounds__(kNT, MINB) lut_stream_kernel(const __grid_constant__ StreamParams p) {
+  if (threadIdx.x == 0) check_dyn_base();
+  trace_at(0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (p.pdl) pdl_launch_dependents();
+  const long long G = gridDim.x, W = (long long)p.S * p.Ws, c = blockIdx.x;
+  const Pos start = pos_at(p, c * W / G);
+  const Pos end = pos_at(p, (c + 1) * W / G);
+  const uint32_t ring = kDynBase + kLutSlab;
+  const uint32_t bars = ring + (uint32_t)(p.nst * p.slot);
+  const uint32_t full = bars, empty = bars + 128;
+  const uint32_t s_epoch = bars + 256;   // this call's epoch (shared, written once)
+  if (tid == 0) {
+    for (int j = 0; j < p.nst; ++j) {
+      mbar_init(full + 8 * j, 1);
+      mbar_init(empty + 8 * j, p.su);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kNWC) {
+    // producer: one thread streams the CTA's runs into the ring, su units per stage
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      RingPos rp{0, 0};
+      int t = 0;
+      for (Pos a = start; before(a, end);) {
+        const int re = run_end(p, a, end);
+        const SegDev& sg = p.seg[a.g];
+        const size_t ub = (size_t)a.s * sg.RG;
+        for (int rg = a.rg; rg < re; rg += p.su, ++t, rp.next(p.nst)) {
+          if (rp.k > 0) mbar_wait(empty + 8 * rp.j, (uint32_t)((rp.k - 1) & 1));
+          const int n = re - rg < p.su ? re - rg : p.su;
+          const uint32_t bp = (uint32_t)(n * sg.q * kTileBytes), be = (uint32_t)(n * sg.q * kTileExps);
+          const uint32_t fb = full + 8 * rp.j;
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(bp + be) : "memory");
+          const uint32_t dst = ring + (uint32_t)(rp.j * p.slot);
+          bulk_g2s(dst, sg.planes + (ub + rg) * sg.q * kTileBytes, bp, fb, pol);
+          bulk_g2s(dst + (uint32_t)p.slot_planes, sg.exps + (ub + rg) * sg.q * kTileExps, be, fb, pol);
+        }
+        next_run(p, a, re);
+      }
+    }
+  } else {
+    // consumers: x of the (at most two) slices, their LUTs, the epoch, then the ring
+    if (p.pdl) pdl_wait();
+    trace_at(1);
+    const int s0 = start.s;
+    const bool any = before(start, end);
+    const bool two = end.s > s0 && !(end.s == s0 + 1 && end.g == 0 && end.rg == 0);
+    if (any) {
+      const uint64_t pol_keep = policy_evict_last();
+      const uint4 xa = ldg_keep(p.x + (size_t)s0 * kTileK + 8 * lane, pol_keep);
+      uint4 xb = xa;
+      if (two) xb = ldg_keep(p.x + (size_t)(s0 + 1) * kTileK + 8 * lane, pol_keep);
+      if (tid == 32 && p.S > 1)   // a lane whose x does not gate warp 0
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(s_epoch), "r"((unsigned)(ld_relaxed_u64(p.done) >> 32) + 1u)
+                     : "memory");
+      build_lut(xa, 0u, warp, lane);
+      if (two) build_lut(xb, 128u, warp, lane);
+    } else if (tid == 32 && p.S > 1) {
+      asm volatile("st.shared.u32 [%0], %1;" ::"r"(s_epoch), "r"((unsigned)(ld_relaxed_u64(p.done) >> 32) + 1u)
+                   : "memory");
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(kNWC * 32) : "memory");   // consumer warps only
+    trace_at(2);
+#ifdef SHIFTADD_DEV_TRACE
+    const long long c2 = clock64();
+#endif
+    unsigned ep32;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(ep32) : "r"(s_epoch) : "memory");
+    const unsigned long long ep = (unsigned long long)ep32 << 32;
+    const int r = lane >> 1, h = lane & 1;
+    uint32_t cst[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint32_t v = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) v |= (4u * (uint32_t)(16 * h + ((4 * k + b + r) & 15))) << (8 * b);
+      cst[k] = v;
+    }
+    const int wu = warp;
+    RingPos rp{0, 0};
+    int t = 0;
+    for (Pos a = start; before(a, end);) {
+      const int re = run_end(p, a, end);
+      if (a.s == s0)
+        consume_run_q<0u>(p, p.seg[a.g], a.s, a.rg, re, rp, t, ring, full, empty, cst, wu, lane, ep);
+      else
+        consume_run_q<128u>(p, p.seg[a.g], a.s, a.rg, re, rp, t, ring, full, empty, cst, wu, lane, ep);
+      next_run(p, a, re);
+    }
+#ifdef SHIFTADD_DEV_TRACE
+    trace_clk(11, c2);
+#endif
+  }
+  trace_at(4);
+  if (p.S == 1) return;
+
+  // a5 owner phase: rows of the flattened row groups [c RGtot / G, (c+1) RGtot / G)
+  __syncthreads();
+  trace_at(6);
+
+  unsigned ep;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(ep) : "r"(s_epoch) : "memory");
+  const int og0 = (int)(c * p.RGtot / G), og1 = (int)((c + 1) * p.RGtot / G);
+  const int R = (og1 - og0) * kTileRows;
+  // T threads per row; thread it takes row it % R (consecutive lanes: consecutive rows of one
+  // 128-B line) and slices it / R, it / R + T, ... in order, loading <= 16 words at once and
+  // re-polling only the stale ones.  The T partial sums of a row then meet in shared memory
+  // (the drained ring) and are added in part order: deterministic for a launch shape.
+  int T = R > 0 ? kNT / R : 1;
+  T = T < 1 ? 1 : (T > p.S ? p.S : T);
+  float* red = reinterpret_cast<float*>(shiftadd_dyn_smem + (kLutSlab));   // ring area, drained
+  for (int base = 0; base < R * T; base += kNT) {
+    const int it = base + tid;
+    if (it < R * T) {
+      const int rl = it % R, part = it / R;
+      const unsigned long long* pp =
+          p.part + ((size_t)(og0 + rl / kTileRows) * p.S) * kTileRows + (rl % kTileRows);
+      float sum = 0.f;
+      for (int s0 = part; s0 < p.S; s0 += 8 * T) {
+        unsigned long long v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          v[k] = s0 + k * T < p.S ? ld_relaxed_u64(pp + (size_t)(s0 + k * T) * kTileRows) : 0ull;
+        unsigned spins = 0;
+        for (;;) {
+          bool stale = false;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) stale |= s0 + k * T < p.S && (unsigned)(v[k] >> 32) != ep;
+          if (!stale) break;
+          if (++spins > (1u << 24)) __trap();   // a non-resident CTA: never hang silently
+          __nanosleep(64);
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (s0 + k * T < p.S && (unsigned)(v[k] >> 32) != ep)
+              v[k] = ld_relaxed_u64(pp + (size_t)(s0 + k * T) * kTileRows);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (s0 + k * T < p.S) sum += __uint_as_float((unsigned)v[k]);
+      }
+      red[it] = sum;
+    }
+  }
+#ifdef SHIFTADD_DEV_TRACE
+  if (tid == 0) trace_at(7);
+#endif
+  __syncthreads();
+  for (int rl = tid; rl < R; rl += kNT) {
+    float sum = red[rl];
+    for (int part = 1; part < T; ++part) sum += red[part * R + rl];
+    const int nf = og0 * kTileRows + rl;
+    const int rgf = nf / kTileRows;
+    int g = 0;
+    while (g + 1 < p.nseg && p.seg[g + 1].rgoff <= rgf) ++g;
+    const int nl = nf - p.seg[g].rgoff * kTileRows;
+    if (nl < p.seg[g].N) p.seg[g].y[nl] = __float2half_rn(sum);
+  }
+  __syncthreads();
+  trace_at(5);
+  // this CTA's share of the call's 2^32 (see the header comment)
+  if (tid == 0) {
+    const unsigned long long add = c == 0 ? (1ull << 32) - (unsigned long long)(G - 1) : 1ull;
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p.done), "l"(add) : "memory");
+  }
+}
+
+}  // namespace
+
+#ifdef SHIFTADD_DEV_TRACE
+int g_dev_variant = 0;
+void dev_set_variant(int v) { g_dev_variant = v; }
+cudaError_t dev_set_trace(void* buf) {
+  unsigned long long* p = static_cast<unsigned long long*>(buf);
+  return cudaMemcpyToSymbol(g_trace, &p, sizeof p);
+}
+#endif
+
+int stream_smem_bytes(int qmax, int nst, int su) {
+  return kLutSlab + nst * su * qmax * (kTileBytes + kTileExps) + kBarBytes;
+}
+
+// Ring depth: as many su-unit stages as fit `budget` bytes of shared memory (<= 16).
+int stream_stages(int qmax, int budget, int su) {
+  const int slot = su * qmax * (kTileBytes + kTileExps);
+  int n = (budget - kLutSlab - kBarBytes) / slot;
+  return n > 16 ? 16 : n;
+}
+
+size_t stream_workspace_bytes(int M, int S, int RGtot) {
+  if (S <= 1) return 0;   // no split-K: the kernel touches no workspace
+  return kStreamWsOff + 256 + (size_t)M * S * RGtot * kTileRows * sizeof(unsigned long long);
+}
+
+bool stream_shape_ok(int K, int sms) {
+  const int S = K / kTileK;
+  return S >= 1 && S <= sms;
+}
+
+cudaError_t launch_lut_stream(const StreamLaunch& L, cudaStream_t stream) {
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(lut_stream_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(lut_stream_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 113 * 1024);
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  if (L.nseg < 1 || L.nseg > kMaxSegments || L.nst < 1 || L.nst > 16 || (L.su != 4 && L.su != 8 && L.su != 16))
+    return cudaErrorInvalidValue;
+  StreamParams p = {};
+  p.x = L.x;
+  p.S = L.K / kTileK;
+  p.nseg = L.nseg;
+  int rg = 0, w = 0, qmax = 1;
+  for (int i = 0; i < L.nseg; ++i) {
+    SegDev& d = p.seg[i];
+    d.planes = L.seg[i].planes;
+    d.exps = L.seg[i].exps;
+    d.y = L.seg[i].y;
+    d.q = L.seg[i].q;
+    d.N = L.seg[i].N;
+    d.RG = (d.N + kTileRows - 1) / kTileRows;
+    d.rgoff = rg;
+    d.woff = w;
+    rg += d.RG;
+    w += d.q * d.RG;
+    qmax = d.q > qmax ? d.q : qmax;
+  }
+  p.RGtot = rg;
+  p.Ws = w;
+  if (p.S > 1) {
+    char* ws = static_cast<char*>(L.workspace) + kStreamWsOff;
+    p.done = reinterpret_cast<unsigned long long*>(ws);
+    p.part = reinterpret_cast<unsigned long long*>(ws + 256);
+  }
+  p.nst = L.nst;
+  p.su = L.su;
+  p.slot = L.su * qmax * (kTileBytes + kTileExps);
+  p.slot_planes = L.su * qmax * kTileBytes;
+  p.pdl = L.pdl;
+  cudaLaunchConfig_t c = {};
+  c.gridDim = dim3(L.grid);
+  c.blockDim = dim3(kNT);
+  c.dynamicSmemBytes = stream_smem_bytes(qmax, L.nst, L.su);
+  c.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  c.attrs = attr;
+  c.numAttrs = L.pdl ? 1 : 0;
+  if (L.half) return cudaLaunchKernelEx(&c, lut_stream_kernel<2>, p);
+  return cudaLaunchKernelEx(&c, lut_stream_kernel<1>, p);
+}
+
+}  // namespace shiftadd

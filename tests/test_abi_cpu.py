@@ -80,10 +80,11 @@ def test_packed_bytes_rejects_bad_shapes(L):
 
 
 def test_workspace_bytes(L):
-    # tiled M=1: S*Npad fp32 partials + RG counters; S == 1 needs none
+    # tiled M=1 (streaming kernel): counter region + epoch word + {epoch, fp32} partials
+    # [RG][S][16]; S == 1 needs none.  M>1 (small-batch kernel): counters + fp32 partials.
     S, RG = 4096 // 256, 4096 // 16
     C = 65536 * 4  # per-row-group counters
-    assert L.shiftadd_workspace_bytes(1, 1, 4096, 4096, 3, 128) == C + S * RG * 16 * 4
+    assert L.shiftadd_workspace_bytes(1, 1, 4096, 4096, 3, 128) == C + 256 + 256 + S * RG * 16 * 8
     assert L.shiftadd_workspace_bytes(1, 1, 4096, 256, 3, 128) == 0
     assert L.shiftadd_workspace_bytes(1, 8, 4096, 4096, 3, 128) == C + 8 * S * RG * 16 * 4
     assert L.shiftadd_workspace_bytes(0, 1, 4096, 4096, 3, 128) == 0

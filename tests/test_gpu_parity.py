@@ -205,18 +205,16 @@ def test_mixed_bit_dispatch_interleaved(sa):
 
 # ------------------------------------------------------------ full-size config parity
 def test_m1_kernel_choice(sa):
-    """Cluster split-K for K <= 4096 (and larger K up to 12 MB of planes, clusters of <= 16)
-    with <= 128 row groups per band; else grid split-K through the TMA ring for >= 64 units
-    per SM and S < #SMs, the register-ring split-K otherwise."""
+    """Batch 1: the cluster kernel (K-split over DSMEM) for K <= 4096 where a band holds <= 128
+    row groups; otherwise the all-SM streaming kernel (id 8) for K <= 256 x #SMs; the
+    register-ring split-K beyond.  Small batch as before."""
     def kid(N, K, M=1, q=1):
         signs, alpha = synth.gen_layer(q, N, K, 128, seed=1, device=DEV)
         return sa.gemm_plan(sa.pack(signs, alpha, 128, layout=sa.LAYOUT_TILED), M)[3]
     assert kid(4096, 4096) == 3 and kid(16384, 4096) == 3 and kid(256, 256) == 3 and kid(768, 768) == 3
-    assert kid(2048, 8192) == 3 and kid(28672, 8192, q=3) == 4   # 70B gate/up: TMA ring
-    assert kid(2048, 8192, q=3) == 3                      # 4-slot clusters where the TMA ring split-K
-    assert kid(4096, 11008, q=1) == 4                     # does not apply; it wins where it does
-    assert kid(4096, 11008, q=3) == 4 and kid(80000, 4096) == 4
-    assert kid(8192, 2048 * 20) == 1                      # S = 160 >= #SMs: register ring
+    assert kid(2048, 8192) == 8 and kid(28672, 8192, q=3) == 8 and kid(8192, 28672, q=3) == 8
+    assert kid(4096, 11008, q=2) == 8 and kid(80000, 4096) == 8
+    assert kid(8192, 2048 * 20) == 1                      # S = 160 > #SMs: register ring
     assert kid(4096, 4096, M=2, q=3) == 5 and kid(4096, 4096, M=2, q=4) == 2   # M = 2 cluster ring: q <= 3
     assert kid(4096, 8192, M=2) == 2 and kid(4096, 4096, M=3) == 6 and kid(4096, 4096, M=4, q=4) == 2
     assert kid(4096, 4096, M=5) == 7 and kid(4096, 4096, M=16, q=4) == 2   # M > 4: row chunks
@@ -366,13 +364,14 @@ def test_gpu_rejects_bad_arguments(sa):
         sa.lut_gemm(x[:1, :256], layer)
 
 
-def test_tma_ring_kernel_exact_invariants(sa):
-    """Kernel 4 (TMA weight ring, chunks straddling two slices): y(-x) = -y(x) bit-exactly,
-    run-to-run bit-identical with and without PDL, counters left zeroed."""
+def test_stream_kernel_exact_invariants(sa):
+    """Kernel 8 (all-SM streaming, chunks straddling two slices, epoch-tagged split-K):
+    y(-x) = -y(x) bit-exactly, run-to-run bit-identical with and without PDL, the older
+    kernels' counter region untouched."""
     q, N, K, g = 3, 4736, 8192, 128
     signs, alpha = synth.gen_layer(q, N, K, g, seed=synth.seed_for(6, 4), device=DEV)
     layer = sa.pack(signs, alpha, g, layout=sa.LAYOUT_TILED)
-    assert sa.gemm_plan(layer, 1)[3] == 4
+    assert sa.gemm_plan(layer, 1)[3] == 8
     ws = sa.Workspace(DEV)
     x = synth.gen_x(1, K, seed=11).to(DEV)
     ys = [sa.lut_gemm(x, layer, workspace=ws, pdl=bool(i & 1)).clone() for i in range(4)]

@@ -1,0 +1,137 @@
+"""GPU parity of the all-SM streaming LUT-GEMV (kernel id 8, csrc/lut_stream.cu) and of the
+fused-projection entry point shiftadd_lut_gemv_fused against the fp64 oracle (bar: reading
+R10, floor-normalised relative error <= 2e-3), plus its epoch protocol: many calls of mixed
+shapes on one workspace, eagerly and replayed from a CUDA graph, stay bit-identical."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-3
+DEV = "cuda:0"
+
+
+@pytest.fixture(scope="module")
+def sa():
+    import paper_2406_05981_b200 as m
+    m.lib()
+    return m
+
+
+def _case(sa, q, N, K, seed, g=128):
+    signs, alpha = synth.gen_layer(q, N, K, g, seed=seed)
+    planes, exps, _ = oracle.pack_canonical(signs.numpy(), alpha.numpy(), g)
+    layer = sa.pack(signs.to(DEV), alpha.to(DEV), g, layout=sa.LAYOUT_TILED)
+    return layer, planes, exps
+
+
+# ragged N (partial last row group, N < 16), one slice (no split-K), chunks straddling slices,
+# every q, K up to the LLaMA-2-7B down_proj
+SHAPES = [(1, 40, 256), (2, 1000, 512), (3, 777, 2304), (4, 100, 4096), (2, 4096, 11008), (3, 17, 8192),
+          (1, 3000, 1024), (4, 2500, 6144)]
+
+
+@pytest.mark.parametrize("q,N,K", SHAPES)
+def test_stream_kernel_parity(sa, q, N, K):
+    layer, planes, exps = _case(sa, q, N, K, synth.seed_for(8, q, N))
+    x = synth.gen_x(1, K, seed=synth.seed_for(8, 1, K))
+    y = sa.lut_gemm(x.to(DEV), layer, splitk=True, pdl=True)
+    torch.cuda.synchronize()
+    assert sa.gemm_plan(layer, 1)[3] in (3, 8)
+    err = oracle.err_floor(y.float().cpu().numpy(), oracle.gemm(x.numpy(), planes, exps, 128))
+    assert err <= TOL, err
+
+
+@pytest.mark.parametrize("segs", [[(2, 4096), (3, 4096), (2, 4096)],       # LLaMA-2-7B q/k/v, k 3-bit
+                                  [(2, 11008), (3, 11008)],                # gate/up, up 3-bit
+                                  [(1, 40), (4, 1000), (2, 17), (3, 513)],  # ragged, every q
+                                  [(3, 2048)]])
+@pytest.mark.parametrize("K", [1024, 4096])
+def test_fused_segments_parity(sa, segs, K):
+    x = synth.gen_x(1, K, seed=synth.seed_for(8, 2, K))
+    cases = [_case(sa, q, N, K, synth.seed_for(8, 30 + i, q)) for i, (q, N) in enumerate(segs)]
+    ys = sa.lut_gemv_fused(x.to(DEV), [c[0] for c in cases], pdl=True)
+    torch.cuda.synchronize()
+    for (layer, planes, exps), y in zip(cases, ys):
+        err = oracle.err_floor(y.float().cpu().numpy()[None, :], oracle.gemm(x.numpy(), planes, exps, 128))
+        assert err <= TOL, (layer.q, layer.N, err)
+
+
+def test_fused_matches_separate_calls_within_rounding(sa):
+    K = 4096
+    x = synth.gen_x(1, K, seed=5).to(DEV)
+    layers = [_case(sa, q, 4096, K, synth.seed_for(8, 4, q))[0] for q in (2, 3, 2)]
+    fused = sa.lut_gemv_fused(x, layers)
+    sep = [sa.lut_gemm(x, L, splitk=True)[0] for L in layers]
+    torch.cuda.synchronize()
+    for a, b in zip(fused, sep):
+        rms = float(b.float().pow(2).mean().sqrt())
+        assert float((a.float() - b.float()).abs().max()) <= 2e-3 * max(rms, float(b.float().abs().max()))
+
+
+def test_epochs_many_calls_one_workspace_and_graph(sa):
+    """The epoch counter advances by one per call of kernel 8, whatever its shape; stale words
+    of earlier calls (other shapes, same workspace region) are never taken.  Eager calls and a
+    CUDA-graph replay of the same sequence give bit-identical outputs."""
+    ws = sa.Workspace(DEV)
+    specs = [(3, 4736, 8192), (2, 1000, 4096), (3, 4096, 11008), (1, 40, 512)]
+    cases = [_case(sa, q, N, K, synth.seed_for(8, 5, i)) for i, (q, N, K) in enumerate(specs)]
+    xs = [synth.gen_x(1, K, seed=synth.seed_for(8, 6, i)).to(DEV) for i, (_, _, K) in enumerate(specs)]
+    outs = [torch.empty((1, N), dtype=torch.float16, device=DEV) for (_, N, _) in specs]
+
+    def seq():
+        for (L, _, _), x, y in zip(cases, xs, outs):
+            sa.lut_gemm(x, L, out=y, workspace=ws, pdl=True, splitk=True)
+
+    s = torch.cuda.Stream(DEV)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        seq()
+    s.synchronize()
+    ref = [y.clone() for y in outs]
+    for (L, planes, exps), x, y in zip(cases, xs, ref):
+        assert oracle.err_floor(y.float().cpu().numpy(), oracle.gemm(x.cpu().numpy(), planes, exps, 128)) <= TOL
+    with torch.cuda.stream(s):
+        for _ in range(10):
+            seq()
+    s.synchronize()
+    for y, r in zip(outs, ref):
+        assert torch.equal(y, r)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for _ in range(3):
+            seq()
+    for y in outs:
+        y.zero_()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        for _ in range(5):
+            g.replay()
+    s.synchronize()
+    for y, r in zip(outs, ref):
+        assert torch.equal(y, r)
+
+
+def test_stream_basis_vector_and_odd_symmetry_exact(sa):
+    """x = e_j gives fp16 of column j of W_hat exactly; y(-x) = -y(x) bit for bit."""
+    q, N, K, g = 3, 600, 4096, 128
+    signs, alpha = synth.gen_layer(q, N, K, g, seed=synth.seed_for(8, 7))
+    planes, exps, _ = oracle.pack_canonical(signs.numpy(), alpha.numpy(), g)
+    layer = sa.pack(signs.to(DEV), alpha.to(DEV), g, layout=sa.LAYOUT_TILED)
+    W = oracle.dequant(planes, exps, g, K)
+    for j in (0, 255, 256, 4095):
+        x = torch.zeros((1, K), dtype=torch.float16)
+        x[0, j] = 1.0
+        y = sa.lut_gemm(x.to(DEV), layer, splitk=True)
+        torch.cuda.synchronize()
+        want = torch.from_numpy(W[:, j]).to(torch.float16)
+        assert torch.equal(y[0].cpu(), want), j
+    x = synth.gen_x(1, K, seed=3).to(DEV)
+    yp = sa.lut_gemm(x, layer, splitk=True)
+    ym = sa.lut_gemm(-x, layer, splitk=True)
+    torch.cuda.synchronize()
+    assert torch.equal(ym.float(), -yp.float())

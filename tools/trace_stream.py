@@ -1,38 +1,68 @@
-"""Per-CTA phase timeline of the TMA-ring split-K kernel (kernel 4; development tool).
-Usage: SHIFTADD_STREAM_TRACE=1 python tools/trace_stream.py N K q [--pdl]"""
-import os
-import sys
-
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np  # noqa: E402
-import torch  # noqa: E402
-
-import paper_2406_05981_b200 as sa  # noqa: E402
-import synth  # noqa: E402
-
-assert os.environ.get("SHIFTADD_STREAM_TRACE") == "1"
-N, K, q = map(int, sys.argv[1:4])
-PDL = "--pdl" in sys.argv
+"""Per-CTA phase trace of the streaming kernel (id 8) in a chain of back-to-back calls
+(development tool; needs tools/dev_build.sh).  Prints min/avg/max of each phase (us) relative
+to the first CTA start of the last call.  Usage: python tools/trace_stream.py N:K:q ..."""
+import ctypes, os, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch
+import paper_2406_05981_b200 as sa
+import synth
+sa._LIB_PATH = os.path.join(ROOT, "paper_2406_05981_b200", "libshiftadd_dev.so")
+L = sa.lib()
+L.shiftadd_dev_set_trace.argtypes = [ctypes.c_void_p]
+L.shiftadd_dev_set_variant.argtypes = [ctypes.c_int]
+variant = int(os.environ.get("VARIANT", "0"))
+L.shiftadd_dev_set_variant(variant)
 dev = torch.device("cuda:0")
-signs, alpha = synth.gen_layer(q, N, K, 128, seed=1, device=dev)
-layers = [sa.pack(signs, alpha, 128, layout=sa.LAYOUT_TILED)]
-del signs, alpha
-for r in range(3):
-    layers.append(sa.PackedLayer(layers[0].planes.clone(), layers[0].exps.clone(), q, N, K, 128, 1, layers[0].counts))
-x = synth.gen_x(1, K, seed=2, device=dev)
-ws = sa.Workspace(dev)
-S, RG = K // 256, (N + 15) // 16
-need = 65536 * 4 + S * RG * 16 * 4
-ws.buf = torch.zeros(need + 148 * 128 + 4096, dtype=torch.uint8, device=dev)
-for i in range(8):
-    sa.lut_gemm(x, layers[i % 4], workspace=ws, pdl=PDL)
-torch.cuda.synchronize()
-G, _, _, kid = sa.gemm_plan(layers[0], 1)
-assert kid == 4, kid
-tr = ws.buf[need:need + G * 128].cpu().numpy().view(np.uint64).reshape(G, 16).astype(np.int64)
-t0 = tr[:, 0].min()
-print("N=%d K=%d q=%d G=%d pdl=%d  (us from first CTA start)" % (N, K, q, G, PDL))
-for nm, c in [("start", 0), ("pdl_wait", 1), ("luts_built", 2), ("stage0_full", 3), ("loop_end", 4),
-              ("arrived", 5), ("counters_ok", 6), ("end", 7)]:
-    v = (tr[:, c] - t0) / 1000.0
-    print("  %-12s min %7.2f  med %7.2f  max %7.2f" % (nm, v.min(), np.median(v), v.max()))
+l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+names = ["start", "wait", "lut", "stage0", "loop0", "owner", "loopall", "t0data"]
+for spec in sys.argv[1:]:
+    N, K, q = map(int, spec.split(":"))
+    lb = q * N * K // 8
+    R = max(2, -(-4 * l2 // lb))
+    signs, alpha = synth.gen_layer(q, N, K, 128, seed=1, device=dev)
+    base = sa.pack(signs, alpha, 128, layout=sa.LAYOUT_TILED)
+    copies = [base] + [sa.PackedLayer(base.planes.clone(), base.exps.clone(), q, N, K, 128, base.layout, base.counts)
+                       for _ in range(R - 1)]
+    x = synth.gen_x(1, K, seed=1, device=dev)
+    y = torch.empty((1, N), dtype=torch.float16, device=dev)
+    ws = sa.Workspace(dev)
+    tr = torch.zeros(148 * 16, dtype=torch.int64, device=dev)
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream(dev)
+    with torch.cuda.stream(s):
+        for t in range(3):
+            sa.lut_gemm(x, copies[t % R], out=y, workspace=ws, pdl=True)
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for t in range(2 * R):
+            sa.lut_gemm(x, copies[t % R], out=y, workspace=ws, pdl=True)
+    with torch.cuda.stream(s):
+        g.replay()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        g.replay()
+        e1.record(s)
+    s.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / (2 * R)
+    L.shiftadd_dev_set_trace(ctypes.c_void_p(tr.data_ptr()))
+    with torch.cuda.stream(s):
+        g.replay()
+    s.synchronize()
+    L.shiftadd_dev_set_trace(None)
+    t = tr.view(148, 16)[:, :8].cpu().double()
+    t0 = t[:, 0].min()
+    rel = (t - t0) / 1e3
+    out = []
+    for k, nm in enumerate(names):
+        col = rel[:, k]
+        col = col[t[:, k] > 0]
+        if len(col):
+            out.append("%s %.2f/%.2f/%.2f" % (nm, col.min(), col.mean(), col.max()))
+    print("v%d N=%d K=%d q=%d %.2f us/call: %s" % (variant, N, K, q, us, "  ".join(out)), flush=True)
+    cyc = tr.view(148, 16)[:, 8:15].cpu().double()
+    print("   cycles (warp 0): unit1 wait %.0f dot %.0f emit %.0f; loop after LUT %.0f; owner: t0 data %.0f first-stale %.0f spins %.1f (avg)" %
+          tuple(cyc.mean(0).tolist()), flush=True)
+    print("   max: t0 data %.0f spins %.0f" % (cyc[:, 4].max(), cyc[:, 6].max()), flush=True)
