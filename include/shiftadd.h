@@ -72,6 +72,11 @@ typedef enum { SHIFTADD_LAYOUT_CANONICAL = 0, SHIFTADD_LAYOUT_TILED = 1 } shifta
                                    over distributed shared memory).  For testing and
                                    measurement; results agree within rounding order. */
 
+#define SHIFTADD_FLAG_CLUSTER 4u /* tiled layout: use the thread-block-cluster kernels (K-split
+                                    reduced over distributed shared memory; ids 3, 5, 6, 7) where
+                                    they apply, instead of the all-SM streaming kernel.  For
+                                    testing and measurement; results agree within rounding order. */
+
 int shiftadd_abi_version(void);
 const char* shiftadd_status_string(int status);
 const char* shiftadd_last_error(void);

@@ -30,6 +30,7 @@ LAYOUT_CANONICAL = 0
 LAYOUT_TILED = 1
 FLAG_PDL = 1
 FLAG_SPLITK = 2
+FLAG_CLUSTER = 4
 EXP_ZERO = -128
 _ABI_VERSION = 1
 _LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libshiftadd.so")
@@ -324,11 +325,11 @@ def _workspace_for(device, stream=None):
 
 def lut_gemm(x: torch.Tensor, layer: PackedLayer, out: torch.Tensor | None = None,
              workspace: Workspace | None = None, pdl: bool = False, stream=None,
-             splitk: bool = False) -> torch.Tensor:
+             splitk: bool = False, cluster: bool = False) -> torch.Tensor:
     """§8 a2-a7: y[M][N] = x[M][K] (.) the packed layer, fp16 in/out (shiftadd_lut_gemm).
 
-    splitk forces the grid-wide split-K decompositions (SHIFTADD_FLAG_SPLITK), for testing and
-    measurement."""
+    splitk / cluster force the all-SM streaming kernel / the thread-block-cluster kernels
+    (SHIFTADD_FLAG_SPLITK / SHIFTADD_FLAG_CLUSTER), for testing and measurement."""
     squeeze = x.dim() == 1
     x2 = x.unsqueeze(0) if squeeze else x
     if x2.dtype != torch.float16 or not x2.is_cuda or x2.device != layer.device:
@@ -370,7 +371,8 @@ def lut_gemm(x: torch.Tensor, layer: PackedLayer, out: torch.Tensor | None = Non
                                  layer.layout, M, layer.N, layer.K, layer.q, layer.g, out.data_ptr(),
                                  out.stride(0), ws.data_ptr() if ws is not None else None,
                                  ws.numel() if ws is not None else 0,
-                                 (FLAG_PDL if pdl else 0) | (FLAG_SPLITK if splitk else 0), sptr)
+                                 (FLAG_PDL if pdl else 0) | (FLAG_SPLITK if splitk else 0)
+                                 | (FLAG_CLUSTER if cluster else 0), sptr)
     if st:
         _check(st, "shiftadd_lut_gemm")
     return out[0] if squeeze else out

@@ -81,26 +81,41 @@ constexpr int kStreamSmemBudget = 200 * 1024;
 
 size_t tiled_rows(int N) { return (size_t)((N + kTileRows - 1) / kTileRows); }
 
+int mw_of(int M) { return M == 1 ? 1 : M == 2 ? 2 : M <= 4 ? 4 : 8; }
+
+// Streaming kernel (id 8) geometry for a launch of Mc <= 8 rows (or the first chunk of M).
+LaunchPlan plan_stream(int M, int q, int K, int sms) {
+  const int MW = mw_of(M > 8 ? 8 : M);
+  const int S = K / kTileK;
+  const int grid = MW == 8 ? S * (sms / S) : sms;   // MW = 8: one slice per CTA
+  const int nst = stream_stages(q, kStreamSmemBudget, 16, MW);
+  return LaunchPlan{grid, 17 * 32, stream_smem_bytes(q, nst, 16, MW), 8};
+}
+
 LaunchPlan make_plan(int layout, int M, int N, int K, int q, int g, int sms, unsigned flags) {
   if (layout == SHIFTADD_LAYOUT_CANONICAL) return plan_generic(M, N, K, q, g, sms);
+  const bool force_stream = flags & SHIFTADD_FLAG_SPLITK, force_cluster = flags & SHIFTADD_FLAG_CLUSTER;
   if (M == 1) {
     // K <= 4096: the cluster kernel (K-split reduced over DSMEM, measured faster at these
     // sizes); larger K (and SHIFTADD_FLAG_SPLITK): the all-SM streaming kernel (id 8), whose
     // split-K goes through the workspace.  The register-ring / TMA-ring split-K kernels (ids
     // 1, 4) remain for K > 256 x #SMs.
-    if (!(flags & SHIFTADD_FLAG_SPLITK) && K <= 4096 && cluster_applicable(N, K, q, sms))
+    if (!force_stream && (K <= 4096 || force_cluster) && cluster_applicable(N, K, q, sms))
       return plan_gemv_cluster(N, K, q, sms);
-    if (stream_shape_ok(K, sms)) {
-      const int nst = stream_stages(q, kStreamSmemBudget, 16);
-      return LaunchPlan{sms, 17 * 32, stream_smem_bytes(q, nst, 16), 8};
-    }
+    if (stream_shape_ok(K, sms)) return plan_stream(1, q, K, sms);
     if (stream_applicable(N, K, q, sms)) return plan_gemv_stream(N, K, q, sms);
     return plan_gemv_tiled(N, K, q, sms);
   }
-  if (M == 2 && !(flags & SHIFTADD_FLAG_SPLITK) && m2_applicable(N, K, q, sms)) return plan_gemm_m2(N, K, q, sms);
-  if ((M == 3 || M == 4) && !(flags & SHIFTADD_FLAG_SPLITK) && m4_applicable(N, K, q, sms))
-    return plan_gemm_m4(N, K, q, sms);
-  if (M > 4 && !(flags & SHIFTADD_FLAG_SPLITK) && m2_applicable(N, K, q, sms) && m4_applicable(N, K, q, sms)) {
+  // a7 small batch.  M = 2..4 with K <= 4096: the cluster rings (float2 / float4 fp32 entries,
+  // DSMEM reduction; measured faster there).  Otherwise the streaming kernel with M-wide fp16
+  // LUT entries: one pass over the weights for up to 8 rows (two for 9..16).
+  const bool small_m = M <= 4 && K <= 4096 && !force_stream;
+  if (small_m && M == 2 && m2_applicable(N, K, q, sms)) return plan_gemm_m2(N, K, q, sms);
+  if (small_m && M >= 3 && m4_applicable(N, K, q, sms)) return plan_gemm_m4(N, K, q, sms);
+  if (!force_cluster && stream_shape_ok(K, sms)) return plan_stream(M, q, K, sms);
+  if (M == 2 && m2_applicable(N, K, q, sms)) return plan_gemm_m2(N, K, q, sms);
+  if ((M == 3 || M == 4) && m4_applicable(N, K, q, sms)) return plan_gemm_m4(N, K, q, sms);
+  if (M > 4 && m2_applicable(N, K, q, sms) && m4_applicable(N, K, q, sms)) {
     LaunchPlan p = plan_gemm_m4(N, K, q, sms);   // row chunks of 2..4 through kernels 5/6
     p.kernel = 7;
     return p;
@@ -110,12 +125,10 @@ LaunchPlan make_plan(int layout, int M, int N, int K, int q, int g, int sms, uns
 
 size_t workspace_for(int layout, int M, int N, int K) {
   if (layout == SHIFTADD_LAYOUT_CANONICAL) return 0;
-  if (M == 1) {
-    const size_t a = workspace_gemv_tiled(N, K);
-    const size_t b = stream_workspace_bytes(1, K / kTileK, (N + kTileRows - 1) / kTileRows);
-    return a > b ? a : b;
-  }
-  return workspace_gemm_tiled_mb(M, N, K);
+  const int S = K / kTileK, RG = (N + kTileRows - 1) / kTileRows;
+  const size_t b = stream_workspace_bytes(M > 8 ? 8 : M, S, RG);   // row chunks of 8 reuse it in order
+  const size_t a = M == 1 ? workspace_gemv_tiled(N, K) : workspace_gemm_tiled_mb(M, N, K);
+  return a > b ? a : b;
 }
 
 }  // namespace
@@ -405,7 +418,8 @@ shiftadd_status shiftadd_lut_gemm(const uint16_t* x, int ldx, const uint8_t* pla
   if (M < 1) return fail(SHIFTADD_ERR_INVALID, "M=%d < 1", M);
   if (M > 16) return fail(SHIFTADD_ERR_UNSUPPORTED, "M=%d > 16 (small-batch kernels cover M <= 16)", M);
   if (ldx < K || ldy < N) return fail(SHIFTADD_ERR_INVALID, "ldx=%d < K=%d or ldy=%d < N=%d", ldx, K, ldy, N);
-  if (flags & ~(SHIFTADD_FLAG_PDL | SHIFTADD_FLAG_SPLITK)) return fail(SHIFTADD_ERR_INVALID, "unknown flags 0x%x", flags);
+  if (flags & ~(SHIFTADD_FLAG_PDL | SHIFTADD_FLAG_SPLITK | SHIFTADD_FLAG_CLUSTER))
+    return fail(SHIFTADD_ERR_INVALID, "unknown flags 0x%x", flags);
   if (!aligned(x, 16) || (M > 1 && (ldx % 8)) || !aligned(planes, 16) || !aligned(y, 2))
     return fail(SHIFTADD_ERR_INVALID, "misaligned pointer (x rows and planes need 16 B)");
   const size_t need = workspace_for(layout, M, N, K);
@@ -432,29 +446,39 @@ shiftadd_status shiftadd_lut_gemm(const uint16_t* x, int ldx, const uint8_t* pla
   a.stream = reinterpret_cast<cudaStream_t>(stream);
   LaunchPlan p = make_plan(layout, M, N, K, q, g, di.sms, flags);
   // the TMA ring copies exponent tiles with 16-B bulk copies
-  if ((p.kernel == 4 || p.kernel == 8) && !aligned(exps, 16)) p = plan_gemv_tiled(N, K, q, di.sms);
+  if ((p.kernel == 4 || p.kernel == 8) && !aligned(exps, 16))
+    p = M == 1 ? plan_gemv_tiled(N, K, q, di.sms) : plan_gemm_tiled_mb(M, N, K, q, di.sms);
   if ((p.kernel >= 5 && p.kernel <= 7) && !aligned(exps, 16)) p = plan_gemm_tiled_mb(M, N, K, q, di.sms);
   cudaError_t e;
   if (layout == SHIFTADD_LAYOUT_CANONICAL) e = launch_gemm_generic(a, p);
   else if (p.kernel == 8) {
-    StreamLaunch L = {};
-    L.x = a.x;
-    L.K = K;
-    L.nseg = 1;
-    L.seg[0] = StreamSeg{planes, exps, a.y, q, N};
-    L.workspace = workspace;
-    L.grid = p.grid;
-    L.su = 16;
-    L.nst = stream_stages(q, kStreamSmemBudget, L.su);
-    L.pdl = (flags & SHIFTADD_FLAG_PDL) ? 1 : 0;
+    // row chunks of <= 8 (one launch for M <= 8), stream-ordered on the same workspace
+    e = cudaSuccess;
+    for (int m0 = 0; m0 < M && e == cudaSuccess; m0 += 8) {
+      const int mc = M - m0 < 8 ? M - m0 : 8;
+      StreamLaunch L = {};
+      L.x = a.x + (size_t)m0 * ldx;
+      L.M = mc;
+      L.ldx = ldx;
+      L.ldy = ldy;
+      L.K = K;
+      L.nseg = 1;
+      L.seg[0] = StreamSeg{planes, exps, a.y + (size_t)m0 * ldy, q, N};
+      L.workspace = workspace;
+      const LaunchPlan pc = plan_stream(mc, q, K, di.sms);
+      L.grid = pc.grid;
+      L.su = 16;
+      L.nst = stream_stages(q, kStreamSmemBudget, L.su, mw_of(mc));
+      L.pdl = (flags & SHIFTADD_FLAG_PDL) ? 1 : 0;
 #ifdef SHIFTADD_DEV_TRACE
-    if (g_dev_variant & 1) {
-      L.half = 1;
-      L.nst = stream_stages(q, 112 * 1024, L.su);
-      if (L.nst < 2) L.half = 0, L.nst = stream_stages(q, kStreamSmemBudget, L.su);
-    }
+      if ((g_dev_variant & 1) && mc == 1) {
+        L.half = 1;
+        L.su = 8;
+        L.nst = stream_stages(q, 112 * 1024, L.su, 1);
+      }
 #endif
-    e = launch_lut_stream(L, a.stream);
+      e = launch_lut_stream(L, a.stream);
+    }
   }
   else if (p.kernel == 3) e = launch_gemv_cluster(a, p);
   else if (p.kernel == 5) e = launch_gemm_m2(a, p);
@@ -521,6 +545,8 @@ shiftadd_status shiftadd_lut_gemv_fused(const uint16_t* x, int K, int g, int lay
     return fail(SHIFTADD_ERR_INVALID, "workspace needs %zu bytes, 16-B aligned (got %zu)", need, workspace_bytes);
   StreamLaunch L = {};
   L.x = reinterpret_cast<const __half*>(x);
+  L.M = 1;
+  L.ldx = K;
   L.K = K;
   L.nseg = nseg;
   int qmax = 1;
@@ -531,8 +557,15 @@ shiftadd_status shiftadd_lut_gemv_fused(const uint16_t* x, int K, int g, int lay
   L.workspace = workspace;
   L.grid = di.sms;
   L.su = 16;
-  L.nst = stream_stages(qmax, kStreamSmemBudget, L.su);
+  L.nst = stream_stages(qmax, kStreamSmemBudget, L.su, 1);
   L.pdl = (flags & SHIFTADD_FLAG_PDL) ? 1 : 0;
+#ifdef SHIFTADD_DEV_TRACE
+  if (g_dev_variant & 1) {
+    L.half = 1;
+    L.su = 8;
+    L.nst = stream_stages(qmax, 112 * 1024, L.su, 1);
+  }
+#endif
   const cudaError_t e = launch_lut_stream(L, reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "lut_gemv_fused launch");
   return SHIFTADD_OK;

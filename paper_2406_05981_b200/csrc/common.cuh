@@ -213,6 +213,7 @@ struct StreamSeg {
 };
 struct StreamLaunch {
   const __half* x;
+  int M, ldx, ldy;   // M <= 8 rows per launch (M = 1: ldx, ldy unused)
   int K;
   int nseg;
   StreamSeg seg[kMaxSegments];
@@ -270,8 +271,9 @@ cudaError_t launch_gather_wait(const uint32_t* flags, int P, uint32_t* epoch, cu
 LaunchPlan plan_gemv_cluster(int N, int K, int q, int sms);
 cudaError_t launch_gemv_cluster(const GemmArgs& a, const LaunchPlan& p);
 
-int stream_smem_bytes(int qmax, int nst, int su);
-int stream_stages(int qmax, int budget, int su);
+int stream_lut_bytes(int MW);
+int stream_smem_bytes(int qmax, int nst, int su, int MW);
+int stream_stages(int qmax, int budget, int su, int MW);
 size_t stream_workspace_bytes(int M, int S, int RGtot);
 bool stream_shape_ok(int K, int sms);
 cudaError_t launch_lut_stream(const StreamLaunch& L, cudaStream_t stream);

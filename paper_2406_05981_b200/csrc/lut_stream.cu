@@ -39,8 +39,7 @@
 namespace shiftadd {
 namespace {
 
-constexpr int kNWC = 16;                     // consumer warps
-constexpr int kNT = (kNWC + 1) * 32;         // + one producer warp
+constexpr int kNWCMax = 16;                  // consumer warps (16, or 8 in the co-resident variant)
 constexpr int kLutSlab = kLutBytes;          // 64 KB: two slices' LUTs (column halves)
 constexpr int kBarBytes = 512;               // full[16] at +0, empty[16] at +128, epoch at +256
 
@@ -71,14 +70,18 @@ struct SegDev {
 
 struct StreamParams {
   const __half* x;
+  int M, ldx, ldy;          // batch rows (<= 8 per launch), row strides of x and of every y
+  int one_slice;            // 1: G = S x cps CTAs, CTA c covers 1/cps of slice c / cps (MW = 8)
+  int lut_bytes;            // LUT region at kDynBase (64 KB or 128 KB); the ring follows
   int S, nseg, RGtot, Ws;   // Ws = sum over segments of q * RG (weight of one slice)
   SegDev seg[kMaxSegments];
   unsigned long long* done;   // epoch counter (workspace)
-  unsigned long long* part;   // {epoch, fp32} [S][RGtot * 16]
+  unsigned long long* part;   // {epoch, fp32} [M][RGtot][S][16]
   int nst, slot, slot_planes;
   int su;    // units per stage (16, 8 or 4); consumer warp w serves stages t with
              // t % (16 / su) == w / su, unit w % su
   int pdl;
+  int skew;   // offset the two warp halves' stage pairs (see consume_run)
 };
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
@@ -122,6 +125,7 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
 // kDynBase, from the 8 activations of group `lane` (xv).  T[key] = (A[lo&3] + B[lo>>2]) +
 // (C[hi&3] + D[hi>>2]): key bit b <-> +x_b if set, -x_b if clear;
 // warp w writes the keys with hi nibble w, 32 consecutive words per store (conflict-free).
+template <int NWC>
 __device__ __forceinline__ void build_lut(const uint4 xv, uint32_t hoff, int warp, int lane) {
   const float2 f01 = __half22float2(*reinterpret_cast<const __half2*>(&xv.x));
   const float2 f23 = __half22float2(*reinterpret_cast<const __half2*>(&xv.y));
@@ -129,12 +133,15 @@ __device__ __forceinline__ void build_lut(const uint4 xv, uint32_t hoff, int war
   const float2 f67 = __half22float2(*reinterpret_cast<const __half2*>(&xv.w));
   const float A[4] = {-f01.x - f01.y, f01.x - f01.y, f01.y - f01.x, f01.x + f01.y};
   const float B[4] = {-f23.x - f23.y, f23.x - f23.y, f23.y - f23.x, f23.x + f23.y};
-  const int hi = warp;
-  const float H = ((hi & 1 ? f45.x : -f45.x) + (hi & 2 ? f45.y : -f45.y)) +
-                  ((hi & 4 ? f67.x : -f67.x) + (hi & 8 ? f67.y : -f67.y));
   const uint32_t col = kDynBase + hoff + 4 * lane;
 #pragma unroll
-  for (int lo = 0; lo < 16; ++lo) sts_f32(col + ((hi * 16 + lo) << 8), (A[lo & 3] + B[lo >> 2]) + H);
+  for (int hh = 0; hh < 16 / NWC; ++hh) {
+    const int hi = warp + hh * NWC;
+    const float H = ((hi & 1 ? f45.x : -f45.x) + (hi & 2 ? f45.y : -f45.y)) +
+                    ((hi & 4 ? f67.x : -f67.x) + (hi & 8 ? f67.y : -f67.y));
+#pragma unroll
+    for (int lo = 0; lo < 16; ++lo) sts_f32(col + ((hi * 16 + lo) << 8), (A[lo & 3] + B[lo >> 2]) + H);
+  }
 }
 
 // PRMT selector for step j: byte0 <- column byte (j&3) of cst[j>>2], byte1 <- key byte (j&3)
@@ -273,15 +280,21 @@ __device__ __forceinline__ void unit_dot2(uint32_t sp0, uint32_t se0, uint32_t s
 template <int Q, uint32_t HOFF>
 __device__ __forceinline__ void consume_run(const StreamParams& p, const SegDev& sg, int s, int rga, int re,
                                             RingPos& rp, int& t, uint32_t ring, uint32_t full, uint32_t empty,
-                                            const uint32_t (&cst)[4], int wu, int lane, unsigned long long ep) {
+                                            const uint32_t (&cst)[4], int wu, int lane, unsigned long long ep,
+                                            bool skew) {
   const int r = lane >> 1, h = lane & 1;
   // partial words [flat row group][slice][16 rows]: a unit's 16 sums are one 128-B line, and an
   // owner's (row group, all slices) block is S contiguous lines
   unsigned long long* prow = p.part + ((size_t)sg.rgoff * p.S + s) * kTileRows + r;
-  for (int rg = rga; rg < re; rg += 2 * p.su) {
+  // Warps of the upper half take the run's first stage alone and then pairs: the two halves'
+  // pairs are offset by one stage, so one half's barrier waits and stores overlap the other
+  // half's lookups instead of the whole CTA stalling in lockstep.
+  bool single = skew;
+  for (int rg = rga; rg < re;) {
     const int n0 = re - rg < p.su ? re - rg : p.su;
     const int left = re - rg - n0;
-    const int n1 = left < p.su ? left : p.su;   // may be <= 0: no second stage in this run
+    const int n1 = single ? 0 : (left < p.su ? left : p.su);   // may be <= 0: no second stage
+    single = false;
     const RingPos r0 = rp;
     rp.next(p.nst);
     const RingPos r1 = rp;
@@ -322,33 +335,231 @@ __device__ __forceinline__ void consume_run(const StreamParams& p, const SegDev&
       }
     }
     if (rg == rga) trace_clk(10, c0);
+    rg += n0 + (n1 > 0 ? n1 : 0);
   }
 }
 
 template <uint32_t HOFF>
 __device__ __forceinline__ void consume_run_q(const StreamParams& p, const SegDev& sg, int s, int rga, int re,
                                               RingPos& rp, int& t, uint32_t ring, uint32_t full, uint32_t empty,
-                                              const uint32_t (&cst)[4], int wu, int lane, unsigned long long ep) {
+                                              const uint32_t (&cst)[4], int wu, int lane, unsigned long long ep,
+                                              bool skew) {
   switch (sg.q) {
-    case 1: consume_run<1, HOFF>(p, sg, s, rga, re, rp, t, ring, full, empty, cst, wu, lane, ep); break;
-    case 2: consume_run<2, HOFF>(p, sg, s, rga, re, rp, t, ring, full, empty, cst, wu, lane, ep); break;
-    case 3: consume_run<3, HOFF>(p, sg, s, rga, re, rp, t, ring, full, empty, cst, wu, lane, ep); break;
-    default: consume_run<4, HOFF>(p, sg, s, rga, re, rp, t, ring, full, empty, cst, wu, lane, ep); break;
+    case 1: consume_run<1, HOFF>(p, sg, s, rga, re, rp, t, ring, full, empty, cst, wu, lane, ep, skew); break;
+    case 2: consume_run<2, HOFF>(p, sg, s, rga, re, rp, t, ring, full, empty, cst, wu, lane, ep, skew); break;
+    case 3: consume_run<3, HOFF>(p, sg, s, rga, re, rp, t, ring, full, empty, cst, wu, lane, ep, skew); break;
+    default: consume_run<4, HOFF>(p, sg, s, rga, re, rp, t, ring, full, empty, cst, wu, lane, ep, skew); break;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// a7 small batch (App. D): M-wide LUT entries, one weight pass for M rows.
+// A LUT entry holds MW fp16 partial sums -- rows 0..MW-1 of x against the same 8-k group and
+// key -- built in fp32 and rounded once (the paper's FP16 LUT; reading R8/C10),
+// so one LDS.{32,64,128} per key byte serves MW rows, and each half is accumulated into fp32
+// by one FHADD (fp32 + fp16 -> fp32, the .H0/.H1 half selected in the instruction).
+//   MW = 2: 4-B entries, the M = 1 slab layout (two slices in the column halves; 64 KB)
+//   MW = 4: 8-B entries, slice t at +64K t, group g at 8-B slot 16(g>>4) + ((g&15) ^ 8(g>>4))
+//   MW = 8: 16-B entries, one slice, groups 16h..16h+15 at +64K h, slot (g&15) ^ 4h
+// The slots make every LDS phase (32/16/8 lanes) hit distinct banks for any keys.
+template <int MW>
+__host__ __device__ constexpr uint32_t mw_col(int g) {   // byte offset of group g in a key row
+  return MW == 2 ? 4u * (uint32_t)g
+                 : MW == 4 ? 8u * (uint32_t)(16 * (g >> 4) + ((g & 15) ^ (8 * (g >> 4))))
+                           : 16u * (uint32_t)((g & 15) ^ (4 * (g >> 4)));
+}
+template <int MW>
+__host__ __device__ constexpr uint32_t mw_hi(int g) {   // 64 KB block of group g (MW = 8)
+  return MW == 8 ? (uint32_t)(g >> 4) : 0u;
+}
+// LUT base of slice t (0 or 1) of the CTA
+template <int MW>
+__host__ __device__ constexpr uint32_t mw_slice_base(int t) {
+  return kDynBase + (MW == 2 ? 128u * t : MW == 4 ? 65536u * t : 0u);
+}
+
+__device__ __forceinline__ uint32_t pack_h2(float a, float b) {
+  const __half2 v = __floats2half2_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+// a2 for MW rows: lane = group g; warp w writes keys with hi nibble w (+ NWC ...).
+template <int NWC, int MW>
+__device__ __forceinline__ void build_lut_mw(const StreamParams& p, int s, int t, int warp, int lane) {
+  float sa[MW], da[MW], sb[MW], db[MW], x4[MW], x5[MW], x6[MW], x7[MW];
+  const uint64_t pol_keep = policy_evict_last();
+#pragma unroll
+  for (int m = 0; m < MW; ++m) {
+    uint4 xv = make_uint4(0, 0, 0, 0);
+    if (m < p.M) xv = ldg_keep(p.x + (size_t)m * p.ldx + (size_t)s * kTileK + 8 * lane, pol_keep);
+    const float2 f01 = __half22float2(*reinterpret_cast<const __half2*>(&xv.x));
+    const float2 f23 = __half22float2(*reinterpret_cast<const __half2*>(&xv.y));
+    const float2 f45 = __half22float2(*reinterpret_cast<const __half2*>(&xv.z));
+    const float2 f67 = __half22float2(*reinterpret_cast<const __half2*>(&xv.w));
+    sa[m] = f01.x + f01.y; da[m] = f01.x - f01.y;
+    sb[m] = f23.x + f23.y; db[m] = f23.x - f23.y;
+    x4[m] = f45.x; x5[m] = f45.y; x6[m] = f67.x; x7[m] = f67.y;
+  }
+  const uint32_t row0 = mw_slice_base<MW>(t) + 65536u * mw_hi<MW>(lane) + mw_col<MW>(lane);
+#pragma unroll
+  for (int hh = 0; hh < 16 / NWC; ++hh) {
+    const int hi = warp + hh * NWC;
+    float H[MW];
+#pragma unroll
+    for (int m = 0; m < MW; ++m)
+      H[m] = ((hi & 1 ? x4[m] : -x4[m]) + (hi & 2 ? x5[m] : -x5[m])) + ((hi & 4 ? x6[m] : -x6[m]) + (hi & 8 ? x7[m] : -x7[m]));
+#pragma unroll
+    for (int lo = 0; lo < 16; ++lo) {
+      // A[lo&3] = {-s, d, -d, s}(x0, x1), B[lo>>2] likewise from (x2, x3): key bit b -> +-x_b
+      float e[MW];
+#pragma unroll
+      for (int m = 0; m < MW; ++m) {
+        const int a = lo & 3, b = lo >> 2;
+        const float A = a == 0 ? -sa[m] : a == 1 ? da[m] : a == 2 ? -da[m] : sa[m];
+        const float B = b == 0 ? -sb[m] : b == 1 ? db[m] : b == 2 ? -db[m] : sb[m];
+        e[m] = (A + B) + H[m];
+      }
+      const uint32_t addr = row0 + ((uint32_t)(hi * 16 + lo) << 8);
+      if (MW == 2) {
+        asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(pack_h2(e[0], e[1])) : "memory");
+      } else if (MW == 4) {
+        asm volatile("st.shared.v2.b32 [%0], {%1,%2};" ::"r"(addr), "r"(pack_h2(e[0], e[1])),
+                     "r"(pack_h2(e[2 % MW], e[3 % MW])) : "memory");
+      } else {
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(pack_h2(e[0], e[1])),
+                     "r"(pack_h2(e[2 % MW], e[3 % MW])), "r"(pack_h2(e[4 % MW], e[5 % MW])),
+                     "r"(pack_h2(e[6 % MW], e[7 % MW])) : "memory");
+      }
+    }
+  }
+}
+
+// Lookup address of step j: byte 0 = column byte (cst byte j&1), byte 1 = key byte (word byte
+// j&3), byte 2 = 64 KB block (cst byte 2), byte 3 = 0.
+__host__ __device__ constexpr uint32_t step_sel_mw(int j) {
+  return (7u << 12) | (6u << 8) | ((uint32_t)(j & 3) << 4) | (4u + (j & 1));
+}
+
+__device__ __forceinline__ void fhadd_lo(float& acc, uint32_t v) {
+  asm("{.reg .f16 l, h; mov.b32 {l, h}, %1; add.rn.f32.f16 %0, l, %0;}" : "+f"(acc) : "r"(v));
+}
+__device__ __forceinline__ void fhadd_hi(float& acc, uint32_t v) {
+  asm("{.reg .f16 l, h; mov.b32 {l, h}, %1; add.rn.f32.f16 %0, h, %0;}" : "+f"(acc) : "r"(v));
+}
+
+// a3 + a4 for one unit, MW rows: per plane 16 lookups (2 chains of MW fp32 sums), scaled by
+// 2^e into acc[MW].
+template <int Q, uint32_t BASE, int MW>
+__device__ __forceinline__ void unit_dot_mw(uint32_t sp, uint32_t se, const uint32_t (&cst)[8], float (&acc)[MW]) {
+  uint4 w[Q];
+  int e[Q];
+#pragma unroll
+  for (int i = 0; i < Q; ++i) w[i] = lds_u4(sp + i * kTileBytes);
+#pragma unroll
+  for (int i = 0; i < Q; ++i) e[i] = lds_s8(se + i * kTileExps);
+#pragma unroll
+  for (int m = 0; m < MW; ++m) acc[m] = 0.f;
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    float c[2][MW];
+#pragma unroll
+    for (int m = 0; m < MW; ++m) c[0][m] = c[1][m] = 0.f;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const uint32_t word = (j < 4) ? w[i].x : (j < 8) ? w[i].y : (j < 12) ? w[i].z : w[i].w;
+      const uint32_t a = BASE + prmt(word, cst[j >> 1], step_sel_mw(j));
+      uint32_t v[4];
+      if (MW == 2) {
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v[0]) : "r"(a));
+      } else if (MW == 4) {
+        asm volatile("ld.shared.v2.b32 {%0,%1}, [%2];" : "=r"(v[0]), "=r"(v[1]) : "r"(a));
+      } else {
+        asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                     : "r"(a));
+      }
+#pragma unroll
+      for (int m = 0; m < MW; m += 2) {
+        fhadd_lo(c[j & 1][m], v[m >> 1]);
+        fhadd_hi(c[j & 1][m + 1], v[m >> 1]);
+      }
+    }
+    const float sc = pow2_bits(e[i]);
+#pragma unroll
+    for (int m = 0; m < MW; ++m) acc[m] = __fmaf_rn(c[0][m] + c[1][m], sc, acc[m]);
+  }
+}
+
+// Consumer side of one run for MW rows: one unit per warp per stage.
+template <int Q, uint32_t BASE, int MW>
+__device__ __forceinline__ void consume_run_mw(const StreamParams& p, const SegDev& sg, int s, int rga, int re,
+                                               RingPos& rp, uint32_t ring, uint32_t full, uint32_t empty,
+                                               const uint32_t (&cst)[8], int wu, int lane, unsigned long long ep) {
+  const int r = lane >> 1, h = lane & 1;
+  for (int rg = rga; rg < re; rg += p.su, rp.next(p.nst)) {
+    const int n = re - rg < p.su ? re - rg : p.su;
+    const uint32_t slot = ring + (uint32_t)(rp.j * p.slot);
+    mbar_wait(full + 8 * rp.j, (uint32_t)(rp.k & 1));
+    if (wu < n) {
+      float acc[MW];
+      unit_dot_mw<Q, BASE, MW>(slot + (uint32_t)(wu * Q * kTileBytes + 16 * lane),
+                               slot + (uint32_t)(p.slot_planes + wu * Q * kTileExps + lane), cst, acc);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + 8 * rp.j);
+#pragma unroll
+      for (int m = 0; m < MW; ++m) acc[m] += __shfl_xor_sync(0xffffffffu, acc[m], 1);
+      if (h == 0) {
+        const int u = rg + wu;
+#pragma unroll
+        for (int m = 0; m < MW; ++m) {
+          if (m < p.M) {
+            if (p.S == 1) {
+              const int nl = u * kTileRows + r;
+              if (nl < sg.N) sg.y[(size_t)m * p.ldy + nl] = __float2half_rn(acc[m]);
+            } else {
+              const size_t w = ((((size_t)m * p.RGtot + sg.rgoff + u) * p.S) + s) * kTileRows + r;
+              st_relaxed_u64(p.part + w, ep | __float_as_uint(acc[m]));
+            }
+          }
+        }
+      }
+    } else {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + 8 * rp.j);
+    }
+  }
+}
+
+template <uint32_t BASE, int MW>
+__device__ __forceinline__ void consume_run_mw_q(const StreamParams& p, const SegDev& sg, int s, int rga, int re,
+                                                 RingPos& rp, uint32_t ring, uint32_t full, uint32_t empty,
+                                                 const uint32_t (&cst)[8], int wu, int lane, unsigned long long ep) {
+  switch (sg.q) {
+    case 1: consume_run_mw<1, BASE, MW>(p, sg, s, rga, re, rp, ring, full, empty, cst, wu, lane, ep); break;
+    case 2: consume_run_mw<2, BASE, MW>(p, sg, s, rga, re, rp, ring, full, empty, cst, wu, lane, ep); break;
+    case 3: consume_run_mw<3, BASE, MW>(p, sg, s, rga, re, rp, ring, full, empty, cst, wu, lane, ep); break;
+    default: consume_run_mw<4, BASE, MW>(p, sg, s, rga, re, rp, ring, full, empty, cst, wu, lane, ep); break;
   }
 }
 
 // MINB = 2: registers capped so that two CTAs fit one SM -- with <= 113 KB of shared memory
 // the next call's CTA becomes resident (and streams its weights) while this one finishes.
-template <int MINB>
-__global__ void __launch_bounds__(kNT, MINB) lut_stream_kernel(const __grid_constant__ StreamParams p) {
+template <int NWC, int MINB, int MW>
+__global__ void __launch_bounds__((NWC + 1) * 32, MINB) lut_stream_kernel(const __grid_constant__ StreamParams p) {
+  constexpr int kNT = (NWC + 1) * 32;
   if (threadIdx.x == 0) check_dyn_base();
   trace_at(0);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (p.pdl) pdl_launch_dependents();
   const long long G = gridDim.x, W = (long long)p.S * p.Ws, c = blockIdx.x;
-  const Pos start = pos_at(p, c * W / G);
-  const Pos end = pos_at(p, (c + 1) * W / G);
-  const uint32_t ring = kDynBase + kLutSlab;
+  long long wlo = c * W / G, whi = (c + 1) * W / G;
+  if (p.one_slice) {   // G = S x cps: CTA c covers part c % cps of slice c / cps
+    const long long cps = G / p.S, sl = c / cps, sub = c % cps;
+    wlo = sl * p.Ws + sub * p.Ws / cps;
+    whi = sl * p.Ws + (sub + 1) * p.Ws / cps;
+  }
+  const Pos start = pos_at(p, wlo);
+  const Pos end = pos_at(p, whi);
+  const uint32_t ring = kDynBase + (uint32_t)p.lut_bytes;
   const uint32_t bars = ring + (uint32_t)(p.nst * p.slot);
   const uint32_t full = bars, empty = bars + 128;
   const uint32_t s_epoch = bars + 256;   // this call's epoch (shared, written once)
@@ -362,7 +573,7 @@ __global__ void __launch_bounds__(kNT, MINB) lut_stream_kernel(const __grid_cons
   }
   __syncthreads();
 
-  if (warp == kNWC) {
+  if (warp == NWC) {
     // producer: one thread streams the CTA's runs into the ring, su units per stage
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
@@ -393,20 +604,25 @@ __global__ void __launch_bounds__(kNT, MINB) lut_stream_kernel(const __grid_cons
     const bool any = before(start, end);
     const bool two = end.s > s0 && !(end.s == s0 + 1 && end.g == 0 && end.rg == 0);
     if (any) {
-      const uint64_t pol_keep = policy_evict_last();
-      const uint4 xa = ldg_keep(p.x + (size_t)s0 * kTileK + 8 * lane, pol_keep);
-      uint4 xb = xa;
-      if (two) xb = ldg_keep(p.x + (size_t)(s0 + 1) * kTileK + 8 * lane, pol_keep);
       if (tid == 32 && p.S > 1)   // a lane whose x does not gate warp 0
         asm volatile("st.shared.u32 [%0], %1;" ::"r"(s_epoch), "r"((unsigned)(ld_relaxed_u64(p.done) >> 32) + 1u)
                      : "memory");
-      build_lut(xa, 0u, warp, lane);
-      if (two) build_lut(xb, 128u, warp, lane);
+      if (MW == 1) {
+        const uint64_t pol_keep = policy_evict_last();
+        const uint4 xa = ldg_keep(p.x + (size_t)s0 * kTileK + 8 * lane, pol_keep);
+        uint4 xb = xa;
+        if (two) xb = ldg_keep(p.x + (size_t)(s0 + 1) * kTileK + 8 * lane, pol_keep);
+        build_lut<NWC>(xa, 0u, warp, lane);
+        if (two) build_lut<NWC>(xb, 128u, warp, lane);
+      } else {
+        build_lut_mw<NWC, MW>(p, s0, 0, warp, lane);
+        if (two && MW < 8) build_lut_mw<NWC, MW>(p, s0 + 1, 1, warp, lane);
+      }
     } else if (tid == 32 && p.S > 1) {
       asm volatile("st.shared.u32 [%0], %1;" ::"r"(s_epoch), "r"((unsigned)(ld_relaxed_u64(p.done) >> 32) + 1u)
                    : "memory");
     }
-    asm volatile("bar.sync 1, %0;" ::"r"(kNWC * 32) : "memory");   // consumer warps only
+    asm volatile("bar.sync 1, %0;" ::"r"(NWC * 32) : "memory");   // consumer warps only
     trace_at(2);
 #ifdef SHIFTADD_DEV_TRACE
     const long long c2 = clock64();
@@ -415,24 +631,45 @@ __global__ void __launch_bounds__(kNT, MINB) lut_stream_kernel(const __grid_cons
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(ep32) : "r"(s_epoch) : "memory");
     const unsigned long long ep = (unsigned long long)ep32 << 32;
     const int r = lane >> 1, h = lane & 1;
-    uint32_t cst[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      uint32_t v = 0;
-#pragma unroll
-      for (int b = 0; b < 4; ++b) v |= (4u * (uint32_t)(16 * h + ((4 * k + b + r) & 15))) << (8 * b);
-      cst[k] = v;
-    }
     const int wu = warp;
     RingPos rp{0, 0};
-    int t = 0;
-    for (Pos a = start; before(a, end);) {
-      const int re = run_end(p, a, end);
-      if (a.s == s0)
-        consume_run_q<0u>(p, p.seg[a.g], a.s, a.rg, re, rp, t, ring, full, empty, cst, wu, lane, ep);
-      else
-        consume_run_q<128u>(p, p.seg[a.g], a.s, a.rg, re, rp, t, ring, full, empty, cst, wu, lane, ep);
-      next_run(p, a, re);
+    if (MW == 1) {
+      uint32_t cst[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        uint32_t v = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) v |= (4u * (uint32_t)(16 * h + ((4 * k + b + r) & 15))) << (8 * b);
+        cst[k] = v;
+      }
+      const bool skew = p.skew && warp >= NWC / 2;
+      int t = 0;
+      for (Pos a = start; before(a, end);) {
+        const int re = run_end(p, a, end);
+        if (a.s == s0)
+          consume_run_q<0u>(p, p.seg[a.g], a.s, a.rg, re, rp, t, ring, full, empty, cst, wu, lane, ep, skew);
+        else
+          consume_run_q<128u>(p, p.seg[a.g], a.s, a.rg, re, rp, t, ring, full, empty, cst, wu, lane, ep, skew);
+        next_run(p, a, re);
+      }
+    } else {
+      // column bytes of the 16 steps (2 per constant) and the 64 KB block of the lane's groups
+      uint32_t cst[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int g0 = 16 * h + ((2 * k + r) & 15), g1 = 16 * h + ((2 * k + 1 + r) & 15);
+        cst[k] = mw_col<MW>(g0) | (mw_col<MW>(g1) << 8) | (mw_hi<MW>(g0) << 16);
+      }
+      for (Pos a = start; before(a, end);) {
+        const int re = run_end(p, a, end);
+        if (a.s == s0)
+          consume_run_mw_q<mw_slice_base<MW>(0), MW>(p, p.seg[a.g], a.s, a.rg, re, rp, ring, full, empty, cst, wu,
+                                                      lane, ep);
+        else
+          consume_run_mw_q<mw_slice_base<MW>(1), MW>(p, p.seg[a.g], a.s, a.rg, re, rp, ring, full, empty, cst, wu,
+                                                      lane, ep);
+        next_run(p, a, re);
+      }
     }
 #ifdef SHIFTADD_DEV_TRACE
     trace_clk(11, c2);
@@ -449,19 +686,21 @@ __global__ void __launch_bounds__(kNT, MINB) lut_stream_kernel(const __grid_cons
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(ep) : "r"(s_epoch) : "memory");
   const int og0 = (int)(c * p.RGtot / G), og1 = (int)((c + 1) * p.RGtot / G);
   const int R = (og1 - og0) * kTileRows;
-  // T threads per row; thread it takes row it % R (consecutive lanes: consecutive rows of one
-  // 128-B line) and slices it / R, it / R + T, ... in order, loading <= 16 words at once and
+  const int MR = p.M * R;   // (batch row m, output row) pairs owned
+  // T threads per row; thread it takes row it % MR (consecutive lanes: consecutive rows of one
+  // 128-B line) and slices it / MR, it / MR + T, ... in order, loading <= 8 words at once and
   // re-polling only the stale ones.  The T partial sums of a row then meet in shared memory
   // (the drained ring) and are added in part order: deterministic for a launch shape.
-  int T = R > 0 ? kNT / R : 1;
+  int T = MR > 0 ? kNT / MR : 1;
   T = T < 1 ? 1 : (T > p.S ? p.S : T);
-  float* red = reinterpret_cast<float*>(shiftadd_dyn_smem + (kLutSlab));   // ring area, drained
-  for (int base = 0; base < R * T; base += kNT) {
+  float* red = reinterpret_cast<float*>(shiftadd_dyn_smem + p.lut_bytes);   // ring area, drained
+  for (int base = 0; base < MR * T; base += kNT) {
     const int it = base + tid;
-    if (it < R * T) {
-      const int rl = it % R, part = it / R;
+    if (it < MR * T) {
+      const int rl = it % MR, part = it / MR;
+      const int m = rl / R, row = rl % R;
       const unsigned long long* pp =
-          p.part + ((size_t)(og0 + rl / kTileRows) * p.S) * kTileRows + (rl % kTileRows);
+          p.part + (((size_t)m * p.RGtot + og0 + row / kTileRows) * p.S) * kTileRows + (row % kTileRows);
       float sum = 0.f;
       for (int s0 = part; s0 < p.S; s0 += 8 * T) {
         unsigned long long v[8];
@@ -492,15 +731,16 @@ __global__ void __launch_bounds__(kNT, MINB) lut_stream_kernel(const __grid_cons
   if (tid == 0) trace_at(7);
 #endif
   __syncthreads();
-  for (int rl = tid; rl < R; rl += kNT) {
+  for (int rl = tid; rl < MR; rl += kNT) {
     float sum = red[rl];
-    for (int part = 1; part < T; ++part) sum += red[part * R + rl];
-    const int nf = og0 * kTileRows + rl;
+    for (int part = 1; part < T; ++part) sum += red[part * MR + rl];
+    const int m = rl / R, row = rl % R;
+    const int nf = og0 * kTileRows + row;
     const int rgf = nf / kTileRows;
     int g = 0;
     while (g + 1 < p.nseg && p.seg[g + 1].rgoff <= rgf) ++g;
     const int nl = nf - p.seg[g].rgoff * kTileRows;
-    if (nl < p.seg[g].N) p.seg[g].y[nl] = __float2half_rn(sum);
+    if (nl < p.seg[g].N) p.seg[g].y[(size_t)m * p.ldy + nl] = __float2half_rn(sum);
   }
   __syncthreads();
   trace_at(5);
@@ -522,14 +762,18 @@ cudaError_t dev_set_trace(void* buf) {
 }
 #endif
 
-int stream_smem_bytes(int qmax, int nst, int su) {
-  return kLutSlab + nst * su * qmax * (kTileBytes + kTileExps) + kBarBytes;
+// LUT bytes for entries of MW rows (MW = 1: fp32 entries, two slices; 2, 4: fp16, two
+// slices; 8: fp16, one slice)
+int stream_lut_bytes(int MW) { return MW <= 2 ? kLutSlab : 2 * kLutSlab; }
+
+int stream_smem_bytes(int qmax, int nst, int su, int MW) {
+  return stream_lut_bytes(MW) + nst * su * qmax * (kTileBytes + kTileExps) + kBarBytes;
 }
 
 // Ring depth: as many su-unit stages as fit `budget` bytes of shared memory (<= 16).
-int stream_stages(int qmax, int budget, int su) {
+int stream_stages(int qmax, int budget, int su, int MW) {
   const int slot = su * qmax * (kTileBytes + kTileExps);
-  int n = (budget - kLutSlab - kBarBytes) / slot;
+  int n = (budget - stream_lut_bytes(MW) - kBarBytes) / slot;
   return n > 16 ? 16 : n;
 }
 
@@ -547,16 +791,27 @@ cudaError_t launch_lut_stream(const StreamLaunch& L, cudaStream_t stream) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(lut_stream_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (attr_err == cudaSuccess)
-      attr_err = cudaFuncSetAttribute(lut_stream_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 113 * 1024);
+    const int big = 227 * 1024;
+    cudaError_t e = cudaFuncSetAttribute(lut_stream_kernel<16, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(lut_stream_kernel<16, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(lut_stream_kernel<16, 1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(lut_stream_kernel<16, 1, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(lut_stream_kernel<8, 2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 113 * 1024);
+    attr_err = e;
   });
-  if (attr_err != cudaSuccess) return attr_err;
-  if (L.nseg < 1 || L.nseg > kMaxSegments || L.nst < 1 || L.nst > 16 || (L.su != 4 && L.su != 8 && L.su != 16))
+  if (L.nseg < 1 || L.nseg > kMaxSegments || L.nst < 1 || L.nst > 16 || L.su != (L.half ? 8 : 16))
     return cudaErrorInvalidValue;
   StreamParams p = {};
   p.x = L.x;
+  p.M = L.M < 1 ? 1 : L.M;
+  p.ldx = L.ldx;
+  p.ldy = L.ldy;
   p.S = L.K / kTileK;
+  const int MW = p.M == 1 ? 1 : p.M == 2 ? 2 : p.M <= 4 ? 4 : 8;
+  if (p.M > 8) return cudaErrorInvalidValue;
+  p.one_slice = MW == 8 ? 1 : 0;
+  p.lut_bytes = stream_lut_bytes(MW);
   p.nseg = L.nseg;
   int rg = 0, w = 0, qmax = 1;
   for (int i = 0; i < L.nseg; ++i) {
@@ -585,18 +840,27 @@ cudaError_t launch_lut_stream(const StreamLaunch& L, cudaStream_t stream) {
   p.slot = L.su * qmax * (kTileBytes + kTileExps);
   p.slot_planes = L.su * qmax * kTileBytes;
   p.pdl = L.pdl;
+  p.skew = 1;
+#ifdef SHIFTADD_DEV_TRACE
+  if (g_dev_variant & 2) p.skew = 0;
+#endif
   cudaLaunchConfig_t c = {};
   c.gridDim = dim3(L.grid);
-  c.blockDim = dim3(kNT);
-  c.dynamicSmemBytes = stream_smem_bytes(qmax, L.nst, L.su);
+  c.blockDim = dim3(L.half ? 9 * 32 : 17 * 32);
+  c.dynamicSmemBytes = stream_smem_bytes(qmax, L.nst, L.su, MW);
   c.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   c.attrs = attr;
   c.numAttrs = L.pdl ? 1 : 0;
-  if (L.half) return cudaLaunchKernelEx(&c, lut_stream_kernel<2>, p);
-  return cudaLaunchKernelEx(&c, lut_stream_kernel<1>, p);
+  if (L.half && MW == 1) return cudaLaunchKernelEx(&c, lut_stream_kernel<8, 2, 1>, p);
+  switch (MW) {
+    case 1: return cudaLaunchKernelEx(&c, lut_stream_kernel<16, 1, 1>, p);
+    case 2: return cudaLaunchKernelEx(&c, lut_stream_kernel<16, 1, 2>, p);
+    case 4: return cudaLaunchKernelEx(&c, lut_stream_kernel<16, 1, 4>, p);
+    default: return cudaLaunchKernelEx(&c, lut_stream_kernel<16, 1, 8>, p);
+  }
 }
 
 }  // namespace shiftadd

@@ -215,9 +215,11 @@ def test_m1_kernel_choice(sa):
     assert kid(2048, 8192) == 8 and kid(28672, 8192, q=3) == 8 and kid(8192, 28672, q=3) == 8
     assert kid(4096, 11008, q=2) == 8 and kid(80000, 4096) == 8
     assert kid(8192, 2048 * 20) == 1                      # S = 160 > #SMs: register ring
-    assert kid(4096, 4096, M=2, q=3) == 5 and kid(4096, 4096, M=2, q=4) == 2   # M = 2 cluster ring: q <= 3
-    assert kid(4096, 8192, M=2) == 2 and kid(4096, 4096, M=3) == 6 and kid(4096, 4096, M=4, q=4) == 2
-    assert kid(4096, 4096, M=5) == 7 and kid(4096, 4096, M=16, q=4) == 2   # M > 4: row chunks
+    # small batch: cluster rings for M = 2..4 at K <= 4096 (M = 2 ring: q <= 3); the streaming
+    # kernel with M-wide fp16 LUT entries elsewhere (one weight pass per 8 rows)
+    assert kid(4096, 4096, M=2, q=3) == 5 and kid(4096, 4096, M=2, q=4) == 8
+    assert kid(4096, 8192, M=2) == 8 and kid(4096, 4096, M=3) == 6 and kid(4096, 4096, M=4, q=4) == 8
+    assert kid(4096, 4096, M=5) == 8 and kid(4096, 4096, M=16, q=4) == 8 and kid(4096, 11008, M=8) == 8
 
 
 @pytest.mark.parametrize("splitk", [False, True])
@@ -405,9 +407,10 @@ def test_misaligned_exponents_use_register_ring(sa, q, N, K):
         assert oracle.err_floor(y.float().cpu().numpy(), y_ref) <= TOL
 
 
-@pytest.mark.parametrize("M,kid", [(2, 5), (3, 6), (4, 6), (7, 7)])
+@pytest.mark.parametrize("M,kid", [(2, 5), (3, 6), (4, 6), (7, 8)])
 def test_small_batch_ring_exact_invariants(sa, M, kid):
-    """The small-batch cluster-ring kernels (float2 / float4 entries, row chunks): row m of x
+    """The small-batch kernels (cluster rings with float2 / float4 entries; M = 7: the streaming
+    kernel with 8-wide fp16 entries): row m of x
     set to the basis vector e_{j_m} gives the fp16-rounded column j_m exactly, and
     y(-x) = -y(x) bit-exactly."""
     layer, planes, exps, (q, N, K, g) = _exact_layer(sa, 1, q=3, N=80, K=1024)

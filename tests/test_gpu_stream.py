@@ -135,3 +135,72 @@ def test_stream_basis_vector_and_odd_symmetry_exact(sa):
     ym = sa.lut_gemm(-x, layer, splitk=True)
     torch.cuda.synchronize()
     assert torch.equal(ym.float(), -yp.float())
+
+
+# ----------------------------------------------------------------------------- a7 small batch
+def _sampled(sa, q, N, K, M, seed, nrows=96, **kw):
+    """Device result at a full shape vs the oracle on a row sample (canonical bytes of just
+    those rows), floor with the rms of the full device output per batch row."""
+    g = 128
+    signs, alpha = synth.gen_layer(q, N, K, g, seed=seed, device=DEV)
+    layer = sa.pack(signs, alpha, g, layout=sa.LAYOUT_TILED)
+    x = synth.gen_x(M, K, seed=seed + 1)
+    y = sa.lut_gemm(x.to(DEV), layer, pdl=True, **kw)
+    torch.cuda.synchronize()
+    y = y.float().cpu().numpy()
+    rows = np.random.default_rng(seed).choice(N, min(nrows, N), replace=False)
+    rows = np.unique(np.concatenate([rows, [0, N - 1]]))
+    planes, exps, _ = oracle.pack_canonical(signs[:, rows].cpu().numpy(), alpha[:, rows].cpu().numpy(), g)
+    y_ref = oracle.gemm(x.numpy(), planes, exps, g)
+    rms = np.sqrt(np.mean(y.astype(np.float64) ** 2, axis=1, keepdims=True))
+    den = np.maximum(np.abs(y_ref), rms)
+    return float(np.max(np.abs(y[:, rows] - y_ref) / den)), sa.gemm_plan(layer, M)[3]
+
+
+@pytest.mark.parametrize("M", [5, 8, 16])
+@pytest.mark.parametrize("q,N,K", [(2, 4096, 11008), (3, 11008, 4096), (4, 4096, 4096)])
+def test_small_batch_single_pass_full_shapes(sa, M, q, N, K):
+    """LLaMA-2-7B down_proj / up_proj shapes and a 4-bit layer at M = 5, 8, 16 through the
+    streaming kernel's M-wide fp16 LUT entries (one weight pass per 8 rows)."""
+    err, kid = _sampled(sa, q, N, K, M, synth.seed_for(8, 40 + M, q))
+    assert kid == 8
+    assert err <= TOL, err
+
+
+@pytest.mark.parametrize("M", [2, 3, 4, 6, 7])
+@pytest.mark.parametrize("q,N,K", [(2, 4096, 4096), (3, 1000, 2304), (1, 40, 256)])
+def test_small_batch_stream_kernel_parity(sa, M, q, N, K):
+    """Every entry width (MW = 2, 4, 8) of the streaming kernel, forced, incl. M not a power of 2."""
+    signs, alpha = synth.gen_layer(q, N, K, 128, seed=synth.seed_for(8, 50 + M, q))
+    planes, exps, _ = oracle.pack_canonical(signs.numpy(), alpha.numpy(), 128)
+    layer = sa.pack(signs.to(DEV), alpha.to(DEV), 128, layout=sa.LAYOUT_TILED)
+    x = synth.gen_x(M, K, seed=synth.seed_for(8, 60 + M))
+    y = sa.lut_gemm(x.to(DEV), layer, splitk=True)
+    y2 = sa.lut_gemm(x.to(DEV), layer, splitk=True, pdl=True)
+    torch.cuda.synchronize()
+    assert torch.equal(y, y2)
+    err = oracle.err_floor(y.float().cpu().numpy(), oracle.gemm(x.numpy(), planes, exps, 128))
+    assert err <= TOL, err
+
+
+def test_small_batch_mw8_exact_invariants(sa):
+    """M = 8 entries: x = e_j in every row gives fp16 of column j exactly (one nonzero group,
+    LUT entries exact in fp16 for +-1 sums), and y(-x) = -y(x) bit for bit."""
+    q, N, K, g = 2, 300, 2048, 128
+    signs, alpha = synth.gen_layer(q, N, K, g, seed=synth.seed_for(8, 70))
+    planes, exps, _ = oracle.pack_canonical(signs.numpy(), alpha.numpy(), g)
+    layer = sa.pack(signs.to(DEV), alpha.to(DEV), g, layout=sa.LAYOUT_TILED)
+    W = oracle.dequant(planes, exps, g, K)
+    js = [0, 7, 1000, 2047, 512, 255, 256, 1]
+    x = torch.zeros((8, K), dtype=torch.float16)
+    for m, j in enumerate(js):
+        x[m, j] = 1.0
+    y = sa.lut_gemm(x.to(DEV), layer, splitk=True)
+    torch.cuda.synchronize()
+    for m, j in enumerate(js):
+        assert torch.equal(y[m].cpu(), torch.from_numpy(W[:, j]).to(torch.float16)), (m, j)
+    xr = synth.gen_x(8, K, seed=4).to(DEV)
+    yp = sa.lut_gemm(xr, layer, splitk=True)
+    ym = sa.lut_gemm(-xr, layer, splitk=True)
+    torch.cuda.synchronize()
+    assert torch.equal(ym.float(), -yp.float())

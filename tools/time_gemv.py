@@ -15,6 +15,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("shapes", nargs="+")
 ap.add_argument("--pdl", action="store_true")
 ap.add_argument("--splitk", action="store_true")
+ap.add_argument("--cluster", action="store_true", help="thread-block-cluster kernels (FLAG_CLUSTER)")
 ap.add_argument("--colwise", action="store_true", help="NEXT-f1 column-wise scales (M = 1)")
 ap.add_argument("--apot2", action="store_true", help="NEXT-f2 additive PoT, K = 2 terms")
 ap.add_argument("--m", type=int, default=1)
@@ -57,7 +58,7 @@ for spec in a.shapes:
         if a.colwise:
             sa.lut_gemv_colwise(x, L, out=y.view(-1), pdl=a.pdl)
         else:
-            sa.lut_gemm(x, L, out=y, workspace=ws, pdl=a.pdl, splitk=a.splitk)
+            sa.lut_gemm(x, L, out=y, workspace=ws, pdl=a.pdl, splitk=a.splitk, cluster=a.cluster)
 
     with torch.cuda.stream(s):
         for t in range(3):
