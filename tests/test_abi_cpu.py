@@ -86,7 +86,10 @@ def test_workspace_bytes(L):
     C = 65536 * 4  # per-row-group counters
     assert L.shiftadd_workspace_bytes(1, 1, 4096, 4096, 3, 128) == C + 256 + 256 + S * RG * 16 * 8
     assert L.shiftadd_workspace_bytes(1, 1, 4096, 256, 3, 128) == 0
-    assert L.shiftadd_workspace_bytes(1, 8, 4096, 4096, 3, 128) == C + 8 * S * RG * 16 * 4
+    assert L.shiftadd_workspace_bytes(1, 8, 4096, 4096, 3, 128) == C + 512 + 8 * S * RG * 16 * 8
+    # M = 16: the larger of the streaming kernel (two row chunks of 8 reuse one region) and the
+    # small-batch split-K kernel (fp32 partials for all 16 rows)
+    assert L.shiftadd_workspace_bytes(1, 16, 4096, 4096, 3, 128) == max(C + 512 + 8 * S * RG * 16 * 8, C + 16 * S * RG * 16 * 4)
     assert L.shiftadd_workspace_bytes(0, 1, 4096, 4096, 3, 128) == 0
     assert L.shiftadd_workspace_bytes(1, 17, 4096, 4096, 3, 128) == 0
 
