@@ -46,7 +46,8 @@ __all__ = [
     "algorithmic_bytes", "tile_planes", "pack_colwise", "dequant_colwise", "gemm_colwise",
     "lut_gemm_colwise", "algorithmic_bytes_colwise", "additive_pot", "pack_apot2",
     "dequant_apot2", "gemm_apot2", "pot_round_exact", "bcq_greedy", "bcq_ls", "bcq_bs_codes",
-    "bcq_quantize",
+    "bcq_quantize", "pack_blockwise", "dequant_blockwise", "gemm_blockwise", "lut_gemm_blockwise",
+    "blockwise_row_exps", "algorithmic_bytes_blockwise",
 ]
 
 
@@ -411,6 +412,110 @@ def lut_gemm_colwise(x, planes, exps_col):
             bank = np.stack([lut_direct(xi[8 * t:8 * t + 8]) for t in range(kb)])   # [K/8][256]
             y[m] += bank[t_idx, p[i].astype(np.int64)].sum(axis=1)
     return y
+
+
+# ------------------------------------------------ NEXT-f1: block-wise scales, "Ours (Lat.)"
+# PAPER.md:239-244 (§4.2, Fig. 4(a)): "a block-wise scaling factor design that groups 8
+# columns and 1/8 of the original rows to share a scaling factor, ensuring compatibility with
+# the BCQ kernel".  In the OPTQ orientation of that section rows are outputs and columns are
+# inputs, so (reading R24) plane i has one PoT scale per (row block
+# b = n // (N/8), column group c = k // 8): the 8 weights of a key byte share it.
+def _block_rows(N):
+    if N % 8:
+        raise ValueError("block-wise scales need 8 | N (1/8 of the rows per block)")
+    return N // 8
+
+
+def pack_blockwise(signs, alpha_bw):
+    """signs int8 [q][N][K] (+-1), alpha_bw float32 [q][8][K/8] -> planes, exps_bw, n_clamped.
+
+      1. sign fold per block (R3): alpha_i[b][c] < 0 negates s_i[n][k] for the rows n of
+         block b and the 8 columns k of group c, and keeps |alpha_i[b][c]|;
+      2. exponent: P = round(log2|alpha|) (pot_exponent: same zero / clamp rules);
+      3. bits exactly as pack_canonical step 3 (R1, R2).
+    Returns planes uint8 [q][N][K/8], exps_bw int8 [q][8][K/8], n_clamped.
+    """
+    s = np.asarray(signs)
+    a = np.asarray(alpha_bw, dtype=np.float32)
+    if s.ndim != 3:
+        raise ValueError("signs must be [q][N][K]")
+    q, n, k = s.shape
+    nb = _block_rows(n)
+    if k % 8:
+        raise ValueError("need 8 | K")
+    if a.shape != (q, 8, k // 8):
+        raise ValueError("alpha_bw must be [q][8][K/8]")
+    if not np.all((s == 1) | (s == -1)):
+        raise ValueError("signs must be -1 or +1")
+    exps, n_clamped = pot_exponent(a)
+    flip = np.repeat(np.repeat(a < 0, nb, axis=1), 8, axis=2)   # [q][N][K]
+    folded = np.where(flip, -s.astype(np.int16), s.astype(np.int16))
+    bits = (folded == 1).astype(np.uint8).reshape(q, n, k // 8, 8)
+    weights = (1 << np.arange(8, dtype=np.uint16)).astype(np.uint16)
+    planes = (bits.astype(np.uint16) * weights).sum(axis=3).astype(np.uint8)
+    return planes, exps, n_clamped
+
+
+def dequant_blockwise(planes, exps_bw, K):
+    """W_hat[n][k] = sum_i 2^{e_i[n // (N/8)][k // 8]} s_i[n][k], fp64."""
+    p = np.asarray(planes, dtype=np.uint8)
+    q, n, _ = p.shape
+    nb = _block_rows(n)
+    s = unpack_signs(p, K).astype(np.float64)                              # [q][N][K]
+    scale = np.repeat(np.repeat(_pow2(exps_bw), nb, axis=1), 8, axis=2)    # [q][N][K]
+    return (s * scale).sum(axis=0)
+
+
+def gemm_blockwise(x, planes, exps_bw, row_chunk=2048):
+    """y = x W_hat^T in fp64 with block-wise scales (the plain definition)."""
+    xf = np.atleast_2d(np.asarray(x, dtype=np.float64))
+    p = np.asarray(planes, dtype=np.uint8)
+    q, n, kb = p.shape
+    K = kb * 8
+    nb = _block_rows(n)
+    e = np.asarray(exps_bw)
+    if xf.shape[1] != K or e.shape != (q, 8, kb):
+        raise ValueError("x must be [M][K] and exps_bw [q][8][K/8]")
+    y = np.empty((xf.shape[0], n), dtype=np.float64)
+    rows = np.arange(n) // nb
+    for n0 in range(0, n, row_chunk):
+        n1 = min(n, n0 + row_chunk)
+        s = unpack_signs(p[:, n0:n1], K).astype(np.float64)
+        scale = np.repeat(_pow2(e)[:, rows[n0:n1], :], 8, axis=2)
+        y[:, n0:n1] = xf @ (s * scale).sum(axis=0).T
+    return y
+
+
+def lut_gemm_blockwise(x, planes, exps_bw):
+    """The LUT route with block-wise scales, step by step, fp64: one LUT per 8 activations
+    (lut_direct), the key byte of plane i selects T_t[key], and since the
+    8 weights of the key share one scale, that query is shifted by 2^{e_i[b][t]}
+    before it is added."""
+    xf = np.atleast_2d(np.asarray(x, dtype=np.float64))
+    p = np.asarray(planes, dtype=np.uint8)
+    q, n, kb = p.shape
+    nb = _block_rows(n)
+    sc = _pow2(exps_bw)                                       # [q][8][K/8]
+    y = np.zeros((xf.shape[0], n), dtype=np.float64)
+    t_idx = np.arange(kb)[None, :]
+    rows = np.arange(n) // nb
+    for m in range(xf.shape[0]):
+        bank = np.stack([lut_direct(xf[m, 8 * t:8 * t + 8]) for t in range(kb)])   # [K/8][256]
+        for i in range(q):
+            queried = bank[t_idx, p[i].astype(np.int64)]                            # [N][K/8]
+            y[m] += (queried * sc[i][rows]).sum(axis=1)
+    return y
+
+
+def blockwise_row_exps(exps_bw, N):
+    """The block-wise exponents replicated into the row-wise layout with g = 8: [q][N][K/8]
+    (SURVEY C6's "block-wise = g = 8 with exponents replicated over N/8-row blocks")."""
+    return np.repeat(np.asarray(exps_bw), _block_rows(N), axis=1)
+
+
+def algorithmic_bytes_blockwise(M, q, N, K):
+    """HBM bytes of one block-wise GEMV call: planes + int8 exps [q][8][K/8] + fp16 x + y."""
+    return q * N * K // 8 + q * K + 2 * M * K + 2 * M * N
 
 
 def algorithmic_bytes_colwise(M, q, N, K):

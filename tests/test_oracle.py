@@ -635,3 +635,80 @@ def test_s11_t0_is_greedy_and_pot_projection_matches_pot_exponent():
     e, _ = oracle.pot_exponent(vals)
     for v, ei in zip(vals, e):
         assert oracle.pot_round_exact(float(v)) == math.copysign(2.0 ** int(ei), float(v))
+
+
+# --------------------------------------- S12: block-wise scales ("Ours (Lat.)", NEXT-f1)
+def test_s12_blockwise_exact_pot_scales_reproduce_bcq_sum():
+    """alpha_i[b][c] = +-2^P exactly: dequant_blockwise(pack_blockwise(s, alpha)) equals
+    sum_i alpha_i[n // (N/8)][k // 8] s_i[n][k] element by element, written out as a scalar
+    loop with exact rationals.  Pins the block geometry (8 columns x N/8 rows),
+    the per-block sign fold and the bit order (a row-wise or column-wise fold fails)."""
+    rng = _rng(120)
+    q, N, K = 2, 16, 32
+    s = rng.choice([-1, 1], size=(q, N, K)).astype(np.int8)
+    P = rng.integers(-5, 6, size=(q, 8, K // 8))
+    sign = rng.choice([-1.0, 1.0], size=(q, 8, K // 8))
+    alpha = (sign * np.ldexp(1.0, P)).astype(np.float32)
+    planes, exps, ncl = oracle.pack_blockwise(s, alpha)
+    assert ncl == 0 and exps.shape == (q, 8, K // 8) and np.array_equal(exps, P.astype(np.int8))
+    W = oracle.dequant_blockwise(planes, exps, K)
+    for n in range(N):
+        for k in range(K):
+            want = sum(_frac(alpha[i, n // (N // 8), k // 8]) * int(s[i, n, k]) for i in range(q))
+            assert _frac(W[n, k]) == want, (n, k)
+
+
+def test_s12_blockwise_brute_force_gemv_exact():
+    """Every sign pattern of one 8-weight key per plane (q = 2, 2^16 patterns would be many;
+    here all 256 patterns of plane 0 against a fixed plane 1) at N = 8 rows: y = x W^T as an
+    exact rational sum equals gemm_blockwise and the LUT route lut_gemm_blockwise."""
+    rng = _rng(121)
+    q, N, K = 2, 8, 8
+    x = _rand_fp16(rng, (1, K))
+    P = rng.integers(-3, 4, size=(q, 8, 1))
+    alpha = np.ldexp(1.0, P).astype(np.float32)
+    s1 = rng.choice([-1, 1], size=(N, K)).astype(np.int8)
+    for pat in range(256):
+        s0 = np.array([[1 if (pat >> b) & 1 else -1 for b in range(8)]] * N, dtype=np.int8)
+        s0[3] = -s0[3]
+        s = np.stack([s0, s1])
+        planes, exps, _ = oracle.pack_blockwise(s, alpha)
+        y = oracle.gemm_blockwise(x, planes, exps)
+        y2 = oracle.lut_gemm_blockwise(x, planes, exps)
+        for n in range(N):
+            want = sum(_frac(x[0, k]) * _frac(alpha[i, n, 0]) * int(s[i, n, k]) for i in range(q) for k in range(K))
+            assert _frac(y[0, n]) == want and _frac(y2[0, n]) == want
+
+
+def test_s12_blockwise_equals_rowwise_g8_with_replicated_exponents():
+    """The block-wise weight is the row-wise g = 8 weight whose exponents are the block's,
+    replicated over its N/8 rows: same planes from pack_canonical with alpha
+    replicated, same dequantised matrix from the pinned row-wise dequant."""
+    rng = _rng(122)
+    q, N, K = 3, 40, 64
+    s = rng.choice([-1, 1], size=(q, N, K)).astype(np.int8)
+    alpha = (rng.choice([-1.0, 1.0], size=(q, 8, K // 8)) * rng.uniform(0.01, 0.2, size=(q, 8, K // 8))).astype(np.float32)
+    planes, exps, _ = oracle.pack_blockwise(s, alpha)
+    alpha_rows = np.repeat(alpha, N // 8, axis=1)                   # [q][N][K/8]
+    planes_r, exps_r, _ = oracle.pack_canonical(s, alpha_rows, 8)
+    assert np.array_equal(planes, planes_r)
+    assert np.array_equal(oracle.blockwise_row_exps(exps, N), exps_r)
+    assert np.array_equal(oracle.dequant_blockwise(planes, exps, K), oracle.dequant(planes_r, exps_r, 8, K))
+
+
+def test_s12_blockwise_scale_of_one_block_moves_only_its_rows_and_columns():
+    """Shifting one exponent e_i[b][c] by d scales exactly rows of block b, columns 8c..8c+7
+    of plane i's term by 2^d; everything else is unchanged (exact in fp64)."""
+    rng = _rng(123)
+    q, N, K = 2, 32, 48
+    planes = rng.integers(0, 256, size=(q, N, K // 8), dtype=np.uint8)
+    exps = rng.integers(-4, 5, size=(q, 8, K // 8)).astype(np.int8)
+    W0 = oracle.dequant_blockwise(planes, exps, K)
+    e2 = exps.copy()
+    e2[1, 5, 2] += 3
+    W1 = oracle.dequant_blockwise(planes, e2, K)
+    nb = N // 8
+    s1 = oracle.unpack_signs(planes, K)[1].astype(np.float64)
+    delta = np.zeros_like(W0)
+    delta[5 * nb:6 * nb, 16:24] = s1[5 * nb:6 * nb, 16:24] * (2.0 ** (exps[1, 5, 2] + 3) - 2.0 ** exps[1, 5, 2])
+    assert np.array_equal(W1 - W0, delta)
