@@ -182,6 +182,30 @@ shiftadd_status shiftadd_lut_gemv_colwise(const uint16_t* x, const uint8_t* plan
                                           int layout, int N, int K, int q, uint16_t* y, unsigned flags,
                                           void* stream);
 
+/* NEXT-f1 -- block-wise scales, "Ours (Lat.)" (Fig. 4(a)): "a block-wise
+ * scaling factor design that groups 8 columns and 1/8 of the original rows to share a scaling
+ * factor, ensuring compatibility with the BCQ kernel".  Plane i has one PoT scale per (row
+ * block b = n / (N/8), column group c = k / 8) -- the 8 weights of a key byte share it:
+ *   W_hat[n][k] = sum_i 2^{e_i[n / (N/8)][k / 8]} s_i(n, k)       (reading R24)
+ *
+ * shiftadd_pack_blockwise: signs int8 [q][N][K] (+-1), alpha_bw fp32 [q][8][K/8] -> planes
+ *   (same byte format and layouts as shiftadd_pack, each block's sign folded into its 8-bit
+ *   groups) and exps_bw int8 [q][8][K/8] (the compact layout: q K bytes; same P rule, zero
+ *   sentinel and clamp counting as shiftadd_pack).  8 | N, K % 8 == 0 (tiled: K % 256 == 0).
+ *
+ * shiftadd_lut_gemv_blockwise: y[n] = fp16_rne( sum_i sum_c 2^{e_i[b(n)][c]} T_c[key_i(n, c)] ),
+ *   M = 1, tiled planes: every LUT query is scaled by its block's 2^e (one FFMA per query; the
+ *   lane keeps its 16 q scale factors in registers, the exponent array is read once per CTA,
+ *   never streamed).  K % 256 == 0, K <= 256 x #SMs, 8 | N, 1 <= q <= 4.  Workspace:
+ *   shiftadd_workspace_bytes_blockwise(N, K) bytes (shiftadd_lut_gemm's zero-once contract).
+ *   flags: 0 or SHIFTADD_FLAG_PDL.  planes 16-B aligned, x 16-B aligned. */
+shiftadd_status shiftadd_pack_blockwise(const int8_t* signs, const float* alpha_bw, int q, int N, int K, int layout,
+                                       uint8_t* planes, int8_t* exps_bw, int32_t* counts, void* stream);
+size_t shiftadd_workspace_bytes_blockwise(int N, int K);
+shiftadd_status shiftadd_lut_gemv_blockwise(const uint16_t* x, const uint8_t* planes, const int8_t* exps_bw,
+                                            int layout, int N, int K, int q, uint16_t* y, void* workspace,
+                                            size_t workspace_bytes, unsigned flags, void* stream);
+
 /* NEXT-f2 -- additive PoT with K = 2 terms per scale (Eq. 2: "the k-th
  * PoT minimizes the residual of the (k-1)-th").
  *

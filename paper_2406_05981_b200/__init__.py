@@ -23,7 +23,7 @@ __all__ = [
     "LAYOUT_CANONICAL", "LAYOUT_TILED", "FLAG_PDL", "FLAG_SPLITK", "EXP_ZERO", "ShiftAddError", "lib",
     "PackedLayer", "packed_bytes", "pack", "lut_gemm", "lut_gemv", "workspace_bytes",
     "gemm_plan", "Workspace", "pack_colwise", "lut_gemv_colwise", "pack_apot2", "bcq_quantize",
-    "lut_gemv_fused", "workspace_bytes_fused",
+    "lut_gemv_fused", "workspace_bytes_fused", "pack_blockwise", "lut_gemv_blockwise",
 ]
 
 LAYOUT_CANONICAL = 0
@@ -102,6 +102,13 @@ def lib():
         L.shiftadd_lut_gemv_fused.restype = c_int
         L.shiftadd_lut_gemv_fused.argtypes = [vp, c_int, c_int, c_int, c_int, ctypes.POINTER(_Segment), vp, c_size,
                                               ctypes.c_uint, vp]
+        L.shiftadd_pack_blockwise.restype = c_int
+        L.shiftadd_pack_blockwise.argtypes = [vp, vp, c_int, c_int, c_int, c_int, vp, vp, vp, vp]
+        L.shiftadd_workspace_bytes_blockwise.restype = c_size
+        L.shiftadd_workspace_bytes_blockwise.argtypes = [c_int, c_int]
+        L.shiftadd_lut_gemv_blockwise.restype = c_int
+        L.shiftadd_lut_gemv_blockwise.argtypes = [vp, vp, vp, c_int, c_int, c_int, c_int, vp, vp, c_size,
+                                                  ctypes.c_uint, vp]
         L.shiftadd_gemm_plan.restype = c_int
         L.shiftadd_gemm_plan.argtypes = [c_int] * 6 + [ctypes.POINTER(c_int * 4)]
         v = L.shiftadd_abi_version()
@@ -149,6 +156,7 @@ class PackedLayer:
     counts: torch.Tensor      # int32[2] on device: clamped exponents, invalid inputs
     _ws_bytes: dict = field(default_factory=dict, repr=False)   # M -> workspace bytes
     colwise: bool = False     # NEXT-f1: exps is exps_col [q][K] (column-wise scales)
+    blockwise: bool = False   # NEXT-f1: exps is exps_bw [q][8][K/8] (block-wise scales, "Ours (Lat.)")
     exps2: torch.Tensor | None = None   # NEXT-f2: second additive-PoT term codes (like exps)
 
     @property
@@ -263,6 +271,55 @@ def pack_colwise(signs: torch.Tensor, alpha_col: torch.Tensor, layout: int = LAY
     return PackedLayer(planes, exps, q, N, K, K, layout, counts, colwise=True)
 
 
+def pack_blockwise(signs: torch.Tensor, alpha_bw: torch.Tensor, layout: int = LAYOUT_TILED,
+                   stream=None) -> PackedLayer:
+    """NEXT-f1 block-wise scales ("Ours (Lat.)") on the device: int8 sign
+    planes [q][N][K] and fp32 scales [q][8][K/8] (8 columns x N/8 rows per scale) -> key bytes
+    (each block's sign folded) + compact exps_bw int8 [q][8][K/8] (shiftadd_pack_blockwise)."""
+    if signs.dtype != torch.int8 or alpha_bw.dtype != torch.float32:
+        raise TypeError("signs must be int8 and alpha_bw float32")
+    if not (signs.is_cuda and alpha_bw.is_cuda):
+        raise ValueError("pack_blockwise runs on the GPU; pass CUDA tensors")
+    q, N, K = signs.shape
+    if tuple(alpha_bw.shape) != (q, 8, K // 8):
+        raise ValueError("alpha_bw must be [q][8][K/8]")
+    signs = signs.contiguous()
+    alpha_bw = alpha_bw.contiguous()
+    pb, _ = packed_bytes(layout, q, N, K, K)
+    dev = signs.device
+    planes = torch.empty(pb, dtype=torch.uint8, device=dev)
+    exps = torch.empty(q * K, dtype=torch.int8, device=dev)
+    counts = torch.zeros(2, dtype=torch.int32, device=dev)
+    with torch.cuda.device(dev):
+        st = lib().shiftadd_pack_blockwise(_ptr(signs), _ptr(alpha_bw), q, N, K, layout, _ptr(planes), _ptr(exps),
+                                           _ptr(counts), _stream_ptr(stream, dev))
+    _check(st, "shiftadd_pack_blockwise")
+    return PackedLayer(planes, exps, q, N, K, 8, layout, counts, blockwise=True)
+
+
+def lut_gemv_blockwise(x: torch.Tensor, layer: PackedLayer, out: torch.Tensor | None = None, pdl: bool = False,
+                       workspace: Workspace | None = None, stream=None) -> torch.Tensor:
+    """y = x (.) the block-wise layer, batch 1 (shiftadd_lut_gemv_blockwise)."""
+    x = x.reshape(-1)
+    if not layer.blockwise:
+        raise ValueError("layer was not packed by pack_blockwise")
+    if x.dtype != torch.float16 or not x.is_cuda or x.numel() != layer.K:
+        raise ValueError("x must be fp16 [K] on the device")
+    dev = layer.device
+    if out is None:
+        out = torch.empty(layer.N, dtype=torch.float16, device=dev)
+    need = int(lib().shiftadd_workspace_bytes_blockwise(layer.N, layer.K))
+    ws = (workspace or _workspace_for(dev, stream)).get(need)
+    if torch.cuda.current_device() != dev.index:
+        torch.cuda.set_device(dev)
+    sptr = (stream if stream is not None else torch.cuda.current_stream(dev)).cuda_stream
+    _check(lib().shiftadd_lut_gemv_blockwise(x.data_ptr(), layer.planes.data_ptr(), layer.exps.data_ptr(), layer.layout,
+                                             layer.N, layer.K, layer.q, out.data_ptr(),
+                                             ws.data_ptr() if ws is not None else None, ws.numel() if ws is not None else 0,
+                                             FLAG_PDL if pdl else 0, sptr), "shiftadd_lut_gemv_blockwise")
+    return out
+
+
 def lut_gemv_colwise(x: torch.Tensor, layer: PackedLayer, out: torch.Tensor | None = None, pdl: bool = False,
                      stream=None) -> torch.Tensor:
     """NEXT-f1: y[N] = x[K] (.) a column-wise-scaled layer, fp16 (shiftadd_lut_gemv_colwise)."""
@@ -344,6 +401,11 @@ def lut_gemm(x: torch.Tensor, layer: PackedLayer, out: torch.Tensor | None = Non
         out = torch.empty((M, layer.N), dtype=torch.float16, device=dev)
     if out.dtype != torch.float16 or out.dim() != 2 or out.shape[0] != M or out.stride(-1) != 1:
         raise ValueError("out must be fp16 [M][>=N] with unit column stride")
+    if layer.blockwise:
+        if M != 1:
+            raise ShiftAddError("block-wise layers: batch-1 only (shiftadd_lut_gemv_blockwise)")
+        lut_gemv_blockwise(x2[0], layer, out=out[0], pdl=pdl, workspace=workspace, stream=stream)
+        return out[0] if squeeze else out
     if layer.colwise:
         if M != 1:
             raise ShiftAddError("column-wise layers: batch-1 only (shiftadd_lut_gemv_colwise)")

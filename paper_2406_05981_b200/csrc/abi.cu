@@ -235,6 +235,72 @@ shiftadd_status shiftadd_lut_gemv_colwise(const uint16_t* x, const uint8_t* plan
   return SHIFTADD_OK;
 }
 
+shiftadd_status shiftadd_pack_blockwise(const int8_t* signs, const float* alpha_bw, int q, int N, int K, int layout,
+                                       uint8_t* planes, int8_t* exps_bw, int32_t* counts, void* stream) {
+  if (!signs || !alpha_bw || !planes || !exps_bw) return fail(SHIFTADD_ERR_INVALID, "null pointer argument");
+  shiftadd_status st = check_shape(q, N, K, 8, 8);
+  if (st != SHIFTADD_OK) return st;
+  if (N % 8) return fail(SHIFTADD_ERR_INVALID, "block-wise scales need 8 | N (N=%d)", N);
+  if ((st = check_layout(layout, K, 128)) != SHIFTADD_OK) return st;
+  if (!aligned(signs, 8) || !aligned(alpha_bw, 4) || !aligned(planes, 16) || (counts && !aligned(counts, 4)))
+    return fail(SHIFTADD_ERR_INVALID, "misaligned pointer (signs 8 B, alpha 4 B, planes 16 B)");
+  DevInfo di;
+  if ((st = device_info(&di)) != SHIFTADD_OK) return st;
+  const cudaError_t e = launch_pack_blockwise(signs, alpha_bw, q, N, K, layout, planes, exps_bw, counts,
+                                              reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "pack_blockwise launch");
+  return SHIFTADD_OK;
+}
+
+size_t shiftadd_workspace_bytes_blockwise(int N, int K) {
+  if (N < 8 || N % 8 || N > kMaxRows || K < kTileK || K % kTileK) return 0;
+  return stream_workspace_bytes(1, K / kTileK, (N + kTileRows - 1) / kTileRows);
+}
+
+shiftadd_status shiftadd_lut_gemv_blockwise(const uint16_t* x, const uint8_t* planes, const int8_t* exps_bw,
+                                            int layout, int N, int K, int q, uint16_t* y, void* workspace,
+                                            size_t workspace_bytes, unsigned flags, void* stream) {
+  if (!x || !planes || !exps_bw || !y) return fail(SHIFTADD_ERR_INVALID, "null pointer argument");
+  shiftadd_status st = check_shape(q, N, K, 8, 4);
+  if (st != SHIFTADD_OK) return st;
+  if (N % 8) return fail(SHIFTADD_ERR_INVALID, "block-wise scales need 8 | N (N=%d)", N);
+  if ((st = check_layout(layout, K, 128)) != SHIFTADD_OK) return st;
+  if (layout != SHIFTADD_LAYOUT_TILED) return fail(SHIFTADD_ERR_UNSUPPORTED, "block-wise GEMV needs the tiled layout");
+  if (flags & ~SHIFTADD_FLAG_PDL) return fail(SHIFTADD_ERR_INVALID, "unknown flags 0x%x", flags);
+  if (!aligned(x, 16) || !aligned(planes, 16) || !aligned(y, 2))
+    return fail(SHIFTADD_ERR_INVALID, "misaligned pointer (x, planes 16 B)");
+  DevInfo di;
+  if ((st = device_info(&di)) != SHIFTADD_OK) return st;
+  if (!stream_shape_ok(K, di.sms)) return fail(SHIFTADD_ERR_UNSUPPORTED, "block-wise GEMV: K=%d above 256 x #SMs", K);
+  const size_t need = shiftadd_workspace_bytes_blockwise(N, K);
+  if (need > 0 && (!workspace || workspace_bytes < need || !aligned(workspace, 16)))
+    return fail(SHIFTADD_ERR_INVALID, "workspace needs %zu bytes, 16-B aligned (got %zu)", need, workspace_bytes);
+  StreamLaunch L = {};
+  L.x = reinterpret_cast<const __half*>(x);
+  L.M = 1;
+  L.ldx = K;
+  L.K = K;
+  L.nseg = 1;
+  L.seg[0] = StreamSeg{planes, exps_bw, reinterpret_cast<__half*>(y), q, N};
+  L.exps_bw = exps_bw;
+  L.workspace = workspace;
+  L.grid = di.sms;
+  if (N % 128 == 0) {   // scaled LUTs: q LUTs of 32 KB (64 KB slab for q <= 2, two slabs else)
+    L.su = 16;
+    const int lut = q <= 2 ? 64 * 1024 : 128 * 1024;
+    const int slot = L.su * q * (kTileBytes + kTileExps);
+    L.nst = (kStreamSmemBudget - lut - 512) / slot;
+    L.nst = L.nst > 16 ? 16 : L.nst;
+  } else {
+    L.su = 8;
+    L.nst = stream_stages(q, kStreamSmemBudget, L.su, 1);
+  }
+  L.pdl = (flags & SHIFTADD_FLAG_PDL) ? 1 : 0;
+  const cudaError_t e = launch_lut_stream(L, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "lut_gemv_blockwise launch");
+  return SHIFTADD_OK;
+}
+
 shiftadd_status shiftadd_pack_apot2(const int8_t* signs, const float* alpha, int q, int N, int K, int g,
                                     int layout, uint8_t* planes, int8_t* exps, int8_t* exps2, int32_t* counts,
                                     void* stream) {

@@ -220,6 +220,7 @@ struct StreamLaunch {
   void* workspace;
   int grid, nst, su, pdl;
   int half;   // 1: the co-resident variant (<= 113 KB shared memory, two CTAs fit one SM)
+  const int8_t* exps_bw;   // non-null: NEXT-f1 block-wise exponents [q][8][K/8] (M = 1, one segment)
 };
 
 struct LaunchPlan {
@@ -239,6 +240,8 @@ cudaError_t launch_pack(const int8_t* signs, const float* alpha, int q, int N, i
 
 cudaError_t launch_pack_apot2(const float* alpha, int q, int N, int K, int g, int layout, int8_t* exps2,
                               cudaStream_t stream);
+cudaError_t launch_pack_blockwise(const int8_t* signs, const float* alpha_bw, int q, int N, int K, int layout,
+                                  uint8_t* planes, int8_t* exps_bw, int32_t* counts, cudaStream_t stream);
 cudaError_t launch_pack_colwise(const int8_t* signs, const float* alpha_col, int q, int N, int K,
                                 int layout, uint8_t* planes, int8_t* exps_col, int32_t* counts,
                                 cudaStream_t stream);

@@ -82,6 +82,9 @@ struct StreamParams {
              // t % (16 / su) == w / su, unit w % su
   int pdl;
   int skew;   // offset the two warp halves' stage pairs (see consume_run)
+  const int8_t* exps_bw;   // NEXT-f1 block-wise exponents [q][8][K/8] (BW kernels; planes only in the ring)
+  int bw_rows;             // rows per block, N / 8
+  int bw_rgb;              // BW = 2: row groups per block (N / 128)
 };
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
@@ -541,9 +544,234 @@ __device__ __forceinline__ void consume_run_mw_q(const StreamParams& p, const Se
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// NEXT-f1 block-wise scales, "Ours (Lat.)": one PoT scale per (row block
+// of N/8 rows, 8-column group) -- the 8 weights of a key byte share it, so each LUT query is
+// scaled once: acc = fma(T[key], 2^e, acc), the 2^e formed by an integer add on the exponent
+// field of 1.0 (pow2_bits).  A lane's 16 queries of a plane touch 16 column groups (the tiled
+// rotation), so it keeps those 16 q scale factors in registers for the current (slice, row
+// block) and reloads them (16 q bytes of the compact [q][8][K/8] array, L1/L2 resident) only
+// when its row block changes.  The exponent array is never streamed: q K bytes per call.
+// The 16 q scale factors of a lane are kept as bf16 pairs (2^e is exact in bf16: an 8-bit
+// exponent and no mantissa), 8 q registers; a query widens its factor back to fp32 with one
+// shift or mask (the high half is already an fp32 bit pattern once the low half is cleared).
+template <int Q>
+__device__ __forceinline__ void load_bw_scales(const int8_t* __restrict__ exps_bw, int KB, int s, int b, int r, int h,
+                                               uint32_t (&S2)[Q][8]) {
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    // the lane's 16 groups 32s + 16h + 0..15 are one aligned 16-B load; step j uses group
+    // (j + r) & 15, so rotate the 16 bytes right by r (words by r >> 2, then bytes by r & 3)
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(exps_bw + ((size_t)i * 8 + b) * KB + 32 * s + 16 * h));
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    const int rw = r >> 2, rb = r & 3;
+    uint32_t t[4], e4[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      t[k] = rw == 0 ? w[k] : rw == 1 ? w[(k + 1) & 3] : rw == 2 ? w[(k + 2) & 3] : w[(k + 3) & 3];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) e4[k] = __funnelshift_r(t[k], t[(k + 1) & 3], 8 * rb);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      uint32_t pr = 0;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int j = 2 * k + u;
+        const int e = (int)(int8_t)((e4[j >> 2] >> (8 * (j & 3))) & 0xffu);
+        pr |= ((uint32_t)(e < -127 ? 0 : e + 127) << 7) << (16 * u);   // bf16 bits of 2^e (EXP_ZERO: +0)
+      }
+      S2[i][k] = pr;
+    }
+  }
+}
+
+template <int Q, uint32_t HOFF>
+__device__ __forceinline__ float unit_dot_bw(uint32_t sp, const uint32_t (&cst)[4], const uint32_t (&S2)[Q][8]) {
+  uint4 w[Q];
+#pragma unroll
+  for (int i = 0; i < Q; ++i) w[i] = lds_u4(sp + i * kTileBytes);
+  float pc[4];
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const uint32_t word = (j < 4) ? w[i].x : (j < 8) ? w[i].y : (j < 12) ? w[i].z : w[i].w;
+      const float v = lds_f32(kDynBase + HOFF + prmt(word, cst[j >> 2], step_sel(j)));
+      const float sc = __uint_as_float((j & 1) ? (S2[i][j >> 1] & 0xffff0000u) : (S2[i][j >> 1] << 16));
+      pc[j & 3] = (i == 0 && j < 4) ? v * sc : __fmaf_rn(v, sc, pc[j & 3]);
+    }
+  }
+  return (pc[0] + pc[1]) + (pc[2] + pc[3]);
+}
+
+template <int Q, uint32_t HOFF>
+__device__ __forceinline__ void consume_run_bw(const StreamParams& p, const SegDev& sg, int s, int rga, int re,
+                                               RingPos& rp, uint32_t ring, uint32_t full, uint32_t empty,
+                                               const uint32_t (&cst)[4], int wu, int lane, unsigned long long ep) {
+  const int r = lane >> 1, h = lane & 1;
+  uint32_t S[Q][8];
+  int cur_b = -1;
+  for (int rg = rga; rg < re; rg += p.su, rp.next(p.nst)) {
+    const int n = re - rg < p.su ? re - rg : p.su;
+    const uint32_t slot = ring + (uint32_t)(rp.j * p.slot);
+    const int u = rg + wu;
+    if (wu < n) {
+      const int nrow = u * kTileRows + r;
+      int b = nrow / p.bw_rows;
+      b = b > 7 ? 7 : b;   // padding rows of the last row group
+      if (b != cur_b) {
+        load_bw_scales<Q>(p.exps_bw, p.S * (kTileK / 8), s, b, r, h, S);
+        cur_b = b;
+      }
+    }
+    mbar_wait(full + 8 * rp.j, (uint32_t)(rp.k & 1));
+    if (wu < n) {
+      float acc = unit_dot_bw<Q, HOFF>(slot + (uint32_t)(wu * Q * kTileBytes + 16 * lane), cst, S);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + 8 * rp.j);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      if (h == 0) {
+        if (p.S == 1) {
+          const int nl = u * kTileRows + r;
+          if (nl < sg.N) sg.y[nl] = __float2half_rn(acc);
+        } else {
+          const size_t w = (((size_t)sg.rgoff + u) * p.S + s) * kTileRows + r;
+          st_relaxed_u64(p.part + w, ep | __float_as_uint(acc));
+        }
+      }
+    } else {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + 8 * rp.j);
+    }
+  }
+}
+
+template <uint32_t HOFF>
+__device__ __forceinline__ void consume_run_bw_q(const StreamParams& p, const SegDev& sg, int s, int rga, int re,
+                                                 RingPos& rp, uint32_t ring, uint32_t full, uint32_t empty,
+                                                 const uint32_t (&cst)[4], int wu, int lane, unsigned long long ep) {
+  switch (sg.q) {
+    case 1: consume_run_bw<1, HOFF>(p, sg, s, rga, re, rp, ring, full, empty, cst, wu, lane, ep); break;
+    case 2: consume_run_bw<2, HOFF>(p, sg, s, rga, re, rp, ring, full, empty, cst, wu, lane, ep); break;
+    case 3: consume_run_bw<3, HOFF>(p, sg, s, rga, re, rp, ring, full, empty, cst, wu, lane, ep); break;
+    default: consume_run_bw<4, HOFF>(p, sg, s, rga, re, rp, ring, full, empty, cst, wu, lane, ep); break;
+  }
+}
+
+// BW = 2 (N % 128 == 0: a row block is whole row groups): the block scales are folded into
+// the LUT instead -- for the (slice, row block) a run of units lies in, plane i gets its own
+// LUT T'_i[c][key] = 2^{e_i[b][c]} T_c[key] (an exact fp32 scaling by a power of two), so a
+// query is PRMT + LDS + FADD as in the row-wise kernel and no shift remains per query or per
+// chunk.  Plane i's LUT sits in slab i >> 1, column half i & 1 (the LDS immediate); the CTA
+// rebuilds its q LUTs when its units cross into the next row block or slice (consumer warps
+// meet on a named barrier before and after).
+template <int NWC, int Q>
+__device__ __forceinline__ void build_lut_scaled(const uint4 xv, const int8_t* __restrict__ exps_bw, int KB, int s, int b,
+                                                 int warp, int lane) {
+  const float2 f01 = __half22float2(*reinterpret_cast<const __half2*>(&xv.x));
+  const float2 f23 = __half22float2(*reinterpret_cast<const __half2*>(&xv.y));
+  const float2 f45 = __half22float2(*reinterpret_cast<const __half2*>(&xv.z));
+  const float2 f67 = __half22float2(*reinterpret_cast<const __half2*>(&xv.w));
+  const float A[4] = {-f01.x - f01.y, f01.x - f01.y, f01.y - f01.x, f01.x + f01.y};
+  const float B[4] = {-f23.x - f23.y, f23.x - f23.y, f23.y - f23.x, f23.x + f23.y};
+  float sc[Q];
+#pragma unroll
+  for (int i = 0; i < Q; ++i) sc[i] = pow2_bits((int)__ldg(exps_bw + ((size_t)i * 8 + b) * KB + 32 * s + lane));
+#pragma unroll
+  for (int hh = 0; hh < 16 / NWC; ++hh) {
+    const int hi = warp + hh * NWC;
+    const float H = ((hi & 1 ? f45.x : -f45.x) + (hi & 2 ? f45.y : -f45.y)) +
+                    ((hi & 4 ? f67.x : -f67.x) + (hi & 8 ? f67.y : -f67.y));
+#pragma unroll
+    for (int lo = 0; lo < 16; ++lo) {
+      const float t = (A[lo & 3] + B[lo >> 2]) + H;
+#pragma unroll
+      for (int i = 0; i < Q; ++i)
+        sts_f32(kDynBase + (uint32_t)(i >> 1) * 65536u + (uint32_t)(i & 1) * 128u + 4u * lane + ((uint32_t)(hi * 16 + lo) << 8),
+                t * sc[i]);
+    }
+  }
+}
+
+template <int Q>
+__device__ __forceinline__ float unit_dot_lut(uint32_t sp, const uint32_t (&cst)[4]) {
+  uint4 w[Q];
+#pragma unroll
+  for (int i = 0; i < Q; ++i) w[i] = lds_u4(sp + i * kTileBytes);
+  float pc[4];
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    const uint32_t base = kDynBase + (uint32_t)(i >> 1) * 65536u + (uint32_t)(i & 1) * 128u;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const uint32_t word = (j < 4) ? w[i].x : (j < 8) ? w[i].y : (j < 12) ? w[i].z : w[i].w;
+      const float v = lds_f32(base + prmt(word, cst[j >> 2], step_sel(j)));
+      pc[j & 3] = (i == 0 && j < 4) ? v : pc[j & 3] + v;
+    }
+  }
+  return (pc[0] + pc[1]) + (pc[2] + pc[3]);
+}
+
+template <int NWC, int Q>
+__device__ __forceinline__ void consume_run_lut(const StreamParams& p, const SegDev& sg, int s, int rga, int re,
+                                                RingPos& rp, uint32_t ring, uint32_t full, uint32_t empty,
+                                                const uint32_t (&cst)[4], int wu, int lane, unsigned long long ep,
+                                                const uint4 xv, int& cur) {
+  const int r = lane >> 1, h = lane & 1;
+  const int KB = p.S * (kTileK / 8);
+  for (int r0 = rga; r0 < re;) {
+    const int b = r0 / p.bw_rgb;
+    const int r1 = (b + 1) * p.bw_rgb < re ? (b + 1) * p.bw_rgb : re;
+    const int key = s * 8 + b;
+    if (key != cur) {   // rebuild the q scaled LUTs for (s, b)
+      asm volatile("bar.sync 1, %0;" ::"r"(NWC * 32) : "memory");
+      build_lut_scaled<NWC, Q>(xv, p.exps_bw, KB, s, b, wu, lane);
+      asm volatile("bar.sync 1, %0;" ::"r"(NWC * 32) : "memory");
+      cur = key;
+    }
+    for (int rg = r0; rg < r1; rg += p.su, rp.next(p.nst)) {
+      const int n = r1 - rg < p.su ? r1 - rg : p.su;
+      const uint32_t slot = ring + (uint32_t)(rp.j * p.slot);
+      mbar_wait(full + 8 * rp.j, (uint32_t)(rp.k & 1));
+      if (wu < n) {
+        float acc = unit_dot_lut<Q>(slot + (uint32_t)(wu * Q * kTileBytes + 16 * lane), cst);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + 8 * rp.j);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        if (h == 0) {
+          const int u = rg + wu;
+          if (p.S == 1) {
+            const int nl = u * kTileRows + r;
+            if (nl < sg.N) sg.y[nl] = __float2half_rn(acc);
+          } else {
+            st_relaxed_u64(p.part + (((size_t)sg.rgoff + u) * p.S + s) * kTileRows + r, ep | __float_as_uint(acc));
+          }
+        }
+      } else {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + 8 * rp.j);
+      }
+    }
+    r0 = r1;
+  }
+}
+
+template <int NWC>
+__device__ __forceinline__ void consume_run_lut_q(const StreamParams& p, const SegDev& sg, int s, int rga, int re,
+                                                  RingPos& rp, uint32_t ring, uint32_t full, uint32_t empty,
+                                                  const uint32_t (&cst)[4], int wu, int lane, unsigned long long ep,
+                                                  const uint4 xv, int& cur) {
+  switch (sg.q) {
+    case 1: consume_run_lut<NWC, 1>(p, sg, s, rga, re, rp, ring, full, empty, cst, wu, lane, ep, xv, cur); break;
+    case 2: consume_run_lut<NWC, 2>(p, sg, s, rga, re, rp, ring, full, empty, cst, wu, lane, ep, xv, cur); break;
+    case 3: consume_run_lut<NWC, 3>(p, sg, s, rga, re, rp, ring, full, empty, cst, wu, lane, ep, xv, cur); break;
+    default: consume_run_lut<NWC, 4>(p, sg, s, rga, re, rp, ring, full, empty, cst, wu, lane, ep, xv, cur); break;
+  }
+}
+
 // MINB = 2: registers capped so that two CTAs fit one SM -- with <= 113 KB of shared memory
 // the next call's CTA becomes resident (and streams its weights) while this one finishes.
-template <int NWC, int MINB, int MW>
+template <int NWC, int MINB, int MW, int BW = 0>
 __global__ void __launch_bounds__((NWC + 1) * 32, MINB) lut_stream_kernel(const __grid_constant__ StreamParams p) {
   constexpr int kNT = (NWC + 1) * 32;
   if (threadIdx.x == 0) check_dyn_base();
@@ -583,15 +811,20 @@ __global__ void __launch_bounds__((NWC + 1) * 32, MINB) lut_stream_kernel(const 
         const int re = run_end(p, a, end);
         const SegDev& sg = p.seg[a.g];
         const size_t ub = (size_t)a.s * sg.RG;
-        for (int rg = a.rg; rg < re; rg += p.su, ++t, rp.next(p.nst)) {
+        for (int rg = a.rg; rg < re; ++t, rp.next(p.nst)) {
           if (rp.k > 0) mbar_wait(empty + 8 * rp.j, (uint32_t)((rp.k - 1) & 1));
-          const int n = re - rg < p.su ? re - rg : p.su;
-          const uint32_t bp = (uint32_t)(n * sg.q * kTileBytes), be = (uint32_t)(n * sg.q * kTileExps);
+          int n = re - rg < p.su ? re - rg : p.su;
+          if (BW == 2) {   // stages do not cross a row-block boundary
+            const int bend = (rg / p.bw_rgb + 1) * p.bw_rgb;
+            n = bend - rg < n ? bend - rg : n;
+          }
+          const uint32_t bp = (uint32_t)(n * sg.q * kTileBytes), be = BW ? 0u : (uint32_t)(n * sg.q * kTileExps);
           const uint32_t fb = full + 8 * rp.j;
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(bp + be) : "memory");
           const uint32_t dst = ring + (uint32_t)(rp.j * p.slot);
           bulk_g2s(dst, sg.planes + (ub + rg) * sg.q * kTileBytes, bp, fb, pol);
-          bulk_g2s(dst + (uint32_t)p.slot_planes, sg.exps + (ub + rg) * sg.q * kTileExps, be, fb, pol);
+          if (!BW) bulk_g2s(dst + (uint32_t)p.slot_planes, sg.exps + (ub + rg) * sg.q * kTileExps, be, fb, pol);
+          rg += n;
         }
         next_run(p, a, re);
       }
@@ -607,14 +840,14 @@ __global__ void __launch_bounds__((NWC + 1) * 32, MINB) lut_stream_kernel(const 
       if (tid == 32 && p.S > 1)   // a lane whose x does not gate warp 0
         asm volatile("st.shared.u32 [%0], %1;" ::"r"(s_epoch), "r"((unsigned)(ld_relaxed_u64(p.done) >> 32) + 1u)
                      : "memory");
-      if (MW == 1) {
+      if (MW == 1 && BW != 2) {
         const uint64_t pol_keep = policy_evict_last();
         const uint4 xa = ldg_keep(p.x + (size_t)s0 * kTileK + 8 * lane, pol_keep);
         uint4 xb = xa;
         if (two) xb = ldg_keep(p.x + (size_t)(s0 + 1) * kTileK + 8 * lane, pol_keep);
         build_lut<NWC>(xa, 0u, warp, lane);
         if (two) build_lut<NWC>(xb, 128u, warp, lane);
-      } else {
+      } else if (MW != 1) {
         build_lut_mw<NWC, MW>(p, s0, 0, warp, lane);
         if (two && MW < 8) build_lut_mw<NWC, MW>(p, s0 + 1, 1, warp, lane);
       }
@@ -644,12 +877,28 @@ __global__ void __launch_bounds__((NWC + 1) * 32, MINB) lut_stream_kernel(const 
       }
       const bool skew = p.skew && warp >= NWC / 2;
       int t = 0;
+      uint4 xs[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+      if (BW == 2 && any) {
+        const uint64_t pol_keep = policy_evict_last();
+        xs[0] = ldg_keep(p.x + (size_t)s0 * kTileK + 8 * lane, pol_keep);
+        if (two) xs[1] = ldg_keep(p.x + (size_t)(s0 + 1) * kTileK + 8 * lane, pol_keep);
+      }
+      int cur = -1;
       for (Pos a = start; before(a, end);) {
         const int re = run_end(p, a, end);
-        if (a.s == s0)
+        if (BW == 2) {
+          consume_run_lut_q<NWC>(p, p.seg[a.g], a.s, a.rg, re, rp, ring, full, empty, cst, wu, lane, ep,
+                                 a.s == s0 ? xs[0] : xs[1], cur);
+        } else if (BW == 1) {
+          if (a.s == s0)
+            consume_run_bw_q<0u>(p, p.seg[a.g], a.s, a.rg, re, rp, ring, full, empty, cst, wu, lane, ep);
+          else
+            consume_run_bw_q<128u>(p, p.seg[a.g], a.s, a.rg, re, rp, ring, full, empty, cst, wu, lane, ep);
+        } else if (a.s == s0) {
           consume_run_q<0u>(p, p.seg[a.g], a.s, a.rg, re, rp, t, ring, full, empty, cst, wu, lane, ep, skew);
-        else
+        } else {
           consume_run_q<128u>(p, p.seg[a.g], a.s, a.rg, re, rp, t, ring, full, empty, cst, wu, lane, ep, skew);
+        }
         next_run(p, a, re);
       }
     } else {
@@ -797,10 +1046,14 @@ cudaError_t launch_lut_stream(const StreamLaunch& L, cudaStream_t stream) {
     if (e == cudaSuccess) e = cudaFuncSetAttribute(lut_stream_kernel<16, 1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(lut_stream_kernel<16, 1, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(lut_stream_kernel<8, 1, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(lut_stream_kernel<16, 1, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    if (e == cudaSuccess)
       e = cudaFuncSetAttribute(lut_stream_kernel<8, 2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 113 * 1024);
     attr_err = e;
   });
-  if (L.nseg < 1 || L.nseg > kMaxSegments || L.nst < 1 || L.nst > 16 || L.su != (L.half ? 8 : 16))
+  if (L.nseg < 1 || L.nseg > kMaxSegments || L.nst < 1 || L.nst > 16 || (L.su != 8 && L.su != 16))
     return cudaErrorInvalidValue;
   StreamParams p = {};
   p.x = L.x;
@@ -840,20 +1093,32 @@ cudaError_t launch_lut_stream(const StreamLaunch& L, cudaStream_t stream) {
   p.slot = L.su * qmax * (kTileBytes + kTileExps);
   p.slot_planes = L.su * qmax * kTileBytes;
   p.pdl = L.pdl;
+  p.exps_bw = L.exps_bw;
+  p.bw_rows = L.seg[0].N / 8;
+  p.bw_rgb = (L.exps_bw && L.seg[0].N % 128 == 0) ? L.seg[0].N / 128 : 0;
+  if (p.bw_rgb > 0) p.lut_bytes = qmax <= 2 ? kLutSlab : 2 * kLutSlab;
   p.skew = 1;
 #ifdef SHIFTADD_DEV_TRACE
   if (g_dev_variant & 2) p.skew = 0;
 #endif
   cudaLaunchConfig_t c = {};
   c.gridDim = dim3(L.grid);
-  c.blockDim = dim3(L.half ? 9 * 32 : 17 * 32);
-  c.dynamicSmemBytes = stream_smem_bytes(qmax, L.nst, L.su, MW);
+  c.blockDim = dim3((L.half || (L.exps_bw && p.bw_rgb == 0)) ? 9 * 32 : 17 * 32);
+  c.dynamicSmemBytes = p.lut_bytes + L.nst * p.slot + kBarBytes;
   c.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   c.attrs = attr;
   c.numAttrs = L.pdl ? 1 : 0;
+  if (L.exps_bw) {
+    if (MW != 1 || L.nseg != 1) return cudaErrorInvalidValue;
+    // N % 128 == 0: scaled LUTs per (slice, row block); else the per-query scale (8 consumer
+    // warps: room for the 8 q scale registers per lane)
+    if (p.bw_rgb > 0) return cudaLaunchKernelEx(&c, lut_stream_kernel<16, 1, 1, 2>, p);
+    if (L.su != 8) return cudaErrorInvalidValue;
+    return cudaLaunchKernelEx(&c, lut_stream_kernel<8, 1, 1, 1>, p);
+  }
   if (L.half && MW == 1) return cudaLaunchKernelEx(&c, lut_stream_kernel<8, 2, 1>, p);
   switch (MW) {
     case 1: return cudaLaunchKernelEx(&c, lut_stream_kernel<16, 1, 1>, p);

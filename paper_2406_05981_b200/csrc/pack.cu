@@ -101,7 +101,10 @@ __global__ void pack_planes_kernel(const int8_t* __restrict__ signs, const float
         const long long row = (long long)i * N + n;
         const uint2 sv = __ldg(reinterpret_cast<const uint2*>(signs + row * K) + kb);
         uint32_t flip;
-        if (colwise) {
+        if (colwise == 2) {   // NEXT-f1 block-wise: alpha_bw [q][8][K/8], block b = n / (N/8)
+          const float a = __ldg(alpha + ((long long)i * 8 + n / (N / 8)) * KB + kb);
+          flip = (a < 0.f) ? 0xffu : 0u;
+        } else if (colwise) {
           const float* ac = alpha + (long long)i * K + kb * 8;
           flip = 0u;
 #pragma unroll
@@ -245,6 +248,20 @@ cudaError_t launch_pack_colwise(const int8_t* signs, const float* alpha_col, int
                                  : (long long)(K / kTileK) * RG * q * kTileBytes;
   pack_planes_kernel<<<grid_for(nbytes, threads), threads, 0, stream>>>(signs, alpha_col, q, N, K, 8, layout,
                                                                          nbytes, RG, planes, counts, 1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_blockwise(const int8_t* signs, const float* alpha_bw, int q, int N, int K, int layout,
+                                  uint8_t* planes, int8_t* exps_bw, int32_t* counts, cudaStream_t stream) {
+  const int threads = 256;
+  const long long groups = (long long)q * 8 * (K / 8);
+  const bool canon = layout == SHIFTADD_LAYOUT_CANONICAL;
+  const int RG = (N + kTileRows - 1) / kTileRows;
+  pack_exps_kernel<<<grid_for(groups, threads), threads, 0, stream>>>(alpha_bw, groups, exps_bw, counts);
+  const long long nbytes = canon ? (long long)q * N * (K / 8)
+                                 : (long long)(K / kTileK) * RG * q * kTileBytes;
+  pack_planes_kernel<<<grid_for(nbytes, threads), threads, 0, stream>>>(signs, alpha_bw, q, N, K, 8, layout,
+                                                                         nbytes, RG, planes, counts, 2);
   return cudaGetLastError();
 }
 

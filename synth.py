@@ -80,6 +80,23 @@ def gen_layer_colwise(q: int, N: int, K: int, seed: int, device="cpu", std: floa
     return signs, alpha
 
 
+def gen_layer_blockwise(q: int, N: int, K: int, seed: int, device="cpu", std: float = 0.02):
+    """Greedy BCQ with block-wise scales (NEXT-f1 "Ours (Lat.)"): plane i
+    takes b_i = sign(r), alpha_i[b][c] = mean |r| over the N/8 rows of block b and the 8
+    columns of group c, r -= alpha_i b_i.  Returns (signs int8 [q][N][K], alpha fp32 [q][8][K/8])."""
+    gen = _gen(seed, device)
+    r = torch.randn((N, K), generator=gen, device=device, dtype=torch.float32) * std
+    signs = torch.empty((q, N, K), dtype=torch.int8, device=device)
+    alpha = torch.empty((q, 8, K // 8), dtype=torch.float32, device=device)
+    for i in range(q):
+        b = torch.where(r >= 0, 1.0, -1.0)
+        a = r.abs().view(8, N // 8, K // 8, 8).mean(dim=(1, 3))          # [8][K/8]
+        signs[i] = b.to(torch.int8)
+        alpha[i] = a
+        r = r - a.repeat_interleave(N // 8, dim=0).repeat_interleave(8, dim=1) * b
+    return signs, alpha
+
+
 def gen_x(M: int, K: int, seed: int, device="cpu", outlier_scale: float = 20.0):
     """fp16 activations [M][K]: N(0,1) with max(1, K//256) outlier channels x outlier_scale."""
     gen = _gen(seed, device)
