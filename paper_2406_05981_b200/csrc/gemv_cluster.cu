@@ -25,7 +25,6 @@
 // In a cluster a CTA's shared addresses carry its rank in bits 24+ (a rank-0 address used by
 // rank 1 is an illegal instruction -- measured), so the PRMT that forms a lookup address
 // takes byte 3 = rank from the constant registers (see step_sel_c).
-#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -1296,18 +1295,8 @@ cudaError_t launch_m4_q(const GemmArgs& a, const LaunchPlan& p, int C) {
                             a.y, a.ldy, pdl ? kFlagPdl : 0);
 }
 
-int env_int(const char* name, int dflt) {
-  const char* e = std::getenv(name);
-  return e ? std::atoi(e) : dflt;
-}
-int cluster_enabled() {
-  static int v = env_int("SHIFTADD_CLUSTER", 1);
-  return v;
-}
-int cluster_trace() {
-  static int v = env_int("SHIFTADD_CLUSTER_TRACE", 0);
-  return v;
-}
+// The launch choices below are fixed at their measured defaults; the library
+// reads no environment.
 
 // Variants (warps, LUT slots).  HALF: 8 warps x 128 registers and 2 slots (~90 KB of shared
 // memory), so two CTAs share an SM -- when one finishes, a CTA of the next kernel on the
@@ -1323,16 +1312,11 @@ struct ClusterShape {
 
 ClusterShape cluster_shape(int N, int K, int q, bool allow16 = true) {
   (void)N; (void)q;
-  static const int forced_sc = env_int("SHIFTADD_CLUSTER_SC", 0);
-  static const int half = env_int("SHIFTADD_CLUSTER_HALF", 0);
+  (void)allow16;
   const int S = K / kTileK;
-  const int sc = forced_sc > 0 ? (forced_sc > kMaxSc ? kMaxSc : forced_sc) : ((S + 1) / 2 <= kMaxC ? 2 : kMaxSc);
+  const int sc = (S + 1) / 2 <= kMaxC ? 2 : kMaxSc;
   // (S + sc - 1) / sc may exceed the portable 8: clusters of up to 16 are non-portable
-  static const int ring = env_int("SHIFTADD_RING", 1);
-  static const int lut16 = env_int("SHIFTADD_LUT16", 0);
-  if (allow16 && ring && lut16 && !forced_sc && !half && S <= 16)   // fp16-pair LUT: 4 slices per CTA
-    return ClusterShape{kRing16, 4, (S + 3) / 4};
-  const int variant = sc > 2 ? kFull4 : (half ? kHalf : (ring ? kRing : kFull2));
+  const int variant = sc > 2 ? kFull4 : kRing;
   return ClusterShape{variant, sc, (S + sc - 1) / sc};
 }
 
@@ -1426,18 +1410,6 @@ int max_clusters(int variant, int C) {
   return slot;
 }
 
-int x_tma() {
-  static int v = env_int("SHIFTADD_X_TMA", 0);
-  return v;
-}
-int push_end_mode() {
-  static int v = env_int("SHIFTADD_PUSH_END", -1);   // -1: at the end for 4-slot CTAs
-  return v;
-}
-int x_first() {
-  static int v = env_int("SHIFTADD_CLUSTER_XFIRST", 0);
-  return v;
-}
 
 template <int Q, int SCM, int NW, int REGS, bool COLW = false, bool AP2 = false>
 cudaError_t launch_cluster_q(const GemmArgs& a, const LaunchPlan& p, int C) {
@@ -1461,18 +1433,15 @@ cudaError_t launch_cluster_q(const GemmArgs& a, const LaunchPlan& p, int C) {
   c.attrs = attr;
   c.numAttrs = pdl ? 2 : 1;
   unsigned long long* trace = nullptr;
-  if (cluster_trace() && a.workspace && a.workspace_bytes >= kCounterBytes + (size_t)p.grid * 256)
-    trace = reinterpret_cast<unsigned long long*>(static_cast<char*>(a.workspace) + kCounterBytes);
   // ring slots requested before griddepcontrol.wait: ~pre_kb KB per CTA (what HBM delivers
   // to an SM's share during the wait; more only delays x, which queues behind them)
   constexpr int D = COLW ? cl_ring_colw(Q, REGS) : (AP2 ? cl_ring_ap2(Q, REGS) : cl_ring(Q, REGS));
-  static const int pre_kb = env_int("SHIFTADD_PRE_KB", 1024);
+  constexpr int pre_kb = 1024;
   const int slot_bytes = (p.threads / 32) * Q * kTileBytes;
   int pre = (pre_kb * 1024 + slot_bytes / 2) / slot_bytes;
   pre = pre < 0 ? 0 : (pre > D ? D : pre);
-  const int flags = (pdl ? kFlagPdl : 0) | (x_first() ? kFlagXFirst : 0) | (pre << kPreShift) |
-                    (push_end_mode() > 0 || (push_end_mode() < 0 && SCM > 2) ? kFlagPushEnd : 0) |
-                    (x_tma() ? kFlagXTma : 0);
+  // pushes at the end for 4-slot CTAs (measured), in the loop otherwise
+  const int flags = (pdl ? kFlagPdl : 0) | (pre << kPreShift) | (SCM > 2 ? kFlagPushEnd : 0);
   return cudaLaunchKernelEx(&c, gemv_cluster_kernel<Q, SCM, NW, REGS, COLW, AP2>, a.x,
                             reinterpret_cast<const uint4*>(a.planes), a.exps, a.N, S, RG, C, a.y, flags, trace,
                             a.exps2, a.gather);
@@ -1500,8 +1469,6 @@ cudaError_t launch_ring_q(const GemmArgs& a, const LaunchPlan& p, int C) {
   c.attrs = attr;
   c.numAttrs = pdl ? 2 : 1;
   unsigned long long* trace = nullptr;
-  if (cluster_trace() && a.workspace && a.workspace_bytes >= kCounterBytes + (size_t)p.grid * 256)
-    trace = reinterpret_cast<unsigned long long*>(static_cast<char*>(a.workspace) + kCounterBytes);
   return cudaLaunchKernelEx(&c, gemv_cluster_ring_kernel<Q, H16>, a.x, a.planes, a.exps, a.N, S, RG, C, a.y,
                             pdl ? kFlagPdl : 0, trace, a.gather);
 }
@@ -1525,6 +1492,11 @@ __global__ void gather_wait_kernel(const uint32_t* __restrict__ flags, int P, ui
   // flags, and this rank's own flag covers that GEMV's stores), and lets its dependents
   // start at once -- they call griddepcontrol.wait, i.e. wait for this kernel to finish.
   pdl_launch_dependents();
+  // The epoch counter is advanced by the previous gather_wait and read by the GEMV it follows;
+  // under PDL this kernel may start while that GEMV (and, transitively, the previous wait) is
+  // still running, so read it only after griddepcontrol.wait.  (The wait itself is cheap: this
+  // rank's own flag is published at the end of that GEMV anyway.)
+  pdl_wait();
   const int r = threadIdx.x;
   const uint32_t epoch = *epoch_ctr + 1u;
   unsigned long long t0;
@@ -1565,14 +1537,11 @@ constexpr double kBigC = 12.0 * (1 << 20);
 
 bool cluster_applicable(int N, int K, int q, int sms) {
   (void)sms;
-  if (!cluster_enabled()) return false;
   const int S = K / kTileK;
   if (S < 1) return false;
   const ClusterShape cs = cluster_shape(N, K, q);
-  if (cs.C > (cs.sc == 1 || env_int("SHIFTADD_CLUSTER_C16", 1) ? kMaxCColw : kMaxC)) return false;
-  static const double big_c = env_int("SHIFTADD_CLUSTER_BIGC", 0) > 0 ? env_int("SHIFTADD_CLUSTER_BIGC", 0) * 1048576.0
-                                                                       : kBigC;
-  if (cs.variant == kFull4 && cs.C > 4 && (double)q * N * K / 8 > big_c) return false;
+  if (cs.C > kMaxCColw) return false;
+  if (cs.variant == kFull4 && cs.C > 4 && (double)q * N * K / 8 > kBigC) return false;
   const int ncl = max_clusters(cs.variant, cs.C);
   if (ncl <= 0) return false;
   const int RG = (N + kTileRows - 1) / kTileRows;
@@ -1624,9 +1593,8 @@ cudaError_t launch_gemv_colwise(const GemmArgs& a) {
 // §8 a7, M = 2 (kernel id 5): tiled layout, K <= 4096, q <= 3 (a 60 KB ring holds >= 2 stages).
 bool m2_applicable(int N, int K, int q, int sms) {
   (void)sms;
-  static const int on = env_int("SHIFTADD_M2_RING", 1);
   const int S = K / kTileK;
-  if (!on || S < 1 || S > 2 * kMaxC || q < 1 || q > 3) return false;
+  if (S < 1 || S > 2 * kMaxC || q < 1 || q > 3) return false;
   const int C = (S + 1) / 2;
   const int ncl = max_clusters(kRing, C);
   if (ncl <= 0) return false;
@@ -1657,9 +1625,8 @@ cudaError_t launch_gemm_m2(const GemmArgs& a, const LaunchPlan& p) {
 // §8 a7, M = 3..4 (kernel id 6): tiled layout, K <= 4096 (one slice per CTA), q <= 3.
 bool m4_applicable(int N, int K, int q, int sms) {
   (void)sms;
-  static const int on = env_int("SHIFTADD_M4_RING", 1);
   const int S = K / kTileK;
-  if (!on || S < 1 || S > kMaxCColw || q < 1 || q > 3) return false;
+  if (S < 1 || S > kMaxCColw || q < 1 || q > 3) return false;
   const int ncl = max_clusters(kRing, S);
   if (ncl <= 0) return false;
   const int RG = (N + kTileRows - 1) / kTileRows;

@@ -31,7 +31,6 @@
 //    (several threads per row, one round trip), stores fp16 (RNE) and zeroes the counter.
 // PDL: dependents are released at kernel start; the first unit's weights are requested
 //    before griddepcontrol.wait, x after it.
-#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -429,7 +428,6 @@ struct Variant {
   int nw, regs;
 };
 constexpr Variant kVariants[] = {{16, 128}, {8, 128}, {16, 64}, {24, 80}};
-constexpr int kNumVariants = 4;
 
 struct Cfg {
   int variant;     // index into kVariants
@@ -443,26 +441,11 @@ struct Cfg {
   int dyn;           // 1 = dynamic unit claiming inside slice groups (slice-aligned grids)
 };
 
-Cfg config_from_env() {
-  Cfg c{2, 0, 0, 0, 0, 0, 85, 0, 0};
-  if (const char* e = std::getenv("SHIFTADD_DYN")) c.dyn = std::atoi(e) != 0;
-  if (const char* e = std::getenv("SHIFTADD_UNIT_RELEASE")) c.unit_release = std::atoi(e) != 0;
-  if (const char* e = std::getenv("SHIFTADD_ALIGN_MIN")) c.align_min = std::atoi(e);
-  if (const char* e = std::getenv("SHIFTADD_PREBUILD")) c.pre_build = std::atoi(e);
-  if (const char* e = std::getenv("SHIFTADD_PREWAIT")) c.pre_wait = std::atoi(e);
-  if (const char* e = std::getenv("SHIFTADD_NO_ALIGN")) c.no_align = std::atoi(e) != 0;
-  if (const char* e = std::getenv("SHIFTADD_EXP")) c.mode = std::atoi(e);
-  if (const char* e = std::getenv("SHIFTADD_VARIANT")) c.variant = std::atoi(e);
-  if (const char* e = std::getenv("SHIFTADD_PER_SM")) c.per_sm = std::atoi(e) < 0 ? 0 : std::atoi(e);
-  if (c.mode != 3 && c.mode != 4 && c.mode != 5) c.mode = 0;
-  if (c.variant < 0 || c.variant >= kNumVariants) c.variant = 0;
-  return c;
-}
+// Fixed at the measured defaults: variant 2 (16 warps x 64 registers), CTAs per
+// SM by problem size, slice-aligned grids keeping >= 85% of the slots.  No environment is read.
+constexpr Cfg kCfg{2, 0, 0, 0, 0, 0, 85, 0, 0};
 
-const Cfg& cfg() {
-  static Cfg c = config_from_env();
-  return c;
-}
+const Cfg& cfg() { return kCfg; }
 
 constexpr int kDynSmem = kLutBytes + 16;  // 64 KB LUT + the dynamic mode's unit count
 
@@ -501,12 +484,7 @@ cudaError_t launch_k(const GemmArgs& a, const LaunchPlan& p) {
 template <int Q, int V>
 cudaError_t launch_v(const GemmArgs& a, const LaunchPlan& p) {
   constexpr int NW = kVariants[V].nw, REGS = kVariants[V].regs;
-  switch (cfg().mode) {
-    case 3: return launch_k<Q, NW, REGS, 3>(a, p);
-    case 4: return launch_k<Q, NW, REGS, 4>(a, p);
-    case 5: return launch_k<Q, NW, REGS, 5>(a, p);
-    default: return launch_k<Q, NW, REGS, 0>(a, p);
-  }
+  return launch_k<Q, NW, REGS, 0>(a, p);
 }
 
 template <int Q>
@@ -581,7 +559,7 @@ __global__ void __launch_bounds__((kStreamNWC + 1) * 32, 1)
 gemv_stream_kernel(const __half* __restrict__ x, const uint8_t* __restrict__ planes,
                    const int8_t* __restrict__ exps, int N, int S, int RG, long long U,
                    __half* __restrict__ y, float* __restrict__ partial, unsigned* __restrict__ cnt, int pdl,
-                   int npre, int loads_only, unsigned long long* __restrict__ trace, int nown) {
+                   int npre, unsigned long long* __restrict__ trace, int nown) {
   using SM = StreamSmem<Q>;
   unsigned long long* tr = trace ? trace + 16 * blockIdx.x : nullptr;   // dev trace
   if (tr && threadIdx.x == 0) tr[0] = gtimer();
@@ -666,8 +644,7 @@ gemv_stream_kernel(const __half* __restrict__ x, const uint8_t* __restrict__ pla
 #pragma unroll
         for (int i = 0; i < Q; ++i) e[i] = lds_s8(se + i * kTileExps);
         const int s = (int)((unsigned)u / (unsigned)RG);
-        const float acc = loads_only ? unit_xor<Q>(w, e)   // experiment: the ring without lookups
-                                     : s == s_first ? unit_dot<Q, 0, 0u>(w, e, cst) : unit_dot<Q, 0, 128u>(w, e, cst);
+        const float acc = s == s_first ? unit_dot<Q, 0, 0u>(w, e, cst) : unit_dot<Q, 0, 128u>(w, e, cst);
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + 8 * j);   // the unit's bytes are consumed
         c.rg_base = (long long)s * RG;
@@ -746,28 +723,9 @@ cudaError_t launch_stream_q(const GemmArgs& a, const LaunchPlan& p) {
   unsigned* sync = reinterpret_cast<unsigned*>(a.workspace);
   float* partial = reinterpret_cast<float*>(reinterpret_cast<char*>(a.workspace) + kCounterBytes);
   const int pdl = (a.flags & SHIFTADD_FLAG_PDL) ? 1 : 0;
-  static const int npre = [] {
-    const char* e = std::getenv("SHIFTADD_STREAM_PRE");
-    return e ? std::atoi(e) : 1;
-  }();
-  // dev trace (SHIFTADD_STREAM_TRACE=1): 16 words per CTA after the partials
-  static const int trace_on = [] {
-    const char* e = std::getenv("SHIFTADD_STREAM_TRACE");
-    return e ? std::atoi(e) : 0;
-  }();
+  constexpr int npre = 1;   // stages requested before griddepcontrol.wait (measured best)
   unsigned long long* trace = nullptr;
-  const size_t part_bytes = (size_t)S * RG * kTileRows * sizeof(float);
-  if (trace_on && a.workspace_bytes >= kCounterBytes + part_bytes + (size_t)p.grid * 128)
-    trace = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(a.workspace) + kCounterBytes + part_bytes);
-  static const int owners = [] {
-    const char* e = std::getenv("SHIFTADD_STREAM_OWNERS");
-    return e ? std::atoi(e) : 0;
-  }();
-  const int nown = owners > 0 && owners < p.grid ? owners : p.grid;
-  static const int loads_only = [] {
-    const char* e = std::getenv("SHIFTADD_STREAM_LOADS_ONLY");
-    return e ? std::atoi(e) : 0;
-  }();
+  const int nown = p.grid;
   cudaLaunchConfig_t c = {};
   c.gridDim = dim3(p.grid);
   c.blockDim = dim3(p.threads);
@@ -779,7 +737,7 @@ cudaError_t launch_stream_q(const GemmArgs& a, const LaunchPlan& p) {
   c.attrs = attr;
   c.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&c, gemv_stream_kernel<Q>, a.x, a.planes, a.exps, a.N, S, RG, U, a.y, partial, sync,
-                            pdl, npre, loads_only, trace, nown);
+                            pdl, npre, trace, nown);
 }
 
 int stream_smem(int q) {
@@ -817,11 +775,7 @@ LaunchPlan plan_gemv_tiled(int N, int K, int q, int sms) {
 // Large layers (more than ~64 units per SM, chunks within two slices) stream through the
 // TMA ring (kernel 4); SHIFTADD_STREAM=0 keeps them on the register-ring kernel.
 bool stream_applicable(int N, int K, int q, int sms) {
-  static const int on = [] {
-    const char* e = std::getenv("SHIFTADD_STREAM");
-    return e ? std::atoi(e) : 1;
-  }();
-  if (!on || q < 1 || q > 4) return false;
+  if (q < 1 || q > 4) return false;
   const long long S = K / kTileK;
   const long long RG = (N + kTileRows - 1) / kTileRows;
   return S > 1 && S < sms && S * RG >= 64LL * sms;

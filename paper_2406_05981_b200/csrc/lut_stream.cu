@@ -39,7 +39,6 @@
 namespace shiftadd {
 namespace {
 
-constexpr int kNWCMax = 16;                  // consumer warps (16, or 8 in the co-resident variant)
 constexpr int kLutSlab = kLutBytes;          // 64 KB: two slices' LUTs (column halves)
 constexpr int kBarBytes = 512;               // full[16] at +0, empty[16] at +128, epoch at +256
 
@@ -1037,9 +1036,14 @@ bool stream_shape_ok(int K, int sms) {
 }
 
 cudaError_t launch_lut_stream(const StreamLaunch& L, cudaStream_t stream) {
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
+  // kernel attributes are per device: set them once on each device that launches
+  static std::once_flag once[64];
+  static cudaError_t attr_err[64];
+  int dev = 0;
+  cudaError_t de = cudaGetDevice(&dev);
+  if (de != cudaSuccess) return de;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  std::call_once(once[dev], [dev] {
     const int big = 227 * 1024;
     cudaError_t e = cudaFuncSetAttribute(lut_stream_kernel<16, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(lut_stream_kernel<16, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
@@ -1051,8 +1055,9 @@ cudaError_t launch_lut_stream(const StreamLaunch& L, cudaStream_t stream) {
       e = cudaFuncSetAttribute(lut_stream_kernel<16, 1, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(lut_stream_kernel<8, 2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 113 * 1024);
-    attr_err = e;
+    attr_err[dev] = e;
   });
+  if (attr_err[dev] != cudaSuccess) return attr_err[dev];
   if (L.nseg < 1 || L.nseg > kMaxSegments || L.nst < 1 || L.nst > 16 || (L.su != 8 && L.su != 16))
     return cudaErrorInvalidValue;
   StreamParams p = {};

@@ -51,13 +51,13 @@ def launches(path, tag):
         per[name][0] += 1
         per[name][1] += v
     tot = sum(v[1] for v in per.values()) or 1.0
-    out = ["# %s -- ncu launch list of `python bench.py --steps 4 --warmup 3 --no-cpu-baseline`" % tag, "",
+    out = ["# %s -- ncu launch list of `python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-layers`" % tag, "",
            "Cold-cache, serialised per-launch times (`--metrics gpu__time_duration.sum --clock-control none`):",
            "compare SHARES, not absolutes.  The list covers the whole process: layer synthesis (torch",
            "RNG/elementwise kernels) and packing (`pack_*`, one-time per layer) precede the timed region;",
-           "a bench step launches only the LUT-GEMV kernel (`gemv_cluster_ring_kernel` for the K = 4096",
-           "bench layers; `gemv_tiled_kernel` is the grid split-K kernel), one per layer, so within",
-           "the step the LUT-GEMV is 100% of device time.", "",
+           "a decode step launches only LUT-GEMV kernels -- `lut_stream_kernel` (q/k/v fused, gate/up fused",
+           "where the bit widths differ, down_proj) and `gemv_cluster_ring_kernel` (o_proj, gate/up",
+           "concatenated) -- plus the e2e leg's `copy_kernel`.", "",
            "| kernel | launches | total us | share of whole process |", "|---|---|---|---|"]
     for name, (n, us) in sorted(per.items(), key=lambda kv: -kv[1][1]):
         out.append("| `%s` | %d | %.1f | %.1f%% |" % (name, n, us, 100 * us / tot))
@@ -102,17 +102,28 @@ if __name__ == "__main__":
     tag = sys.argv[1]
     os.makedirs(PROF, exist_ok=True)
     launches(sys.argv[2], tag)
-    traffic = []
+    # dram traffic per launch of every captured kernel, keyed by kernel id (bench.py's
+    # roofline.traffic reads the dominant kernel's entry)
+    ids = {"lut_stream_kernel": 8, "gemv_cluster_ring_kernel": 3}
+    per_kernel = defaultdict(list)
     for rep in sys.argv[3:]:
-        ms = report(rep, tag)
-        for m in ms:
-            if "dram__bytes_read.sum" in m:
-                t = to_bytes(*m["dram__bytes_read.sum"]) + to_bytes(*m.get("dram__bytes_write.sum", ("0", "byte")))
-                traffic.append(t)
-    if traffic:
-        with open(os.path.join(PROF, "ncu_traffic.json"), "w") as f:
-            json.dump({"round": tag, "per_launch_bytes": traffic,
-                       "traffic_bytes_per_launch_avg": sum(traffic) / len(traffic),
-                       "note": "dram__bytes_read.sum + dram__bytes_write.sum per launch of the full capture(s); "
-                               "the bench step's 4 layers (attn q2, attn q3, fc1 q2, fc1 q3) in order"}, f, indent=1)
-    print("ok", tag, traffic)
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rows = list(csv.reader(io.StringIO(raw)))
+        hdr, units = rows[0], rows[1]
+        report(rep, tag)
+        for vals in rows[2:]:
+            kname = vals[hdr.index("Kernel Name")]
+            kid = next((v for k, v in ids.items() if k in kname), None)
+            if kid is None or "dram__bytes_read.sum" not in hdr:
+                continue
+            ir, iw = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
+            t = to_bytes(vals[ir], units[ir]) + to_bytes(vals[iw], units[iw])
+            per_kernel[str(kid)].append(t)
+    out = {"round": tag, "kernels": {k: sum(v) / len(v) for k, v in per_kernel.items()},
+           "per_launch_bytes": dict(per_kernel),
+           "note": "dram__bytes_read.sum + dram__bytes_write.sum per launch of the full captures (tools/evidence.sh): "
+                   "kernel 8 = block 0 q/k/v fused, block 0 down_proj, block 1 q/k/v fused; kernel 3 = block 0 "
+                   "o_proj, block 0 gate/up concatenated"}
+    with open(os.path.join(PROF, "ncu_traffic.json"), "w") as f:
+        json.dump(out, f, indent=1)
+    print("ok", tag, out["kernels"])
