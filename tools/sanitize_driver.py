@@ -1,0 +1,73 @@
+"""One small call of every device path, for compute-sanitizer (tests/test_gpu_sanitizers.py).
+Exits non-zero if any result misses the oracle bar, so a sanitizer run also checks results."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import oracle  # noqa: E402
+import paper_2406_05981_b200 as sa  # noqa: E402
+import synth  # noqa: E402
+
+dev = torch.device("cuda:0")
+bad = []
+
+
+def check(name, y, ref):
+    err = oracle.err_floor(y.float().cpu().numpy().reshape(ref.shape), ref)
+    if not err <= 2e-3:
+        bad.append((name, err))
+
+
+def rowwise(q, N, K, M, **kw):
+    s, a = synth.gen_layer(q, N, K, 128, seed=synth.seed_for(12, N, K))
+    p, e, _ = oracle.pack_canonical(s.numpy(), a.numpy(), 128)
+    L = sa.pack(s.to(dev), a.to(dev), 128, layout=sa.LAYOUT_TILED)
+    x = synth.gen_x(M, K, seed=M)
+    y = sa.lut_gemm(x.to(dev), L, pdl=True, **kw)
+    torch.cuda.synchronize()
+    check("rowwise q%d N%d K%d M%d %s %s" % (q, N, K, M, kw, sa.gemm_plan(L, M)), y, oracle.gemm(x.numpy(), p, e, 128))
+
+
+rowwise(3, 256, 1024, 1)                      # cluster kernel (3)
+rowwise(3, 272, 1024, 1, splitk=True)         # streaming kernel (8), straddling chunks
+rowwise(2, 64, 256, 1, splitk=True)           # streaming, S = 1
+rowwise(3, 272, 1024, 2)                      # cluster ring M = 2 (5)
+rowwise(3, 272, 1024, 3)                      # cluster ring M = 3..4 (6)
+for M in (2, 4, 8, 12):                       # streaming MW = 2, 4, 8 and two row chunks
+    rowwise(2, 200, 1024, M, splitk=True)
+# fused segments
+K = 1024
+x = synth.gen_x(1, K, seed=3)
+cases = []
+for i, (q, N) in enumerate([(2, 96), (3, 40), (1, 33)]):
+    s, a = synth.gen_layer(q, N, K, 128, seed=synth.seed_for(12, 50 + i))
+    p, e, _ = oracle.pack_canonical(s.numpy(), a.numpy(), 128)
+    cases.append((sa.pack(s.to(dev), a.to(dev), 128, layout=sa.LAYOUT_TILED), p, e))
+ys = sa.lut_gemv_fused(x.to(dev), [c[0] for c in cases], pdl=True)
+torch.cuda.synchronize()
+for (L, p, e), y in zip(cases, ys):
+    check("fused", y, oracle.gemm(x.numpy(), p, e, 128))
+# block-wise: scaled LUTs (N % 128 == 0) and per-query scales
+for N in (256, 40):
+    s, a = synth.gen_layer_blockwise(2, N, 1024, seed=synth.seed_for(12, 60, N))
+    p, e, _ = oracle.pack_blockwise(s.numpy(), a.numpy())
+    L = sa.pack_blockwise(s.to(dev), a.to(dev))
+    xb = synth.gen_x(1, 1024, seed=4)
+    y = sa.lut_gemv_blockwise(xb.to(dev), L, pdl=True)
+    torch.cuda.synchronize()
+    check("blockwise N%d" % N, y, oracle.gemm_blockwise(xb.numpy(), p, e))
+# canonical layout (generic kernel)
+s, a = synth.gen_layer(2, 64, 512, 64, seed=5)
+p, e, _ = oracle.pack_canonical(s.numpy(), a.numpy(), 64)
+L = sa.pack(s.to(dev), a.to(dev), 64, layout=sa.LAYOUT_CANONICAL)
+xc = synth.gen_x(3, 512, seed=6)
+y = sa.lut_gemm(xc.to(dev), L)
+torch.cuda.synchronize()
+check("canonical", y, oracle.gemm(xc.numpy(), p, e, 64))
+if bad:
+    print("PARITY FAILURES", bad)
+    sys.exit(3)
+print("sanitize driver ok")
