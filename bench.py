@@ -415,15 +415,27 @@ def main():
         return run_reference(args)
 
     import paper_2406_05981_b200 as sa
+    from paper_2406_05981_b200 import dist as sdist
     ws_size, rank, local = dist_env()
     if ws_size != args.gpus:
         raise SystemExit("--gpus %d but WORLD_SIZE %d" % (args.gpus, ws_size))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    ndev = torch.cuda.device_count()
+    if ws_size > ndev and not args.dry_run:
+        raise SystemExit("--gpus %d needs %d visible GPUs (%d visible); --dry-run shares them" % (ws_size, ws_size, ndev))
+    local_dev = local % ndev
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     group = None
+    backend = None
     if ws_size > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        # one GPU per rank over NCCL; a dry run with fewer GPUs than ranks (the test boxes have
+        # one) shares them and gathers through the host over gloo
+        backend = "nccl" if ws_size <= ndev else "gloo"
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
         group = dist.group.WORLD
     sa.lib()
     stream = torch.cuda.Stream(dev)
@@ -448,7 +460,10 @@ def main():
             Lc(wsp, True)
             if group is not None:
                 for o, gbuf in zip(Lc.outs, gathered[li]):
-                    torch.distributed.all_gather_into_tensor(gbuf, o, group=group)
+                    if backend == "gloo":
+                        sdist.gather_output(o.view(1, -1), group, out=gbuf.view(1, -1))
+                    else:
+                        torch.distributed.all_gather_into_tensor(gbuf, o, group=group)
 
     with torch.cuda.stream(stream):
         for _ in range(2):
@@ -469,10 +484,10 @@ def main():
 
     def barrier():
         if group is not None:
-            torch.distributed.barrier(device_ids=[local])
+            torch.distributed.barrier(device_ids=[local_dev])
         torch.cuda.synchronize(dev)
 
-    with ClockSampler(local) as clk:
+    with ClockSampler(local_dev) as clk:
         with torch.cuda.stream(stream):
             for _ in range(args.warmup):
                 g_step.replay()

@@ -38,6 +38,14 @@ def gather_output(y_local: torch.Tensor, group=None, out: torch.Tensor | None = 
     M, n = y_local.shape
     if world == 1:
         return y_local
+    if y_local.is_cuda and dist.get_backend(group) == "gloo":
+        # gloo moves host tensors only: stage through the host (several ranks sharing one GPU
+        # in tests, or a CPU-only process group) -- the collective's plumbing, not the compute
+        y_host = gather_output(y_local.cpu(), group)
+        if out is not None:
+            out.copy_(y_host.view(out.shape))
+            return out
+        return y_host.to(y_local.device)
     if M == 1:
         flat = out.view(-1) if out is not None else torch.empty(world * n, dtype=y_local.dtype,
                                                                 device=y_local.device)
