@@ -151,6 +151,44 @@ shiftadd_status shiftadd_lut_gemv_fused(const uint16_t* x, int K, int g, int lay
                                         const shiftadd_segment* segs, void* workspace, size_t workspace_bytes,
                                         unsigned flags, void* stream);
 
+/* A decode step as ONE persistent launch (§8 a2-a6 over a whole model; kernel id 9): an
+ * ordered "program" of batch-1 calls of the shiftadd_lut_gemv_fused form -- in a decoder,
+ * per block q/k/v, o, gate/up, down (PAPER.md:286-292 gives each layer its own q).  One CTA
+ * per SM runs the calls in order; its producer warp streams the weights of call after call
+ * into shared memory (weights never depend on activations), so HBM stays busy across call
+ * boundaries, and the consumer warps build each call's LUTs, query, reduce and store y.
+ * Call j computes, for every segment i, exactly what shiftadd_lut_gemv_fused computes:
+ *   y_i[n] = fp16_rne( sum_j sum_G 2^{e_i[j][n][G]} sum_{k in G} s_i(j,n,k) x[k] ).
+ * SHIFTADD_CALL_WAIT in a call's flags: x is read only after every earlier call of the
+ * program has stored all of its y (the call consumes earlier outputs -- e.g. x of call j is
+ * y of call j-1); without it, x must not be written by the program.  Outputs of different
+ * calls must not overlap.
+ * Usage: shiftadd_program_encode(calls) writes shiftadd_program_bytes(ncalls) bytes into a
+ * caller HOST buffer; the caller copies them to DEVICE memory once (they hold the device
+ * pointers of the calls, not the data); shiftadd_lut_gemv_program(calls, program, ...) then
+ * launches with the same calls (validated again on the host; the kernel traps if the device
+ * copy is not the encoding of these calls).
+ * Per call: x fp16 [K] 16-B aligned, K % 256 == 0, 256 <= K <= 256 x #SMs, g % 128 == 0,
+ * g | K, 1 <= nseg <= 4, each segment as in shiftadd_lut_gemv_fused (tiled layout).
+ * Workspace: shiftadd_workspace_bytes_program(calls) bytes, zeroed once before first use,
+ * used by program launches only (not shared with other entry points), one launch at a time.
+ * flags: 0.  The launch is cooperative (one CTA per SM, all co-resident). */
+#define SHIFTADD_CALL_WAIT 1u
+typedef struct {
+  const uint16_t* x;     /* fp16 [K] activations of this call                 */
+  int K;                 /* reduction length                                   */
+  int g;                 /* scale group of every segment (multiple of 128)     */
+  int nseg;              /* output segments sharing x (1..4)                   */
+  unsigned flags;        /* 0 or SHIFTADD_CALL_WAIT                            */
+  shiftadd_segment seg[4];
+} shiftadd_call;
+size_t shiftadd_program_bytes(int ncalls);
+shiftadd_status shiftadd_program_encode(const shiftadd_call* calls, int ncalls, void* out, size_t out_bytes);
+size_t shiftadd_workspace_bytes_program(const shiftadd_call* calls, int ncalls);
+shiftadd_status shiftadd_lut_gemv_program(const shiftadd_call* calls, int ncalls, const void* program,
+                                          size_t program_bytes, void* workspace, size_t workspace_bytes,
+                                          unsigned flags, void* stream);
+
 /* Batch-1 convenience: shiftadd_lut_gemm with M = 1, ldx = K, ldy = N. */
 shiftadd_status shiftadd_lut_gemv(const uint16_t* x, const uint8_t* planes, const int8_t* exps,
                                   int layout, int N, int K, int q, int g, uint16_t* y,

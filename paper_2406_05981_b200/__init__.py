@@ -23,7 +23,7 @@ __all__ = [
     "LAYOUT_CANONICAL", "LAYOUT_TILED", "FLAG_PDL", "FLAG_SPLITK", "EXP_ZERO", "ShiftAddError", "lib",
     "PackedLayer", "packed_bytes", "pack", "lut_gemm", "lut_gemv", "workspace_bytes",
     "gemm_plan", "Workspace", "pack_colwise", "lut_gemv_colwise", "pack_apot2", "bcq_quantize",
-    "lut_gemv_fused", "workspace_bytes_fused", "pack_blockwise", "lut_gemv_blockwise",
+    "lut_gemv_fused", "workspace_bytes_fused", "pack_blockwise", "lut_gemv_blockwise", "Program", "CALL_WAIT",
 ]
 
 LAYOUT_CANONICAL = 0
@@ -47,6 +47,12 @@ class _Segment(ctypes.Structure):
     """shiftadd_segment (include/shiftadd.h)."""
     _fields_ = [("planes", ctypes.c_void_p), ("exps", ctypes.c_void_p), ("N", ctypes.c_int), ("q", ctypes.c_int),
                 ("y", ctypes.c_void_p)]
+
+
+class _Call(ctypes.Structure):
+    """shiftadd_call (include/shiftadd.h)."""
+    _fields_ = [("x", ctypes.c_void_p), ("K", ctypes.c_int), ("g", ctypes.c_int), ("nseg", ctypes.c_int),
+                ("flags", ctypes.c_uint), ("seg", _Segment * 4)]
 
 
 def lib():
@@ -109,6 +115,15 @@ def lib():
         L.shiftadd_lut_gemv_blockwise.restype = c_int
         L.shiftadd_lut_gemv_blockwise.argtypes = [vp, vp, vp, c_int, c_int, c_int, c_int, vp, vp, c_size,
                                                   ctypes.c_uint, vp]
+        L.shiftadd_program_bytes.restype = c_size
+        L.shiftadd_program_bytes.argtypes = [c_int]
+        L.shiftadd_program_encode.restype = c_int
+        L.shiftadd_program_encode.argtypes = [ctypes.POINTER(_Call), c_int, vp, c_size]
+        L.shiftadd_workspace_bytes_program.restype = c_size
+        L.shiftadd_workspace_bytes_program.argtypes = [ctypes.POINTER(_Call), c_int]
+        L.shiftadd_lut_gemv_program.restype = c_int
+        L.shiftadd_lut_gemv_program.argtypes = [ctypes.POINTER(_Call), c_int, vp, c_size, vp, c_size,
+                                                ctypes.c_uint, vp]
         L.shiftadd_gemm_plan.restype = c_int
         L.shiftadd_gemm_plan.argtypes = [c_int] * 6 + [ctypes.POINTER(c_int * 4)]
         v = L.shiftadd_abi_version()
@@ -490,6 +505,59 @@ def lut_gemv_fused(x: torch.Tensor, layers, outs=None, workspace: Workspace | No
 def lut_gemv(x: torch.Tensor, layer: PackedLayer, **kw) -> torch.Tensor:
     """Batch-1 form: x fp16 [K] -> y fp16 [N]."""
     return lut_gemm(x.reshape(-1), layer, **kw)
+
+
+CALL_WAIT = 1
+
+
+class Program:
+    """A decode step as one persistent launch (shiftadd_lut_gemv_program, kernel id 9).
+
+    calls: list of (x, layers, outs, wait) in execution order -- x fp16 [K] on the device,
+    layers: 1..4 tiled PackedLayers sharing x (same K and g), outs: their fp16 [N_i] outputs,
+    wait: x is read only after every earlier call stored its outputs (SHIFTADD_CALL_WAIT).
+    The encoded program (device pointers of the calls) is copied to the device once here; the
+    tensors must stay alive and in place while the Program is used.  The workspace is owned by
+    the Program (program launches do not share it with other calls)."""
+
+    def __init__(self, calls, device=None):
+        if not calls:
+            raise ValueError("empty program")
+        self.device = torch.device(device) if device is not None else calls[0][1][0].device
+        arr = (_Call * len(calls))()
+        self._keep = []
+        for j, (x, layers, outs, wait) in enumerate(calls):
+            x = x.reshape(-1)
+            if x.dtype != torch.float16 or not x.is_cuda or not 1 <= len(layers) <= 4 or len(outs) != len(layers):
+                raise ValueError("call %d: fp16 x on the device and 1..4 segments with outputs" % j)
+            for L, y in zip(layers, outs):
+                if L.K != x.numel() or L.g != layers[0].g or L.layout != LAYOUT_TILED or L.colwise or \
+                        L.exps2 is not None:
+                    raise ValueError("call %d: tiled row-wise layers with the K and g of x" % j)
+                if y.dtype != torch.float16 or y.numel() != L.N or not y.is_contiguous():
+                    raise ValueError("call %d: outputs must be contiguous fp16 [N_i]" % j)
+            c = arr[j]
+            c.x, c.K, c.g, c.nseg, c.flags = x.data_ptr(), x.numel(), layers[0].g, len(layers), CALL_WAIT if wait else 0
+            for i, (L, y) in enumerate(zip(layers, outs)):
+                c.seg[i] = _Segment(L.planes.data_ptr(), L.exps.data_ptr(), L.N, L.q, y.data_ptr())
+            self._keep.append((x, layers, outs))
+        self.calls, self.n = arr, len(calls)
+        nb = int(lib().shiftadd_program_bytes(self.n))
+        host = torch.empty(nb, dtype=torch.uint8).pin_memory()
+        _check(lib().shiftadd_program_encode(arr, self.n, host.data_ptr(), nb), "shiftadd_program_encode")
+        self.program = host.to(self.device)
+        need = int(lib().shiftadd_workspace_bytes_program(arr, self.n))
+        if need == 0:
+            raise ShiftAddError("shiftadd_workspace_bytes_program: " + lib().shiftadd_last_error().decode())
+        self.workspace = torch.zeros(need, dtype=torch.uint8, device=self.device)
+
+    def __call__(self, stream=None):
+        if torch.cuda.current_device() != self.device.index:
+            torch.cuda.set_device(self.device)
+        sptr = (stream if stream is not None else torch.cuda.current_stream(self.device)).cuda_stream
+        _check(lib().shiftadd_lut_gemv_program(self.calls, self.n, self.program.data_ptr(), self.program.numel(),
+                                               self.workspace.data_ptr(), self.workspace.numel(), 0, sptr),
+               "shiftadd_lut_gemv_program")
 
 
 COPY_SRC_READY = 4

@@ -3,6 +3,7 @@
 // Synchronous argument validation (nothing is launched on failure), device checks, the
 // mixed-bit dispatch of §8 a6 (q -> template instance, host side, no device cost) and the
 // layout/batch dispatch between the kernels.  No exceptions cross the boundary.
+#include <vector>
 #include <cstdarg>
 #include <cstdio>
 #include <mutex>
@@ -449,6 +450,8 @@ shiftadd_status shiftadd_copy(void* dst, const void* src, size_t bytes, unsigned
 // development builds only: per-CTA phase timestamps of the streaming kernel into `buf`
 // (16 u64 per CTA), NULL to stop
 int shiftadd_dev_set_trace(void* buf) { return (int)dev_set_trace(buf); }
+int shiftadd_dev_set_program_trace(void* buf) { return (int)dev_set_program_trace(buf); }
+int shiftadd_dev_set_program_variant(int v) { return (int)dev_set_program_variant(v); }
 void shiftadd_dev_set_variant(int v) { dev_set_variant(v); }
 #endif
 
@@ -634,6 +637,96 @@ shiftadd_status shiftadd_lut_gemv_fused(const uint16_t* x, int K, int g, int lay
 #endif
   const cudaError_t e = launch_lut_stream(L, reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "lut_gemv_fused launch");
+  return SHIFTADD_OK;
+}
+
+// ------------------------------------------------------------------ decode program (kernel 9)
+size_t shiftadd_program_bytes(int ncalls) { return ncalls < 1 ? 0 : program_bytes(ncalls); }
+
+namespace {
+shiftadd_status check_program(const shiftadd_call* calls, int ncalls, std::vector<ProgramCallDesc>* out,
+                              int* qmax, size_t* part_max) {
+  if (!calls || ncalls < 1) return fail(SHIFTADD_ERR_INVALID, "need ncalls >= 1 and a call array");
+  out->resize(ncalls);
+  *qmax = 1;
+  *part_max = 0;
+  shiftadd_status st;
+  for (int j = 0; j < ncalls; ++j) {
+    const shiftadd_call& c = calls[j];
+    if (!c.x) return fail(SHIFTADD_ERR_INVALID, "call %d: null x", j);
+    if (!aligned(c.x, 16)) return fail(SHIFTADD_ERR_INVALID, "call %d: x must be 16-B aligned", j);
+    if (c.nseg < 1 || c.nseg > kMaxSegments)
+      return fail(SHIFTADD_ERR_INVALID, "call %d: nseg=%d outside [1, %d]", j, c.nseg, kMaxSegments);
+    if (c.flags & ~SHIFTADD_CALL_WAIT) return fail(SHIFTADD_ERR_INVALID, "call %d: unknown flags 0x%x", j, c.flags);
+    ProgramCallDesc& d = (*out)[j];
+    d.x = reinterpret_cast<const __half*>(c.x);
+    d.K = c.K;
+    d.nseg = c.nseg;
+    d.wait = (c.flags & SHIFTADD_CALL_WAIT) ? 1 : 0;
+    int rg = 0;
+    for (int i = 0; i < c.nseg; ++i) {
+      const shiftadd_segment& sg = c.seg[i];
+      if (!sg.planes || !sg.exps || !sg.y) return fail(SHIFTADD_ERR_INVALID, "call %d segment %d: null pointer", j, i);
+      if ((st = check_shape(sg.q, sg.N, c.K, c.g, 4)) != SHIFTADD_OK) return st;
+      if (!aligned(sg.planes, 16) || !aligned(sg.exps, 16) || !aligned(sg.y, 2))
+        return fail(SHIFTADD_ERR_INVALID, "call %d segment %d: planes / exps must be 16-B aligned", j, i);
+      d.seg[i] = StreamSeg{sg.planes, sg.exps, reinterpret_cast<__half*>(sg.y), sg.q, sg.N};
+      *qmax = sg.q > *qmax ? sg.q : *qmax;
+      rg += (sg.N + kTileRows - 1) / kTileRows;
+    }
+    if ((st = check_layout(SHIFTADD_LAYOUT_TILED, c.K, c.g)) != SHIFTADD_OK) return st;
+    const size_t pb = program_part_bytes(c.K / kTileK, rg);
+    *part_max = pb > *part_max ? pb : *part_max;
+  }
+  return SHIFTADD_OK;
+}
+}  // namespace
+
+shiftadd_status shiftadd_program_encode(const shiftadd_call* calls, int ncalls, void* out, size_t out_bytes) {
+  std::vector<ProgramCallDesc> d;
+  int qmax;
+  size_t part_max;
+  const shiftadd_status st = check_program(calls, ncalls, &d, &qmax, &part_max);
+  if (st != SHIFTADD_OK) return st;
+  if (!out || out_bytes < program_bytes(ncalls) || !aligned(out, 8))
+    return fail(SHIFTADD_ERR_INVALID, "program buffer needs %zu bytes, 8-B aligned", program_bytes(ncalls));
+  program_encode(d.data(), ncalls, out);
+  return SHIFTADD_OK;
+}
+
+size_t shiftadd_workspace_bytes_program(const shiftadd_call* calls, int ncalls) {
+  std::vector<ProgramCallDesc> d;
+  int qmax;
+  size_t part_max;
+  if (check_program(calls, ncalls, &d, &qmax, &part_max) != SHIFTADD_OK) return 0;
+  return program_workspace_bytes(part_max);
+}
+
+shiftadd_status shiftadd_lut_gemv_program(const shiftadd_call* calls, int ncalls, const void* program,
+                                          size_t program_bytes_, void* workspace, size_t workspace_bytes,
+                                          unsigned flags, void* stream) {
+  std::vector<ProgramCallDesc> d;
+  int qmax;
+  size_t part_max;
+  shiftadd_status st = check_program(calls, ncalls, &d, &qmax, &part_max);
+  if (st != SHIFTADD_OK) return st;
+  if (flags) return fail(SHIFTADD_ERR_INVALID, "unknown flags 0x%x", flags);
+  if (!program || program_bytes_ < program_bytes(ncalls) || !aligned(program, 16))
+    return fail(SHIFTADD_ERR_INVALID, "program needs %zu device bytes, 16-B aligned", program_bytes(ncalls));
+  const size_t need = program_workspace_bytes(part_max);
+  if (!workspace || workspace_bytes < need || !aligned(workspace, 256))
+    return fail(SHIFTADD_ERR_INVALID, "workspace needs %zu bytes, 256-B aligned (got %zu)", need, workspace_bytes);
+  DevInfo di;
+  if ((st = device_info(&di)) != SHIFTADD_OK) return st;
+  for (int j = 0; j < ncalls; ++j)
+    if (!stream_shape_ok(d[j].K, di.sms))
+      return fail(SHIFTADD_ERR_UNSUPPORTED, "call %d: K=%d above 256 x %d SMs", j, d[j].K, di.sms);
+  thread_local std::vector<unsigned char> enc;
+  enc.resize(program_bytes(ncalls));
+  const uint64_t hash = program_encode(d.data(), ncalls, enc.data());
+  const cudaError_t e = launch_lut_program(program, ncalls, hash, qmax, part_max, workspace, di.sms,
+                                           reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "lut_gemv_program launch");
   return SHIFTADD_OK;
 }
 

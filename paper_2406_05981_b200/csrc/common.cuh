@@ -223,6 +223,19 @@ struct StreamLaunch {
   const int8_t* exps_bw;   // non-null: NEXT-f1 block-wise exponents [q][8][K/8] (M = 1, one segment)
 };
 
+// The persistent decode program (lut_program.cu, kernel id 9): ordered calls of the fused form.
+struct ProgramCallDesc {
+  const __half* x;
+  int K, nseg, wait;
+  StreamSeg seg[kMaxSegments];
+};
+size_t program_bytes(int ncalls);
+size_t program_part_bytes(int S, int RGtot);
+size_t program_workspace_bytes(size_t part_max);
+uint64_t program_encode(const ProgramCallDesc* calls, int ncalls, void* out);
+cudaError_t launch_lut_program(const void* program, int ncalls, uint64_t hash, int qmax, size_t part_max,
+                               void* workspace, int sms, cudaStream_t stream);
+
 struct LaunchPlan {
   int grid;
   int threads;
@@ -282,6 +295,8 @@ bool stream_shape_ok(int K, int sms);
 cudaError_t launch_lut_stream(const StreamLaunch& L, cudaStream_t stream);
 #ifdef SHIFTADD_DEV_TRACE
 cudaError_t dev_set_trace(void* buf);
+cudaError_t dev_set_program_trace(void* buf);
+cudaError_t dev_set_program_variant(int v);
 extern int g_dev_variant;
 void dev_set_variant(int v);
 #endif

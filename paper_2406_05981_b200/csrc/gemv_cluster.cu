@@ -690,6 +690,10 @@ gemv_cluster_ring_kernel(const __half* __restrict__ x, const uint8_t* __restrict
       }
     }
   } else {
+    // x into L2 before the PDL wait (a hint: L2 is the point of coherence and x is read after
+    // the wait), so a cold x costs no miss on the call's dependent chain
+    if (tid < Sc * 4)
+      asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(x + (size_t)s0 * kTileK + 64 * tid));
     if (pdl) pdl_wait();
     if (tr && tid == 0) tr[8] = gtimer_ns();
     if (tid < Sc * (kTileK / 8)) {   // one 16-B chunk of x per thread

@@ -185,3 +185,44 @@ def test_copy_validation_happens_before_any_launch(L):
     assert L.shiftadd_copy(q, p, 256, 0, None) == 2             # misaligned
     assert L.shiftadd_copy(p, p, 256, 8, None) == 2             # unknown flag
     assert L.shiftadd_copy(p, p, 256, 1 | 4, None) == 7         # valid: no GPU here
+
+
+def test_program_encode_and_validation_happen_on_the_host(L):
+    """Decode program (kernel 9): encoding is host-only (no GPU needed), sizes follow the call
+    list, and every malformed call is rejected before any launch."""
+    import paper_2406_05981_b200 as sa
+    calls = (sa._Call * 2)()
+    fake = 1 << 20   # never dereferenced on the host
+    for j, (K, segs) in enumerate([(4096, [(4096, 2), (4096, 3), (4096, 2)]), (11008, [(4096, 2)])]):
+        c = calls[j]
+        c.x, c.K, c.g, c.nseg, c.flags = fake, K, 128, len(segs), sa.CALL_WAIT if j else 0
+        for i, (N, q) in enumerate(segs):
+            c.seg[i] = sa._Segment(fake, fake, N, q, fake)
+    nb = L.shiftadd_program_bytes(2)
+    assert nb == 2 * L.shiftadd_program_bytes(1) - 64 and L.shiftadd_program_bytes(0) == 0
+    buf = (ctypes.c_uint8 * nb)()
+    assert L.shiftadd_program_encode(calls, 2, ctypes.addressof(buf), nb) == 0
+    assert bytes(buf[:8]) == b"SPRGS201"   # header magic
+    # workspace: 256 + two regions of max S x RGtot x 16 x 8 B (the q/k/v call: 16 x 768)
+    ws = L.shiftadd_workspace_bytes_program(calls, 2)
+    region = max(16 * 768, 43 * 256) * 16 * 8
+    assert ws == 256 + 2 * ((region + 255) // 256 * 256)
+    assert L.shiftadd_program_encode(calls, 2, ctypes.addressof(buf), nb - 1) == 2   # buffer too small
+    calls[1].flags = 8
+    assert L.shiftadd_program_encode(calls, 2, ctypes.addressof(buf), nb) == 2       # unknown flag
+    calls[1].flags = 0
+    calls[1].K = 11000
+    assert L.shiftadd_program_encode(calls, 2, ctypes.addressof(buf), nb) == 2       # K % 256
+    calls[1].K = 11008
+    calls[0].seg[1].q = 5
+    assert L.shiftadd_program_encode(calls, 2, ctypes.addressof(buf), nb) == 2       # q outside 1..4
+    calls[0].seg[1].q = 3
+    calls[0].nseg = 5
+    assert L.shiftadd_program_encode(calls, 2, ctypes.addressof(buf), nb) == 2
+    calls[0].nseg = 3
+    calls[0].x = fake + 2
+    assert L.shiftadd_program_encode(calls, 2, ctypes.addressof(buf), nb) == 2       # x alignment
+    calls[0].x = fake
+    assert L.shiftadd_program_encode(calls, 0, ctypes.addressof(buf), nb) == 2
+    # a valid program on a machine without a GPU: the launch reports a CUDA error, no crash
+    assert L.shiftadd_lut_gemv_program(calls, 2, fake, nb, fake, ws, 0, None) == 7
