@@ -219,6 +219,17 @@ shiftadd_status shiftadd_pack_colwise(const int8_t* signs, const float* alpha_co
 shiftadd_status shiftadd_lut_gemv_colwise(const uint16_t* x, const uint8_t* planes, const int8_t* exps_col,
                                           int layout, int N, int K, int q, uint16_t* y, unsigned flags,
                                           void* stream);
+/* shiftadd_lut_gemv_colwise_ws: the same result for any K % 256 == 0 up to 256 x #SMs (the
+ *   LLaMA-2-70B / OPT-66B shapes the cluster kernel cannot hold).  K <= 4096 shapes the
+ *   cluster kernel takes go there (no workspace touched) unless flags has
+ *   SHIFTADD_FLAG_SPLITK; otherwise the all-SM streaming kernel (id 8) builds, per 256-k slice,
+ *   plane i's LUT from x[k] 2^{e_i[k]} and reduces the K-split through `workspace`
+ *   (shiftadd_workspace_bytes_colwise(N, K) bytes, same zero-once contract as
+ *   shiftadd_lut_gemm).  flags: 0 or SHIFTADD_FLAG_PDL | SHIFTADD_FLAG_SPLITK. */
+size_t shiftadd_workspace_bytes_colwise(int N, int K);
+shiftadd_status shiftadd_lut_gemv_colwise_ws(const uint16_t* x, const uint8_t* planes, const int8_t* exps_col,
+                                             int layout, int N, int K, int q, uint16_t* y, void* workspace,
+                                             size_t workspace_bytes, unsigned flags, void* stream);
 
 /* NEXT-f1 -- block-wise scales, "Ours (Lat.)" (Fig. 4(a)): "a block-wise
  * scaling factor design that groups 8 columns and 1/8 of the original rows to share a scaling

@@ -89,6 +89,11 @@ def lib():
         L.shiftadd_pack_colwise.argtypes = [vp, vp, c_int, c_int, c_int, c_int, vp, vp, vp, vp]
         L.shiftadd_lut_gemv_colwise.restype = c_int
         L.shiftadd_lut_gemv_colwise.argtypes = [vp, vp, vp, c_int, c_int, c_int, c_int, vp, ctypes.c_uint, vp]
+        L.shiftadd_workspace_bytes_colwise.restype = c_size
+        L.shiftadd_workspace_bytes_colwise.argtypes = [c_int, c_int]
+        L.shiftadd_lut_gemv_colwise_ws.restype = c_int
+        L.shiftadd_lut_gemv_colwise_ws.argtypes = [vp, vp, vp, c_int, c_int, c_int, c_int, vp, vp, c_size,
+                                                   ctypes.c_uint, vp]
         L.shiftadd_pack_apot2.restype = c_int
         L.shiftadd_pack_apot2.argtypes = [vp, vp, c_int, c_int, c_int, c_int, c_int, vp, vp, vp, vp, vp]
         L.shiftadd_lut_gemm_apot2.restype = c_int
@@ -336,8 +341,9 @@ def lut_gemv_blockwise(x: torch.Tensor, layer: PackedLayer, out: torch.Tensor | 
 
 
 def lut_gemv_colwise(x: torch.Tensor, layer: PackedLayer, out: torch.Tensor | None = None, pdl: bool = False,
-                     stream=None) -> torch.Tensor:
-    """NEXT-f1: y[N] = x[K] (.) a column-wise-scaled layer, fp16 (shiftadd_lut_gemv_colwise)."""
+                     stream=None, workspace: "Workspace | None" = None, splitk: bool = False) -> torch.Tensor:
+    """NEXT-f1: y[N] = x[K] (.) a column-wise-scaled layer, fp16 (shiftadd_lut_gemv_colwise_ws:
+    the cluster kernel for K <= 4096, else -- or with splitk -- the all-SM streaming kernel)."""
     if not layer.colwise:
         raise ValueError("layer was not packed with pack_colwise")
     xv = x.reshape(-1)
@@ -351,12 +357,16 @@ def lut_gemv_colwise(x: torch.Tensor, layer: PackedLayer, out: torch.Tensor | No
     dev = layer.device
     if torch.cuda.current_device() != dev.index:
         torch.cuda.set_device(dev)
+    need = int(lib().shiftadd_workspace_bytes_colwise(layer.N, layer.K)) if layer.layout == LAYOUT_TILED else 0
+    ws = (workspace or _workspace_for(dev, stream)).get(need)
     sptr = (stream if stream is not None else torch.cuda.current_stream(dev)).cuda_stream
-    st = lib().shiftadd_lut_gemv_colwise(xv.data_ptr(), layer.planes.data_ptr(), layer.exps.data_ptr(),
-                                         layer.layout, layer.N, layer.K, layer.q, out.data_ptr(),
-                                         FLAG_PDL if pdl else 0, sptr)
+    flags = (FLAG_PDL if pdl else 0) | (FLAG_SPLITK if splitk else 0)
+    st = lib().shiftadd_lut_gemv_colwise_ws(xv.data_ptr(), layer.planes.data_ptr(), layer.exps.data_ptr(),
+                                            layer.layout, layer.N, layer.K, layer.q, out.data_ptr(),
+                                            ws.data_ptr() if ws is not None else None,
+                                            ws.numel() if ws is not None else 0, flags, sptr)
     if st:
-        _check(st, "shiftadd_lut_gemv_colwise")
+        _check(st, "shiftadd_lut_gemv_colwise_ws")
     return out
 
 

@@ -236,6 +236,55 @@ shiftadd_status shiftadd_lut_gemv_colwise(const uint16_t* x, const uint8_t* plan
   return SHIFTADD_OK;
 }
 
+size_t shiftadd_workspace_bytes_colwise(int N, int K) {
+  if (N < 1 || N > kMaxRows || K < kTileK || K % kTileK) return 0;
+  return stream_workspace_bytes(1, K / kTileK, (N + kTileRows - 1) / kTileRows);
+}
+
+shiftadd_status shiftadd_lut_gemv_colwise_ws(const uint16_t* x, const uint8_t* planes, const int8_t* exps_col,
+                                             int layout, int N, int K, int q, uint16_t* y, void* workspace,
+                                             size_t workspace_bytes, unsigned flags, void* stream) {
+  if (!x || !planes || !exps_col || !y) return fail(SHIFTADD_ERR_INVALID, "null pointer argument");
+  shiftadd_status st = check_shape(q, N, K, 8, 4);
+  if (st != SHIFTADD_OK) return st;
+  if ((st = check_layout(layout, K, 128)) != SHIFTADD_OK) return st;
+  if (layout != SHIFTADD_LAYOUT_TILED)
+    return fail(SHIFTADD_ERR_UNSUPPORTED, "column-wise GEMV needs the tiled layout");
+  if (flags & ~(SHIFTADD_FLAG_PDL | SHIFTADD_FLAG_SPLITK)) return fail(SHIFTADD_ERR_INVALID, "unknown flags 0x%x", flags);
+  if (!aligned(x, 16) || !aligned(planes, 16) || !aligned(exps_col, 8) || !aligned(y, 2))
+    return fail(SHIFTADD_ERR_INVALID, "misaligned pointer (x, planes 16 B; exps_col 8 B)");
+  DevInfo di;
+  if ((st = device_info(&di)) != SHIFTADD_OK) return st;
+  // K <= 4096: the cluster kernel (no workspace) unless SHIFTADD_FLAG_SPLITK; else the all-SM
+  // streaming kernel with per-plane column-scaled LUTs
+  if (!(flags & SHIFTADD_FLAG_SPLITK) && colwise_applicable(N, K, q))
+    return shiftadd_lut_gemv_colwise(x, planes, exps_col, layout, N, K, q, y, flags & SHIFTADD_FLAG_PDL, stream);
+  if (!stream_shape_ok(K, di.sms)) return fail(SHIFTADD_ERR_UNSUPPORTED, "column-wise GEMV: K=%d above 256 x #SMs", K);
+  const size_t need = shiftadd_workspace_bytes_colwise(N, K);
+  if (need > 0 && (!workspace || workspace_bytes < need || !aligned(workspace, 16)))
+    return fail(SHIFTADD_ERR_INVALID, "workspace needs %zu bytes, 16-B aligned (got %zu)", need, workspace_bytes);
+  StreamLaunch L = {};
+  L.x = reinterpret_cast<const __half*>(x);
+  L.M = 1;
+  L.ldx = K;
+  L.K = K;
+  L.nseg = 1;
+  L.seg[0] = StreamSeg{planes, exps_col, reinterpret_cast<__half*>(y), q, N};
+  L.exps_bw = exps_col;
+  L.colwise = 1;
+  L.workspace = workspace;
+  L.grid = di.sms;
+  L.su = 16;
+  const int lut = q <= 2 ? 64 * 1024 : 128 * 1024;
+  const int slot = L.su * q * (kTileBytes + kTileExps);
+  L.nst = (kStreamSmemBudget - lut - 512) / slot;
+  L.nst = L.nst > 16 ? 16 : L.nst;
+  L.pdl = (flags & SHIFTADD_FLAG_PDL) ? 1 : 0;
+  const cudaError_t e = launch_lut_stream(L, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "lut_gemv_colwise_ws launch");
+  return SHIFTADD_OK;
+}
+
 shiftadd_status shiftadd_pack_blockwise(const int8_t* signs, const float* alpha_bw, int q, int N, int K, int layout,
                                        uint8_t* planes, int8_t* exps_bw, int32_t* counts, void* stream) {
   if (!signs || !alpha_bw || !planes || !exps_bw) return fail(SHIFTADD_ERR_INVALID, "null pointer argument");

@@ -221,6 +221,7 @@ struct StreamLaunch {
   int grid, nst, su, pdl;
   int half;   // 1: the co-resident variant (<= 113 KB shared memory, two CTAs fit one SM)
   const int8_t* exps_bw;   // non-null: NEXT-f1 block-wise exponents [q][8][K/8] (M = 1, one segment)
+  int colwise;             // 1: exps_bw holds NEXT-f1 column-wise exponents [q][K] instead
 };
 
 // The persistent decode program (lut_program.cu, kernel id 9): ordered calls of the fused form.

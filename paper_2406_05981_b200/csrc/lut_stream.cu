@@ -504,6 +504,41 @@ __device__ __forceinline__ void build_lut_scaled(const uint4 xv, const int8_t* _
   }
 }
 
+// NEXT-f1 column-wise scales, "Ours (Acc.)" (realisation SPEC.md:375,
+// reading R18): plane i has one PoT scale per input column k, so the shift moves onto the
+// activations -- plane i's LUT of the slice is built from x[k] 2^{e_i[k]} (an exact fp32
+// multiply by a power of two; EXP_ZERO gives +0) and queried unscaled.  Same slab layout as
+// the block-wise scaled LUTs (plane i in slab i >> 1, column half i & 1); lane = group of 8 k.
+template <int NWC, int Q>
+__device__ __forceinline__ void build_lut_colw(const uint4 xv, const int8_t* __restrict__ exps_col, int K, int s,
+                                               int warp, int lane) {
+  const float2 f01 = __half22float2(*reinterpret_cast<const __half2*>(&xv.x));
+  const float2 f23 = __half22float2(*reinterpret_cast<const __half2*>(&xv.y));
+  const float2 f45 = __half22float2(*reinterpret_cast<const __half2*>(&xv.z));
+  const float2 f67 = __half22float2(*reinterpret_cast<const __half2*>(&xv.w));
+  const float x8[8] = {f01.x, f01.y, f23.x, f23.y, f45.x, f45.y, f67.x, f67.y};
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    const uint2 ev = __ldg(reinterpret_cast<const uint2*>(exps_col + (size_t)i * K + (size_t)s * kTileK + 8 * lane));
+    float v[8];
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const int e = (int)(int8_t)(((b < 4 ? ev.x : ev.y) >> (8 * (b & 3))) & 0xffu);
+      v[b] = x8[b] * pow2_bits(e);
+    }
+    const float A[4] = {-v[0] - v[1], v[0] - v[1], v[1] - v[0], v[0] + v[1]};
+    const float B[4] = {-v[2] - v[3], v[2] - v[3], v[3] - v[2], v[2] + v[3]};
+    const uint32_t col = kDynBase + (uint32_t)(i >> 1) * 65536u + (uint32_t)(i & 1) * 128u + 4u * lane;
+#pragma unroll
+    for (int hh = 0; hh < 16 / NWC; ++hh) {
+      const int hi = warp + hh * NWC;
+      const float H = ((hi & 1 ? v[4] : -v[4]) + (hi & 2 ? v[5] : -v[5])) + ((hi & 4 ? v[6] : -v[6]) + (hi & 8 ? v[7] : -v[7]));
+#pragma unroll
+      for (int lo = 0; lo < 16; ++lo) sts_f32(col + ((hi * 16 + lo) << 8), (A[lo & 3] + B[lo >> 2]) + H);
+    }
+  }
+}
+
 template <int Q>
 __device__ __forceinline__ float unit_dot_lut(uint32_t sp, const uint32_t (&cst)[4]) {
   uint4 w[Q];
@@ -523,7 +558,7 @@ __device__ __forceinline__ float unit_dot_lut(uint32_t sp, const uint32_t (&cst)
   return (pc[0] + pc[1]) + (pc[2] + pc[3]);
 }
 
-template <int NWC, int Q>
+template <int NWC, int Q, bool COLW>
 __device__ __forceinline__ void consume_run_lut(const StreamParams& p, const SegDev& sg, int s, int rga, int re,
                                                 RingPos& rp, uint32_t ring, uint32_t full, uint32_t empty,
                                                 const uint32_t (&cst)[4], int wu, int lane, unsigned long long ep,
@@ -534,9 +569,12 @@ __device__ __forceinline__ void consume_run_lut(const StreamParams& p, const Seg
     const int b = r0 / p.bw_rgb;
     const int r1 = (b + 1) * p.bw_rgb < re ? (b + 1) * p.bw_rgb : re;
     const int key = s * 8 + b;
-    if (key != cur) {   // rebuild the q scaled LUTs for (s, b)
+    if (key != cur) {   // rebuild the q scaled LUTs for (s, b) (column-wise: for s)
       asm volatile("bar.sync 1, %0;" ::"r"(NWC * 32) : "memory");
-      build_lut_scaled<NWC, Q>(xv, p.exps_bw, KB, s, b, wu, lane);
+      if (COLW)
+        build_lut_colw<NWC, Q>(xv, p.exps_bw, p.S * kTileK, s, wu, lane);
+      else
+        build_lut_scaled<NWC, Q>(xv, p.exps_bw, KB, s, b, wu, lane);
       asm volatile("bar.sync 1, %0;" ::"r"(NWC * 32) : "memory");
       cur = key;
     }
@@ -567,16 +605,16 @@ __device__ __forceinline__ void consume_run_lut(const StreamParams& p, const Seg
   }
 }
 
-template <int NWC>
+template <int NWC, bool COLW>
 __device__ __forceinline__ void consume_run_lut_q(const StreamParams& p, const SegDev& sg, int s, int rga, int re,
                                                   RingPos& rp, uint32_t ring, uint32_t full, uint32_t empty,
                                                   const uint32_t (&cst)[4], int wu, int lane, unsigned long long ep,
                                                   const uint4 xv, int& cur) {
   switch (sg.q) {
-    case 1: consume_run_lut<NWC, 1>(p, sg, s, rga, re, rp, ring, full, empty, cst, wu, lane, ep, xv, cur); break;
-    case 2: consume_run_lut<NWC, 2>(p, sg, s, rga, re, rp, ring, full, empty, cst, wu, lane, ep, xv, cur); break;
-    case 3: consume_run_lut<NWC, 3>(p, sg, s, rga, re, rp, ring, full, empty, cst, wu, lane, ep, xv, cur); break;
-    default: consume_run_lut<NWC, 4>(p, sg, s, rga, re, rp, ring, full, empty, cst, wu, lane, ep, xv, cur); break;
+    case 1: consume_run_lut<NWC, 1, COLW>(p, sg, s, rga, re, rp, ring, full, empty, cst, wu, lane, ep, xv, cur); break;
+    case 2: consume_run_lut<NWC, 2, COLW>(p, sg, s, rga, re, rp, ring, full, empty, cst, wu, lane, ep, xv, cur); break;
+    case 3: consume_run_lut<NWC, 3, COLW>(p, sg, s, rga, re, rp, ring, full, empty, cst, wu, lane, ep, xv, cur); break;
+    default: consume_run_lut<NWC, 4, COLW>(p, sg, s, rga, re, rp, ring, full, empty, cst, wu, lane, ep, xv, cur); break;
   }
 }
 
@@ -625,7 +663,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, MINB) lut_stream_kernel(const 
         for (int rg = a.rg; rg < re; ++t, rp.next(p.nst)) {
           if (rp.k > 0) mbar_wait(empty + 8 * rp.j, (uint32_t)((rp.k - 1) & 1));
           int n = re - rg < p.su ? re - rg : p.su;
-          if (BW == 2) {   // stages do not cross a row-block boundary
+          if (BW >= 2) {   // stages do not cross a row-block boundary (column-wise: one block)
             const int bend = (rg / p.bw_rgb + 1) * p.bw_rgb;
             n = bend - rg < n ? bend - rg : n;
           }
@@ -654,7 +692,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, MINB) lut_stream_kernel(const 
       if (tid == 32 && p.S > 1)   // a lane whose x does not gate warp 0
         asm volatile("st.shared.u32 [%0], %1;" ::"r"(s_epoch), "r"((unsigned)(ld_relaxed_u64(p.done) >> 32) + 1u)
                      : "memory");
-      if (MW == 1 && BW != 2) {
+      if (MW == 1 && BW < 2) {
         const uint64_t pol_keep = policy_evict_last();
         const uint4 xa = ldg_keep(p.x + (size_t)s0 * kTileK + 8 * lane, pol_keep);
         uint4 xb = xa;
@@ -692,7 +730,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, MINB) lut_stream_kernel(const 
       const bool skew = p.skew && warp >= NWC / 2;
       int t = 0;
       uint4 xs[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
-      if (BW == 2 && any) {
+      if (BW >= 2 && any) {
         const uint64_t pol_keep = policy_evict_last();
         xs[0] = ldg_keep(p.x + (size_t)s0 * kTileK + 8 * lane, pol_keep);
         if (two) xs[1] = ldg_keep(p.x + (size_t)(s0 + 1) * kTileK + 8 * lane, pol_keep);
@@ -700,8 +738,8 @@ __global__ void __launch_bounds__((NWC + 1) * 32, MINB) lut_stream_kernel(const 
       int cur = -1;
       for (Pos a = start; before(a, end);) {
         const int re = run_end(p, a, end);
-        if (BW == 2) {
-          consume_run_lut_q<NWC>(p, p.seg[a.g], a.s, a.rg, re, rp, ring, full, empty, cst, wu, lane, ep,
+        if (BW >= 2) {
+          consume_run_lut_q<NWC, BW == 3>(p, p.seg[a.g], a.s, a.rg, re, rp, ring, full, empty, cst, wu, lane, ep,
                                  a.s == s0 ? xs[0] : xs[1], cur);
         } else if (BW == 1) {
           if (a.s == s0)
@@ -869,6 +907,8 @@ cudaError_t launch_lut_stream(const StreamLaunch& L, cudaStream_t stream) {
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(lut_stream_kernel<16, 1, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(lut_stream_kernel<16, 1, 1, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    if (e == cudaSuccess)
       e = cudaFuncSetAttribute(lut_stream_kernel<8, 2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 113 * 1024);
     attr_err[dev] = e;
   });
@@ -916,6 +956,7 @@ cudaError_t launch_lut_stream(const StreamLaunch& L, cudaStream_t stream) {
   p.exps_bw = L.exps_bw;
   p.bw_rows = L.seg[0].N / 8;
   p.bw_rgb = (L.exps_bw && L.seg[0].N % 128 == 0) ? L.seg[0].N / 128 : 0;
+  if (L.exps_bw && L.colwise) p.bw_rgb = (L.seg[0].N + kTileRows - 1) / kTileRows;   // one row block
   if (p.bw_rgb > 0) p.lut_bytes = qmax <= 2 ? kLutSlab : 2 * kLutSlab;
   p.skew = 1;
 #ifdef SHIFTADD_DEV_TRACE
@@ -935,6 +976,7 @@ cudaError_t launch_lut_stream(const StreamLaunch& L, cudaStream_t stream) {
     if (MW != 1 || L.nseg != 1) return cudaErrorInvalidValue;
     // N % 128 == 0: scaled LUTs per (slice, row block); else the per-query scale (8 consumer
     // warps: room for the 8 q scale registers per lane)
+    if (L.colwise) return cudaLaunchKernelEx(&c, lut_stream_kernel<16, 1, 1, 3>, p);
     if (p.bw_rgb > 0) return cudaLaunchKernelEx(&c, lut_stream_kernel<16, 1, 1, 2>, p);
     if (L.su != 8) return cudaErrorInvalidValue;
     return cudaLaunchKernelEx(&c, lut_stream_kernel<8, 1, 1, 1>, p);

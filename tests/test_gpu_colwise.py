@@ -53,32 +53,40 @@ SHAPES = [
 ]
 
 
-@pytest.mark.parametrize("q,N,K", SHAPES)
-def test_colwise_gemv_parity(sa, q, N, K):
+# K > 4096 (the streaming kernel, per-plane column-scaled LUTs): LLaMA-2-70B gate/up K, the
+# LLaMA-2-7B down_proj, a ragged 70B-down-like K = 28672
+SHAPES_K = [(3, 8192, 8192), (2, 4096, 11008), (3, 1000, 28672), (1, 40, 4352)]
+
+
+@pytest.mark.parametrize("q,N,K,splitk", [(q, N, K, False) for q, N, K in SHAPES] +
+                         [(q, N, K, True) for q, N, K in SHAPES[:5]] + [(q, N, K, False) for q, N, K in SHAPES_K])
+def test_colwise_gemv_parity(sa, q, N, K, splitk):
     s, a, planes, e = _layer(q, N, K, synth.seed_for(8, q, N % 7))
     L = sa.pack_colwise(s.to(DEV), a.to(DEV))
     x = synth.gen_x(1, K, seed=synth.seed_for(8, 99))
-    y = sa.lut_gemv_colwise(x.to(DEV), L, pdl=True)
+    y = sa.lut_gemv_colwise(x.to(DEV), L, pdl=True, splitk=splitk)
     torch.cuda.synchronize()
     err = oracle.err_floor(y.float().cpu().numpy()[None, :], oracle.gemm_colwise(x.numpy(), planes, e))
     assert err <= TOL, err
 
 
-def test_colwise_basis_vector_gives_rounded_column_exactly(sa):
-    q, N, K = 3, 80, 512
+@pytest.mark.parametrize("K,splitk", [(512, False), (512, True), (8192, False)])
+def test_colwise_basis_vector_gives_rounded_column_exactly(sa, K, splitk):
+    q, N = 3, 80
     s, a, planes, e = _layer(q, N, K, synth.seed_for(8, 7))
     L = sa.pack_colwise(s.to(DEV), a.to(DEV))
     W = oracle.dequant_colwise(planes, e, K)
     for j in (0, 7, 8, 255, 256, 300, K - 1):
         x = synth.gen_special_x("basis", 1, K, j=j)
-        y = sa.lut_gemv_colwise(x.to(DEV), L).cpu().numpy()
+        y = sa.lut_gemv_colwise(x.to(DEV), L, splitk=splitk).cpu().numpy()
         assert np.array_equal(y, oracle.to_fp16(W[:, j]))
 
 
-def test_colwise_column_scaling_equals_exponent_shift_bit_exact(sa):
+@pytest.mark.parametrize("K", [1024, 8192])
+def test_colwise_column_scaling_equals_exponent_shift_bit_exact(sa, K):
     """x[k] * 2 with exps e  ==  x with e_i[k] + 1 for every plane: the kernel pre-shifts x by
     an exact power of two, so both build identical LUTs and the outputs are identical."""
-    q, N, K = 2, 300, 1024
+    q, N = 2, 300
     s, a, _, _ = _layer(q, N, K, synth.seed_for(8, 8))
     L = sa.pack_colwise(s.to(DEV), a.to(DEV))
     a2 = a.clone()
@@ -126,10 +134,12 @@ def test_colwise_deterministic(sa):
 
 
 def test_colwise_unsupported_shapes(sa):
+    """The canonical layout and K above 256 x #SMs stay unsupported (reported, never a fallback)."""
     s, a = synth.gen_layer_colwise(1, 64, 8192, seed=1, device=DEV)
-    L = sa.pack_colwise(s, a)
-    with pytest.raises(sa.ShiftAddError, match="unsupported"):
-        sa.lut_gemv_colwise(synth.gen_x(1, 8192, seed=1).to(DEV), L)
     Lc = sa.pack_colwise(s, a, layout=sa.LAYOUT_CANONICAL)
     with pytest.raises(sa.ShiftAddError, match="unsupported"):
         sa.lut_gemv_colwise(synth.gen_x(1, 8192, seed=1).to(DEV), Lc)
+    K = 256 * (torch.cuda.get_device_properties(0).multi_processor_count + 1)
+    s, a = synth.gen_layer_colwise(1, 16, K, seed=1, device=DEV)
+    with pytest.raises(sa.ShiftAddError, match="unsupported"):
+        sa.lut_gemv_colwise(synth.gen_x(1, K, seed=1).to(DEV), sa.pack_colwise(s, a))

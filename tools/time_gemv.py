@@ -56,7 +56,7 @@ for spec in a.shapes:
     s = torch.cuda.Stream(dev)
     def call(L):
         if a.colwise:
-            sa.lut_gemv_colwise(x, L, out=y.view(-1), pdl=a.pdl)
+            sa.lut_gemv_colwise(x, L, out=y.view(-1), pdl=a.pdl, workspace=ws, splitk=a.splitk)
         else:
             sa.lut_gemm(x, L, out=y, workspace=ws, pdl=a.pdl, splitk=a.splitk, cluster=a.cluster)
 
