@@ -71,7 +71,9 @@ KERNEL_NAMES = {0: "gemm_generic_kernel", 1: "gemv_tiled_kernel (grid split-K)",
                 4: "gemv_stream_kernel (grid split-K, TMA weight ring)",
                 5: "gemm_cluster_ring_m2_kernel (M = 2)", 6: "gemm_cluster_ring_m4_kernel (M = 3..4)",
                 7: "gemm_cluster_ring_m2/m4 kernels (M > 4, row chunks)",
-                8: "lut_stream_kernel (all-SM streaming, epoch split-K)"}
+                8: "lut_stream_kernel (all-SM streaming, epoch split-K)",
+                9: "lut_program_kernel (persistent decode program)",
+                10: "gemv_cluster_fused_kernel (fused segments, cluster split-K, TMA weight ring)"}
 
 
 def load_peaks():
@@ -273,7 +275,10 @@ class Launch:
             self.sa.lut_gemv_fused(x.view(-1), self.layers, outs=self.outs, workspace=ws, pdl=pdl)
 
     def kernel(self):
-        return self.sa.gemm_plan(self.layers[0], 1)[3] if self.kind == "gemm" else 8
+        # fused segments: the cluster TMA ring (kernel 10) for K <= 4096, else the streaming kernel
+        if self.kind == "gemm":
+            return self.sa.gemm_plan(self.layers[0], 1)[3]
+        return 10 if self.K <= 4096 and self.plane_bytes() <= 24e6 else 8
 
     def alg_bytes(self):
         return sum(plane_bytes(L.q, L.N, L.K) + L.q * L.N * (L.K // G) + 2 * L.N for L in self.layers) + 2 * self.K
@@ -383,7 +388,7 @@ def time_layer_row(sa, dev, stream, ws, l2, peak, label, segs, K, kind, ws_size)
     else:
         def fn(t):
             sa.lut_gemv_fused(x, copies[t % R], outs=outs, workspace=ws, pdl=True)
-        kid = 8
+        kid = 10 if K <= 4096 and sum(plane_bytes(q, N, K) for N, q in segs) <= 24e6 else 8
     with torch.cuda.stream(stream):
         for t in range(3):
             fn(t)

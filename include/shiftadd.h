@@ -133,12 +133,14 @@ shiftadd_status shiftadd_lut_gemm(const uint16_t* x, int ldx, const uint8_t* pla
  * q per layer, so the k_proj of a block may carry 3 bits while q/v carry 2).  Segment i:
  *   y_i[n] = fp16_rne( sum_j sum_G 2^{e_i[j][n][G]} sum_{k in G} s_i(j,n,k) x[k] ), n < N_i.
  * Equivalent to nseg shiftadd_lut_gemv calls; the one launch builds each K-slice's LUT once
- * for all segments and streams their weights as one byte range per slice (all-SM streaming
- * kernel, id 8).  Batch 1 (M = 1), tiled layout only, K % 256 == 0, K <= 256 x #SMs,
+ * for all segments and streams their weights: K <= 4096 with <= 24 MB of planes on the
+ * thread-block-cluster TMA ring (kernel id 10, K-split reduced over DSMEM, workspace unused),
+ * otherwise -- or with SHIFTADD_FLAG_SPLITK -- as one byte range per slice on the all-SM
+ * streaming kernel (id 8).  Batch 1 (M = 1), tiled layout only, K % 256 == 0, K <= 256 x #SMs,
  * 1 <= nseg <= 4, each segment 1 <= q <= 4 with planes / exps 16-B aligned (packed by
  * shiftadd_pack with the same K and g), y_i fp16 [N_i].  Workspace: shiftadd_workspace_bytes_fused
  * bytes (same zero-once contract as shiftadd_lut_gemm; calls of either kind may share it, not
- * concurrently).  flags: 0 or SHIFTADD_FLAG_PDL. */
+ * concurrently).  flags: 0 or SHIFTADD_FLAG_PDL | SHIFTADD_FLAG_SPLITK. */
 typedef struct {
   const uint8_t* planes; /* tiled planes of segment i            */
   const int8_t* exps;    /* tiled exponents of segment i         */

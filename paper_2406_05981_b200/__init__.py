@@ -483,10 +483,12 @@ def workspace_bytes_fused(layers, M: int = 1) -> int:
 
 
 def lut_gemv_fused(x: torch.Tensor, layers, outs=None, workspace: Workspace | None = None, pdl: bool = False,
-                   stream=None):
+                   stream=None, splitk: bool = False):
     """Fused projections sharing x (shiftadd_lut_gemv_fused): one launch computes
     y_i = x (.) layers[i] for every segment i, each with its own bit width.  x: fp16 [K];
-    layers: tiled PackedLayers with the same K and g; returns the list of y_i (fp16 [N_i])."""
+    layers: tiled PackedLayers with the same K and g; returns the list of y_i (fp16 [N_i]).
+    K <= 4096 with <= 24 MB of planes runs on the cluster TMA ring (kernel 10) unless splitk
+    forces the all-SM streaming kernel (8), which takes the rest."""
     x = x.reshape(-1)
     if x.dtype != torch.float16 or not x.is_cuda:
         raise ValueError("x must be fp16 on the device")
@@ -508,7 +510,8 @@ def lut_gemv_fused(x: torch.Tensor, layers, outs=None, workspace: Workspace | No
     sptr = (stream if stream is not None else torch.cuda.current_stream(dev)).cuda_stream
     _check(lib().shiftadd_lut_gemv_fused(x.data_ptr(), x.numel(), layers[0].g, LAYOUT_TILED, len(layers), segs,
                                          ws.data_ptr() if ws is not None else None, ws.numel() if ws is not None else 0,
-                                         FLAG_PDL if pdl else 0, sptr), "shiftadd_lut_gemv_fused")
+                                         (FLAG_PDL if pdl else 0) | (FLAG_SPLITK if splitk else 0), sptr),
+           "shiftadd_lut_gemv_fused")
     return outs
 
 

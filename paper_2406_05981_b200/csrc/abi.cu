@@ -641,7 +641,7 @@ shiftadd_status shiftadd_lut_gemv_fused(const uint16_t* x, int K, int g, int lay
   if (!x || !segs) return fail(SHIFTADD_ERR_INVALID, "null pointer argument");
   if (layout != SHIFTADD_LAYOUT_TILED) return fail(SHIFTADD_ERR_UNSUPPORTED, "fused segments need the tiled layout");
   if (nseg < 1 || nseg > kMaxSegments) return fail(SHIFTADD_ERR_INVALID, "nseg=%d outside [1, %d]", nseg, kMaxSegments);
-  if (flags & ~SHIFTADD_FLAG_PDL) return fail(SHIFTADD_ERR_INVALID, "unknown flags 0x%x", flags);
+  if (flags & ~(SHIFTADD_FLAG_PDL | SHIFTADD_FLAG_SPLITK)) return fail(SHIFTADD_ERR_INVALID, "unknown flags 0x%x", flags);
   if (!aligned(x, 16)) return fail(SHIFTADD_ERR_INVALID, "x must be 16-B aligned");
   shiftadd_status st;
   int rg = 0;
@@ -659,7 +659,7 @@ shiftadd_status shiftadd_lut_gemv_fused(const uint16_t* x, int K, int g, int lay
   if (!stream_shape_ok(K, di.sms))
     return fail(SHIFTADD_ERR_UNSUPPORTED, "fused segments: K=%d above 256 x %d SMs", K, di.sms);
   const size_t need = stream_workspace_bytes(1, K / kTileK, rg);
-  if (!workspace || workspace_bytes < need || !aligned(workspace, 16))
+  if (need > 0 && (!workspace || workspace_bytes < need || !aligned(workspace, 16)))
     return fail(SHIFTADD_ERR_INVALID, "workspace needs %zu bytes, 16-B aligned (got %zu)", need, workspace_bytes);
   StreamLaunch L = {};
   L.x = reinterpret_cast<const __half*>(x);
@@ -677,6 +677,17 @@ shiftadd_status shiftadd_lut_gemv_fused(const uint16_t* x, int K, int g, int lay
   L.su = 16;
   L.nst = stream_stages(qmax, kStreamSmemBudget, L.su, 1);
   L.pdl = (flags & SHIFTADD_FLAG_PDL) ? 1 : 0;
+  // K <= 4096: the cluster TMA ring (kernel 10, DSMEM reduction, no workspace) unless
+  // SHIFTADD_FLAG_SPLITK; otherwise (or if no cluster shape fits) the all-SM streaming kernel
+  // (measured on B200: q/k/v 4096 x 3 at 2/3/2 bits 8.2 vs 9.1 us; gate/up 11008 x 2 at 2/3
+  // bits 12.0 vs 11.5 us -- the 120 SMs clusters of 8 pack lose to all 148 above ~24 MB)
+  double plane_bytes = 0;
+  for (int i = 0; i < nseg; ++i) plane_bytes += (double)segs[i].q * segs[i].N * K / 8;
+  if (!(flags & SHIFTADD_FLAG_SPLITK) && K <= 4096 && plane_bytes <= 24e6 && fused_cluster_ok(K, rg)) {
+    const cudaError_t ec = launch_gemv_cluster_fused(L, reinterpret_cast<cudaStream_t>(stream));
+    if (ec != cudaSuccess) return cuda_fail(ec, "lut_gemv_fused (cluster) launch");
+    return SHIFTADD_OK;
+  }
 #ifdef SHIFTADD_DEV_TRACE
   if (g_dev_variant & 1) {
     L.half = 1;

@@ -294,6 +294,9 @@ int stream_stages(int qmax, int budget, int su, int MW);
 size_t stream_workspace_bytes(int M, int S, int RGtot);
 bool stream_shape_ok(int K, int sms);
 cudaError_t launch_lut_stream(const StreamLaunch& L, cudaStream_t stream);
+// kernel 10: fused segments on the cluster TMA ring (M = 1, K <= 4096)
+bool fused_cluster_ok(int K, int RGtot);
+cudaError_t launch_gemv_cluster_fused(const StreamLaunch& L, cudaStream_t stream);
 #ifdef SHIFTADD_DEV_TRACE
 cudaError_t dev_set_trace(void* buf);
 cudaError_t dev_set_program_trace(void* buf);

@@ -797,6 +797,185 @@ gemv_cluster_ring_kernel(const __half* __restrict__ x, const uint8_t* __restrict
 
 
 // ------------------------------------------------------------------------------------------
+// Fused projections on the cluster TMA ring (kernel id 10): the segments of
+// shiftadd_lut_gemv_fused (LLaMA q/k/v at 2/3/2 bits, gate/up at 2/3) in one launch of the
+// ring kernel's decomposition.  A cluster's band is a range of the segments' concatenated row
+// groups; per slice of the CTA the band splits into runs of one segment (one q), each streamed
+// in stages of <= 16 items of q x 544 B; the consumers walk the same runs and dispatch on q.
+// Reduction (in-loop DSMEM push, owner sums in slice order) as in gemv_cluster_ring_kernel.
+struct FusedSeg {
+  const uint8_t* planes;
+  const int8_t* exps;
+  __half* y;
+  int q, N, RG, rgoff;
+};
+struct FusedArgs {
+  const __half* x;
+  FusedSeg seg[kMaxSegments];
+  int nseg, S, RGtot, C, slot, slot_planes, nst, pdl;
+};
+
+// Run of the band [b0, b1) inside segment g: [max(b0, rgoff), min(b1, rgoff + RG)).
+__device__ __forceinline__ bool fused_run(const FusedArgs& A, int g, int b0, int b1, int& ra, int& rb) {
+  ra = b0 > A.seg[g].rgoff ? b0 : A.seg[g].rgoff;
+  const int e = A.seg[g].rgoff + A.seg[g].RG;
+  rb = b1 < e ? b1 : e;
+  return ra < rb;
+}
+
+template <int Q>
+__device__ __forceinline__ float fused_dot(uint32_t sp, uint32_t se, bool odd, const uint32_t (&cstE)[8],
+                                           const uint32_t (&cstO)[8]) {
+  uint4 w[Q];
+  int e[Q];
+#pragma unroll
+  for (int k = 0; k < Q; ++k) {
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(w[k].x), "=r"(w[k].y), "=r"(w[k].z), "=r"(w[k].w)
+                 : "r"(sp + (uint32_t)(k * kTileBytes)));
+    asm volatile("ld.shared.s8 %0, [%1];" : "=r"(e[k]) : "r"(se + (uint32_t)(k * kTileExps)));
+  }
+  return odd ? unit_dot_c<Q, kDynBase, false>(w, e, e, cstO) : unit_dot_c<Q, kDynBase, false>(w, e, e, cstE);
+}
+
+__global__ void __launch_bounds__((kRingNW + 1) * 32, 1) gemv_cluster_fused_kernel(const __grid_constant__ FusedArgs A) {
+  constexpr int NW = kRingNW;
+  if (threadIdx.x == 0) check_dyn_base();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NT = (NW + 1) * 32;
+  const int r = lane >> 1, h = lane & 1;
+  const uint32_t rank = cluster_rank();
+  const unsigned Cu = (unsigned)A.C, ncl = gridDim.x / Cu, cl = blockIdx.x / Cu;
+  const int S = A.S;
+  const int rg0 = (int)((cl * (unsigned)A.RGtot) / ncl);
+  const int RGb = (int)(((cl + 1) * (unsigned)A.RGtot) / ncl) - rg0;
+  const int s0 = (int)((rank * (unsigned)S) / Cu);
+  const int Sc = (int)(((rank + 1) * (unsigned)S) / Cu) - s0;   // <= 2
+  if (A.pdl) pdl_launch_dependents();
+
+  const uint32_t base = dyn_smem_base_cluster();
+  const uint32_t xs = base + RingMap::lut;
+  const uint32_t recv = xs + RingMap::xstage;
+  const uint32_t bar = base + RingMap::bar;
+  const uint32_t ring = base + (uint32_t)kRingBase;
+  const uint32_t full = ring + (uint32_t)(A.nst * A.slot), empty = full + 64;
+  const int chunk_rg = (RGb + A.C - 1) / A.C;
+  const int chunk = chunk_rg * kTileRows;
+  const int rows = RGb * kTileRows;
+  const int own_lo = (int)rank * chunk;
+  const int cnt = rows - own_lo < chunk ? (rows - own_lo > 0 ? rows - own_lo : 0) : chunk;
+  const float inv_chunk_rg = 1.f / (float)chunk_rg;
+  if (tid == 0) {
+    mbar_init_expect(bar, (uint32_t)((S - Sc) * cnt * 4));
+    for (int j = 0; j < A.nst; ++j) {
+      rmbar_init(full + 8 * j, 1);
+      rmbar_init(empty + 8 * j, NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  cluster_arrive_relaxed();
+
+  if (warp == NW) {
+    // producer: per slice t, per segment run of the band, stages of <= 16 items
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      int st = 0;
+      for (int t = 0; t < Sc; ++t) {
+        for (int g = 0; g < A.nseg; ++g) {
+          int ra, rb;
+          if (!fused_run(A, g, rg0, rg0 + RGb, ra, rb)) continue;
+          const FusedSeg& sg = A.seg[g];
+          for (int a = ra; a < rb; a += NW, ++st) {
+            const int n = rb - a < NW ? rb - a : NW;
+            const int j = st % A.nst;
+            if (st >= A.nst) rmbar_wait(empty + 8 * j, (uint32_t)((st / A.nst - 1) & 1));
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full + 8 * j),
+                         "r"((uint32_t)(n * sg.q * (kTileBytes + kTileExps))) : "memory");
+            const long long u = (long long)(s0 + t) * sg.RG + (a - sg.rgoff);
+            const uint32_t dst = ring + (uint32_t)(j * A.slot);
+            bulk_load_x(dst, sg.planes + u * sg.q * kTileBytes, (uint32_t)(n * sg.q * kTileBytes), full + 8 * j, pol,
+                        false);
+            bulk_load_x(dst + (uint32_t)A.slot_planes, sg.exps + u * sg.q * kTileExps,
+                        (uint32_t)(n * sg.q * kTileExps), full + 8 * j, pol, false);
+          }
+        }
+      }
+    }
+  } else {
+    if (tid < Sc * 4)
+      asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(A.x + (size_t)s0 * kTileK + 64 * tid));
+    if (A.pdl) pdl_wait();
+    if (tid < Sc * (kTileK / 8)) {
+      const uint4 xv = ldg_keep(reinterpret_cast<const uint4*>(A.x + (size_t)s0 * kTileK) + tid, policy_evict_last());
+      asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(xs + 16 * tid), "r"(xv.x), "r"(xv.y), "r"(xv.z),
+                   "r"(xv.w) : "memory");
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+    for (int t = 0; t < Sc; ++t) build_lut_slot<NW>(base + (uint32_t)t * 128u, xs + t * (kTileK * 2), warp, lane);
+    asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+    cluster_wait();
+    uint32_t cstE[8], cstO[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint32_t c0 = 4u * (uint32_t)(16 * h + ((2 * c + r) & 15));
+      const uint32_t c1 = 4u * (uint32_t)(16 * h + ((2 * c + 1 + r) & 15));
+      cstE[c] = c0 | (c1 << 8) | (rank << 16);
+      cstO[c] = cstE[c] + 0x8080u;
+    }
+    int st = 0;
+    for (int t = 0; t < Sc; ++t) {
+      for (int g = 0; g < A.nseg; ++g) {
+        int ra, rb;
+        if (!fused_run(A, g, rg0, rg0 + RGb, ra, rb)) continue;
+        const int q = A.seg[g].q;
+        for (int a = ra; a < rb; a += NW, ++st) {
+          const int n = rb - a < NW ? rb - a : NW;
+          const int j = st % A.nst;
+          rmbar_wait(full + 8 * j, (uint32_t)((st / A.nst) & 1));
+          if (warp < n) {
+            const uint32_t sp = ring + (uint32_t)(j * A.slot + warp * q * kTileBytes + 16 * lane);
+            const uint32_t se = ring + (uint32_t)(j * A.slot + A.slot_planes + warp * q * kTileExps + lane);
+            float v;
+            switch (q) {
+              case 1: v = fused_dot<1>(sp, se, t, cstE, cstO); break;
+              case 2: v = fused_dot<2>(sp, se, t, cstE, cstO); break;
+              case 3: v = fused_dot<3>(sp, se, t, cstE, cstO); break;
+              default: v = fused_dot<4>(sp, se, t, cstE, cstO); break;
+            }
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty + 8 * j) : "memory");
+            v += __shfl_xor_sync(0xffffffffu, v, 1);
+            if (h == 0) {
+              const int rgl = a + warp - rg0;   // band-local row group
+              const int o = (int)(((float)rgl + 0.5f) * inv_chunk_rg);
+              const uint32_t dst = recv + 4u * (uint32_t)((s0 + t) * chunk + (rgl - o * chunk_rg) * kTileRows + r);
+              if (o == (int)rank) sts_f32(dst, v);
+              else st_async_f32(dst, bar, (uint32_t)o, v);
+            }
+          } else {
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty + 8 * j) : "memory");
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  mbar_wait_parity0(bar);
+  for (int jj = tid; jj < cnt; jj += NT) {
+    float v = lds_f32(recv + 4u * (uint32_t)jj);
+    for (int s = 1; s < S; ++s) v += lds_f32(recv + 4u * (uint32_t)(s * chunk + jj));
+    const int nf = rg0 * kTileRows + own_lo + jj;   // row of the concatenated segments
+    const int rgf = nf / kTileRows;
+    int g = 0;
+    while (g + 1 < A.nseg && A.seg[g + 1].rgoff <= rgf) ++g;
+    const int nl = nf - A.seg[g].rgoff * kTileRows;
+    if (nl < A.seg[g].N) A.seg[g].y[nl] = __float2half_rn(v);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // §8 a7, M = 2 on the cluster TMA ring (kernel id 5).  The batch-1 ring kernel's
 // decomposition, weight ring and DSMEM reduction, with float2 LUT entries holding the
 // partial sums of both batch rows: one key byte from HBM, one LDS.64, two FADDs.  A slot is
@@ -1477,6 +1656,72 @@ cudaError_t launch_ring_q(const GemmArgs& a, const LaunchPlan& p, int C) {
                             pdl ? kFlagPdl : 0, trace, a.gather);
 }
 
+// Kernel 10 geometry: clusters of the ring kernel's shape for K; nullptr-free plan or C = 0.
+int fused_cluster_grid(int K, int RGtot, int* C_out) {
+  const int S = K / kTileK;
+  if (S < 1 || (S + 1) / 2 > kMaxC) return 0;
+  const int C = (S + 1) / 2;
+  const int ncl = max_clusters(kRing, C);
+  if (ncl <= 0) return 0;
+  const int bands = ncl < RGtot ? ncl : RGtot;
+  if ((RGtot + bands - 1) / bands > kMaxRGb) return 0;
+  *C_out = C;
+  return bands * C;
+}
+
+cudaError_t launch_fused_impl(const StreamLaunch& L, cudaStream_t stream) {
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(gemv_cluster_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    RingCfg<1>::smem);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(gemv_cluster_fused_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  FusedArgs A = {};
+  A.x = L.x;
+  A.nseg = L.nseg;
+  A.S = L.K / kTileK;
+  int rg = 0, qmax = 1;
+  for (int i = 0; i < L.nseg; ++i) {
+    FusedSeg& d = A.seg[i];
+    d.planes = L.seg[i].planes;
+    d.exps = L.seg[i].exps;
+    d.y = L.seg[i].y;
+    d.q = L.seg[i].q;
+    d.N = L.seg[i].N;
+    d.RG = (d.N + kTileRows - 1) / kTileRows;
+    d.rgoff = rg;
+    rg += d.RG;
+    qmax = d.q > qmax ? d.q : qmax;
+  }
+  A.RGtot = rg;
+  int C = 0;
+  const int grid = fused_cluster_grid(L.K, rg, &C);
+  if (grid <= 0) return cudaErrorNotSupported;
+  A.C = C;
+  A.slot = kRingNW * qmax * (kTileBytes + kTileExps);
+  A.slot_planes = kRingNW * qmax * kTileBytes;
+  A.nst = (kRingBytes - 128) / A.slot > 8 ? 8 : (kRingBytes - 128) / A.slot;
+  A.pdl = L.pdl;
+  cudaLaunchConfig_t c = {};
+  c.gridDim = dim3(grid);
+  c.blockDim = dim3((kRingNW + 1) * 32);
+  c.dynamicSmemBytes = RingCfg<1>::smem;
+  c.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  c.attrs = attr;
+  c.numAttrs = L.pdl ? 2 : 1;
+  return cudaLaunchKernelEx(&c, gemv_cluster_fused_kernel, A);
+}
+
 template <int SCM, int NW, bool AP2 = false>
 cudaError_t launch_cluster_v(const GemmArgs& a, const LaunchPlan& p, int C) {
   switch (a.q) {
@@ -1519,6 +1764,13 @@ __global__ void gather_wait_kernel(const uint32_t* __restrict__ flags, int P, ui
 }
 
 }  // namespace
+
+// kernel 10 entry (shiftadd_lut_gemv_fused, K <= 4096): cudaErrorNotSupported if no cluster shape fits
+cudaError_t launch_gemv_cluster_fused(const StreamLaunch& L, cudaStream_t stream) { return launch_fused_impl(L, stream); }
+bool fused_cluster_ok(int K, int RGtot) {
+  int C = 0;
+  return fused_cluster_grid(K, RGtot, &C) > 0;
+}
 
 cudaError_t launch_gather_wait(const uint32_t* flags, int P, uint32_t* epoch, cudaStream_t stream) {
   cudaLaunchConfig_t c = {};

@@ -777,6 +777,13 @@ __global__ void __launch_bounds__((NWC + 1) * 32, MINB) lut_stream_kernel(const 
 #endif
   }
   trace_at(4);
+#ifdef SHIFTADD_DEV_TRACE
+  if (g_trace && threadIdx.x == 0) {
+    unsigned sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    g_trace[16 * blockIdx.x + 15] = sm;
+  }
+#endif
   if (p.S == 1) return;
 
   // a5 owner phase: rows of the flattened row groups [c RGtot / G, (c+1) RGtot / G)

@@ -50,11 +50,12 @@ def test_stream_kernel_parity(sa, q, N, K):
                                   [(2, 11008), (3, 11008)],                # gate/up, up 3-bit
                                   [(1, 40), (4, 1000), (2, 17), (3, 513)],  # ragged, every q
                                   [(3, 2048)]])
-@pytest.mark.parametrize("K", [1024, 4096])
-def test_fused_segments_parity(sa, segs, K):
+@pytest.mark.parametrize("K", [256, 1024, 4096])
+@pytest.mark.parametrize("splitk", [False, True])   # cluster ring (kernel 10) / all-SM streaming (8)
+def test_fused_segments_parity(sa, segs, K, splitk):
     x = synth.gen_x(1, K, seed=synth.seed_for(8, 2, K))
     cases = [_case(sa, q, N, K, synth.seed_for(8, 30 + i, q)) for i, (q, N) in enumerate(segs)]
-    ys = sa.lut_gemv_fused(x.to(DEV), [c[0] for c in cases], pdl=True)
+    ys = sa.lut_gemv_fused(x.to(DEV), [c[0] for c in cases], pdl=True, splitk=splitk)
     torch.cuda.synchronize()
     for (layer, planes, exps), y in zip(cases, ys):
         err = oracle.err_floor(y.float().cpu().numpy()[None, :], oracle.gemm(x.numpy(), planes, exps, 128))
@@ -135,6 +136,39 @@ def test_stream_basis_vector_and_odd_symmetry_exact(sa):
     ym = sa.lut_gemm(-x, layer, splitk=True)
     torch.cuda.synchronize()
     assert torch.equal(ym.float(), -yp.float())
+
+
+@pytest.mark.parametrize("splitk", [False, True])
+def test_fused_basis_vector_odd_symmetry_and_determinism(sa, splitk):
+    """Fused q/k/v-like segments (q 2/3/2, ragged N) on kernel 10 (cluster) and kernel 8: x = e_j
+    gives fp16 of column j of each segment's W_hat exactly; y(-x) = -y(x) and reruns are bit
+    for bit identical."""
+    K, g = 4096, 128
+    segs = [(2, 1000), (3, 777), (2, 1024)]
+    cases = []
+    for i, (q, N) in enumerate(segs):
+        signs, alpha = synth.gen_layer(q, N, K, g, seed=synth.seed_for(8, 70 + i))
+        planes, exps, _ = oracle.pack_canonical(signs.numpy(), alpha.numpy(), g)
+        cases.append((sa.pack(signs.to(DEV), alpha.to(DEV), g, layout=sa.LAYOUT_TILED),
+                      oracle.dequant(planes, exps, g, K)))
+    layers = [c[0] for c in cases]
+    for j in (0, 255, 256, 4095):
+        x = torch.zeros(K, dtype=torch.float16)
+        x[j] = 1.0
+        ys = sa.lut_gemv_fused(x.to(DEV), layers, splitk=splitk)
+        torch.cuda.synchronize()
+        for (L, W), y in zip(cases, ys):
+            assert torch.equal(y.cpu(), torch.from_numpy(W[:, j]).to(torch.float16)), (j, L.N)
+    x = synth.gen_x(1, K, seed=3).view(-1).to(DEV)
+    yp = [y.clone() for y in sa.lut_gemv_fused(x, layers, splitk=splitk)]
+    ym = sa.lut_gemv_fused(-x, layers, splitk=splitk)
+    torch.cuda.synchronize()
+    for a, b in zip(yp, ym):
+        assert torch.equal(b.float(), -a.float())
+    yr = sa.lut_gemv_fused(x, layers, splitk=splitk)
+    torch.cuda.synchronize()
+    for a, b in zip(yp, yr):
+        assert torch.equal(a, b)
 
 
 # ----------------------------------------------------------------------------- a7 small batch

@@ -33,7 +33,7 @@ for spec in sys.argv[1:]:
         if len(segs) == 1:
             sa.lut_gemm(x.view(1, -1), copies[t % R][0], out=outs[0].view(1, -1), workspace=ws, pdl=True)
         else:
-            sa.lut_gemv_fused(x, copies[t % R], outs=outs, workspace=ws, pdl=True)
+            sa.lut_gemv_fused(x, copies[t % R], outs=outs, workspace=ws, pdl=True, splitk=os.environ.get("SPLITK") == "1")
     with torch.cuda.stream(s):
         for t in range(3):
             call(t)
