@@ -412,6 +412,7 @@ def main():
     ap.add_argument("--impl", default="shiftadd", choices=["shiftadd", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-layers", action="store_true", help="skip the per-layer rows")
+    ap.add_argument("--no-program", action="store_true", help="skip the persistent-program (kernel 9) row")
     ap.add_argument("--dry-run", action="store_true", help="N>1 plumbing only: build the shards, run 2 steps")
     args = ap.parse_args()
     if args.warmup < 3:
@@ -533,6 +534,19 @@ def main():
                               "plane_GBps": round(pbk / us * 1e-3, 1)})
         dom = max(kern_rows, key=lambda r: r["us_per_step"])
 
+        # ---- the same step as ONE persistent launch (kernel 9, shiftadd_lut_gemv_program):
+        # every call waits for the previous one's outputs, as the PDL chain does (N = 1 only)
+        program_row = None
+        if group is None and not args.no_program:
+            prog = sa.Program([(Lc.x, Lc.layers, Lc.outs, j > 0) for j, Lc in enumerate(launches)])
+            us_p = graph_time_us(lambda _t: prog(stream=stream), 20, stream)
+            program_row = {"kernel": 9, "name": KERNEL_NAMES[9], "us_per_token": round(us_p, 2),
+                           "GBps": round(step_bytes_full / us_p * 1e-3, 1),
+                           "frac": round(step_bytes_full / us_p * 1e-3 / peak, 4),
+                           "note": "one cooperative launch per token, calls ordered by a completion counter; "
+                                   "slower than the 128-launch PDL chain (DESIGN.md §6, kernel 9)"}
+            del prog
+
         # ---- per-layer rows (this rank's shard shapes)
         per_layer = []
         if not args.no_layers:
@@ -646,7 +660,7 @@ def main():
                        "l2_defeat": "inputs larger than L2: the step reads all %.2f GB of resident weights "
                                     "once (L2 %d MB)" % (step_bytes_full / ws_size / 1e9, l2 >> 20),
                        "parallelism": ("N-shard x%d + NCCL all-gather per launch" % ws_size) if ws_size > 1
-                       else "single GPU", "pdl": True, "layers": per_layer},
+                       else "single GPU", "pdl": True, "persistent_program": program_row, "layers": per_layer},
             "roofline": roofline,
             "clocks": clocks,
             "gpu_launches": args.steps * len(launches),

@@ -46,10 +46,26 @@ for i, (q, N) in enumerate([(2, 96), (3, 40), (1, 33)]):
     s, a = synth.gen_layer(q, N, K, 128, seed=synth.seed_for(12, 50 + i))
     p, e, _ = oracle.pack_canonical(s.numpy(), a.numpy(), 128)
     cases.append((sa.pack(s.to(dev), a.to(dev), 128, layout=sa.LAYOUT_TILED), p, e))
-ys = sa.lut_gemv_fused(x.to(dev), [c[0] for c in cases], pdl=True)
+for splitk in (False, True):                  # cluster ring (10) / streaming (8)
+    ys = sa.lut_gemv_fused(x.to(dev), [c[0] for c in cases], pdl=True, splitk=splitk)
+    torch.cuda.synchronize()
+    for (L, p, e), y in zip(cases, ys):
+        check("fused splitk=%s" % splitk, y, oracle.gemm(x.numpy(), p, e, 128))
+# persistent decode program (9): call 1 reads call 0's output (SHIFTADD_CALL_WAIT)
+sA, aA = synth.gen_layer(2, 256, 1024, 128, seed=synth.seed_for(12, 71))
+sB, aB = synth.gen_layer(3, 64, 256, 128, seed=synth.seed_for(12, 72))
+pA, eA, _ = oracle.pack_canonical(sA.numpy(), aA.numpy(), 128)
+pB, eB, _ = oracle.pack_canonical(sB.numpy(), aB.numpy(), 128)
+LA = sa.pack(sA.to(dev), aA.to(dev), 128, layout=sa.LAYOUT_TILED)
+LB = sa.pack(sB.to(dev), aB.to(dev), 128, layout=sa.LAYOUT_TILED)
+xa = synth.gen_x(1, 1024, seed=7)
+yA = torch.empty(256, dtype=torch.float16, device=dev)
+yB = torch.empty(64, dtype=torch.float16, device=dev)
+sa.Program([(xa.to(dev), [LA], [yA], False), (yA, [LB], [yB], True)])()
 torch.cuda.synchronize()
-for (L, p, e), y in zip(cases, ys):
-    check("fused", y, oracle.gemm(x.numpy(), p, e, 128))
+refA = oracle.gemm(xa.numpy(), pA, eA, 128)
+check("program call 0", yA, refA)
+check("program call 1", yB, oracle.gemm(oracle.to_fp16(refA).astype("float64"), pB, eB, 128))
 # block-wise: scaled LUTs (N % 128 == 0) and per-query scales
 for N in (256, 40):
     s, a = synth.gen_layer_blockwise(2, N, 1024, seed=synth.seed_for(12, 60, N))

@@ -55,9 +55,9 @@ def launches(path, tag):
            "Cold-cache, serialised per-launch times (`--metrics gpu__time_duration.sum --clock-control none`):",
            "compare SHARES, not absolutes.  The list covers the whole process: layer synthesis (torch",
            "RNG/elementwise kernels) and packing (`pack_*`, one-time per layer) precede the timed region;",
-           "a decode step launches only LUT-GEMV kernels -- `lut_stream_kernel` (q/k/v fused, gate/up fused",
-           "where the bit widths differ, down_proj) and `gemv_cluster_ring_kernel` (o_proj, gate/up",
-           "concatenated) -- plus the e2e leg's `copy_kernel`.", "",
+           "a decode step launches only LUT-GEMV kernels -- `gemv_cluster_fused_kernel` (q/k/v fused),",
+           "`gemv_cluster_ring_kernel` (o_proj, gate/up concatenated), `lut_stream_kernel` (down_proj, gate/up",
+           "fused where the bit widths differ) -- plus the e2e leg's `copy_kernel`.", "",
            "| kernel | launches | total us | share of whole process |", "|---|---|---|---|"]
     for name, (n, us) in sorted(per.items(), key=lambda kv: -kv[1][1]):
         out.append("| `%s` | %d | %.1f | %.1f%% |" % (name, n, us, 100 * us / tot))
@@ -104,7 +104,8 @@ if __name__ == "__main__":
     launches(sys.argv[2], tag)
     # dram traffic per launch of every captured kernel, keyed by kernel id (bench.py's
     # roofline.traffic reads the dominant kernel's entry)
-    ids = {"lut_stream_kernel": 8, "gemv_cluster_ring_kernel": 3}
+    ids = {"lut_stream_kernel": 8, "gemv_cluster_ring_kernel": 3, "gemv_cluster_fused_kernel": 10,
+           "lut_program_kernel": 9}
     per_kernel = defaultdict(list)
     for rep in sys.argv[3:]:
         raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
@@ -121,9 +122,9 @@ if __name__ == "__main__":
             per_kernel[str(kid)].append(t)
     out = {"round": tag, "kernels": {k: sum(v) / len(v) for k, v in per_kernel.items()},
            "per_launch_bytes": dict(per_kernel),
-           "note": "dram__bytes_read.sum + dram__bytes_write.sum per launch of the full captures (tools/evidence.sh): "
-                   "kernel 8 = block 0 q/k/v fused, block 0 down_proj, block 1 q/k/v fused; kernel 3 = block 0 "
-                   "o_proj, block 0 gate/up concatenated"}
+           "note": "dram__bytes_read.sum + dram__bytes_write.sum per launch of the full captures (tools/evidence.sh); "
+                   "the first launches of each kernel in a decode step: kernel 10 = q/k/v fused, kernel 3 = o_proj "
+                   "and gate/up concatenated, kernel 8 = down_proj (and gate/up fused in blocks 20-31)"}
     with open(os.path.join(PROF, "ncu_traffic.json"), "w") as f:
         json.dump(out, f, indent=1)
     print("ok", tag, out["kernels"])

@@ -15,6 +15,7 @@ variant = int(os.environ.get("VARIANT", "0"))
 L.shiftadd_dev_set_variant(variant)
 dev = torch.device("cuda:0")
 l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+PER_SM = {}
 names = ["start", "wait", "lut", "stage0", "loop0", "owner", "loopall", "t0data"]
 for spec in sys.argv[1:]:
     N, K, q = map(int, spec.split(":"))
@@ -66,3 +67,27 @@ for spec in sys.argv[1:]:
     print("   cycles (warp 0): unit1 wait %.0f dot %.0f emit %.0f; loop after LUT %.0f; owner: t0 data %.0f first-stale %.0f spins %.1f (avg)" %
           tuple(cyc.mean(0).tolist()), flush=True)
     print("   max: t0 data %.0f spins %.0f" % (cyc[:, 4].max(), cyc[:, 6].max()), flush=True)
+    # per-CTA: does the loop end follow the CTA's start (streaming-bound) or not (consumer-bound)?
+    st, le = rel[:, 0], rel[:, 4]
+    ok = (t[:, 0] > 0) & (t[:, 4] > 0)
+    st, le = st[ok], le[ok]
+    cc = float(torch.corrcoef(torch.stack([st, le]))[0, 1])
+    order = torch.argsort(st)
+    print("   corr(start, loop end) = %.2f; earliest starters' loop end %.2f, latest starters' %.2f" % (
+        cc, float(le[order[:20]].mean()), float(le[order[-20:]].mean())), flush=True)
+    # per-SM loop duration (LUT done -> loop end): is the slowness a property of the SM?
+    smid = tr.view(148, 16)[:, 15].cpu().long()
+    dur = (rel[:, 4] - rel[:, 2])
+    PER_SM.setdefault(spec, {})
+    for c in range(148):
+        PER_SM[spec][int(smid[c])] = float(dur[c])
+if len(PER_SM) >= 2:
+    specs = list(PER_SM)
+    a, b = PER_SM[specs[0]], PER_SM[specs[1]]
+    sms = sorted(set(a) & set(b))
+    va = torch.tensor([a[s] for s in sms]); vb = torch.tensor([b[s] for s in sms])
+    print("per-SM loop duration correlation between %s and %s: %.2f" % (specs[0], specs[1],
+          float(torch.corrcoef(torch.stack([va, vb]))[0, 1])))
+    slow = sorted(sms, key=lambda s: -a[s])[:12]
+    print("slowest SMs in %s:" % specs[0], slow, " their rank in %s:" % specs[1],
+          [sorted(sms, key=lambda s: -b[s]).index(s) for s in slow])
