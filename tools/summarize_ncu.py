@@ -117,6 +117,8 @@ if __name__ == "__main__":
             kid = next((v for k, v in ids.items() if k in kname), None)
             if kid is None or "dram__bytes_read.sum" not in hdr:
                 continue
+            if "70b" in os.path.basename(rep):   # a per-layer shape, not a launch of the step
+                kid = "%s_llama70b" % kid
             ir, iw = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
             t = to_bytes(vals[ir], units[ir]) + to_bytes(vals[iw], units[iw])
             per_kernel[str(kid)].append(t)
