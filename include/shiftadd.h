@@ -309,8 +309,10 @@ shiftadd_status shiftadd_bcq_quantize(const float* w, int N, int K, int q, int g
  *   pointers (flag arrays uint32[P], zero-initialised); epoch: device uint32, starts at 0,
  *   one per (rank, layer).  2 <= P <= 8.
  *   workspace: shiftadd_workspace_bytes(...) and >= 256 KB + 16 B (a launch counter at
- *   byte 256 KB, left zero).  Supported: tiled layout, shapes the cluster kernel takes
- *   (K <= 4096; shiftadd_gemm_plan kernel id 3); otherwise SHIFTADD_ERR_UNSUPPORTED.
+ *   byte 256 KB, left zero).  Supported: tiled layout; K <= 4096 shapes the cluster kernel
+ *   takes (kernel id 3), and 512 <= K <= 256 x #SMs with 16-B aligned exps on the all-SM
+ *   streaming kernel (id 8, whose owner CTAs store into the peers); otherwise
+ *   SHIFTADD_ERR_UNSUPPORTED.
  *   The wait traps (CUDA error) after ~5 s without progress instead of hanging. */
 shiftadd_status shiftadd_lut_gemv_gather(const uint16_t* x, const uint8_t* planes, const int8_t* exps, int layout,
                                          int N, int K, int q, int g, uint16_t* const* y_peers,

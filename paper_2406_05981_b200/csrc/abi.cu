@@ -441,8 +441,36 @@ shiftadd_status shiftadd_lut_gemv_gather(const uint16_t* x, const uint8_t* plane
   if (!aligned(x, 16) || !aligned(planes, 16)) return fail(SHIFTADD_ERR_INVALID, "misaligned x / planes");
   DevInfo di;
   if ((st = device_info(&di)) != SHIFTADD_OK) return st;
-  if (!cluster_applicable(N, K, q, di.sms))
-    return fail(SHIFTADD_ERR_UNSUPPORTED, "fused gather: K=%d N=%d q=%d outside the cluster kernel", K, N, q);
+  if (!cluster_applicable(N, K, q, di.sms) || K > 4096) {
+    // K > 4096 (LLaMA-2-70B down_proj, OPT-66B fc2 shards): the all-SM streaming kernel (8),
+    // its owner CTAs storing into every rank's buffer
+    if (K < 2 * kTileK || !stream_shape_ok(K, di.sms) || !aligned(exps, 16))
+      return fail(SHIFTADD_ERR_UNSUPPORTED, "fused gather: K=%d N=%d q=%d has no kernel", K, N, q);
+    const size_t need = stream_workspace_bytes(1, K / kTileK, (N + kTileRows - 1) / kTileRows);
+    if (workspace_bytes < need)
+      return fail(SHIFTADD_ERR_INVALID, "workspace needs %zu bytes (got %zu)", need, workspace_bytes);
+    StreamLaunch L = {};
+    L.x = reinterpret_cast<const __half*>(x);
+    L.M = 1;
+    L.ldx = K;
+    L.K = K;
+    L.nseg = 1;
+    L.seg[0] = StreamSeg{planes, exps, nullptr, q, N};
+    L.workspace = workspace;
+    L.grid = di.sms;
+    L.su = 16;
+    L.nst = stream_stages(q, kStreamSmemBudget, L.su, 1);
+    L.pdl = (flags & SHIFTADD_FLAG_PDL) ? 1 : 0;
+    L.gather.y_peers = reinterpret_cast<__half* const*>(y_peers);
+    L.gather.flag_peers = flag_peers;
+    L.gather.counter = reinterpret_cast<unsigned*>(static_cast<char*>(workspace) + kCounterBytes);
+    L.gather.P = P;
+    L.gather.rank = rank;
+    L.gather.epoch = epoch;
+    const cudaError_t e = launch_lut_stream(L, reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "lut_gemv_gather (streaming) launch");
+    return SHIFTADD_OK;
+  }
   GemmArgs a;
   a.x = reinterpret_cast<const __half*>(x);
   a.ldx = K;

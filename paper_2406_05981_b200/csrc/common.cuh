@@ -184,6 +184,28 @@ struct GatherArgs {
   int rank = 0;
 };
 
+// NEXT-f3 completion signal (kernels 3 and 8).  After bar.sync, thread 0 of every CTA adds 1
+// to the launch counter with a gpu-scope acq_rel atomic (its release half covers the CTA's
+// peer stores, cumulative through the barrier).  The last CTA -- whose acquire observed every
+// other CTA's release -- re-arms the counter and publishes the call number into flag[rank] of
+// every rank with one release pattern (fence.acq_rel.sys, then relaxed system-scope stores).
+__device__ __forceinline__ void gather_signal(const GatherArgs& ga) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned prev;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(ga.counter) : "memory");
+    if (prev == gridDim.x - 1) {
+      // one release pattern for all P flags: fence.acq_rel.sys + strong relaxed stores
+      // (st.release.sys per flag compiles to a MEMBAR.ALL.SYS each)
+      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(ga.counter) : "memory");
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+      for (int r = 0; r < ga.P; ++r)
+        asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(ga.flag_peers[r] + ga.rank), "r"(*ga.epoch + 1u)
+                     : "memory");
+    }
+  }
+}
+
 struct GemmArgs {
   const __half* x;
   int ldx;
@@ -222,6 +244,7 @@ struct StreamLaunch {
   int half;   // 1: the co-resident variant (<= 113 KB shared memory, two CTAs fit one SM)
   const int8_t* exps_bw;   // non-null: NEXT-f1 block-wise exponents [q][8][K/8] (M = 1, one segment)
   int colwise;             // 1: exps_bw holds NEXT-f1 column-wise exponents [q][K] instead
+  GatherArgs gather;       // NEXT-f3 (M = 1, one segment, K >= 512): y into every rank's buffer
 };
 
 // The persistent decode program (lut_program.cu, kernel id 9): ordered calls of the fused form.

@@ -255,30 +255,10 @@ __host__ __device__ constexpr int cl_ring(int Q, int REGS) {
   return (REGS - 56) / (5 * Q) < 1 ? 1 : ((REGS - 56) / (5 * Q) > 8 ? 8 : (REGS - 56) / (5 * Q));
 }
 
-// NEXT-f3 completion signal.  After bar.sync, thread 0 of every CTA adds 1 to the launch
-// counter with a gpu-scope acq_rel atomic (its release half covers the CTA's peer stores,
-// cumulative through the barrier).  The last CTA -- whose acquire observed every other
-// CTA's release -- re-arms the counter and publishes `epoch` into flag[rank] of every rank
-// with one release pattern (fence.acq_rel.sys, then relaxed system-scope stores).  Causality is transitive through the two
-// synchronising pairs (gpu scope inside this GPU, system scope to the peers), so a consumer
-// that acquires all P flags == epoch sees every rank's whole y shard.  (A system-scope
-// fence or atomic in every CTA measured 6-12 us per launch; one in the last CTA is cheap.)
-__device__ __forceinline__ void gather_signal(const GatherArgs& ga) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned prev;
-    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(ga.counter) : "memory");
-    if (prev == gridDim.x - 1) {
-      // one release pattern for all P flags: fence.acq_rel.sys + strong relaxed stores
-      // (st.release.sys per flag compiles to a MEMBAR.ALL.SYS each)
-      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(ga.counter) : "memory");
-      asm volatile("fence.acq_rel.sys;" ::: "memory");
-      for (int r = 0; r < ga.P; ++r)
-        asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(ga.flag_peers[r] + ga.rank), "r"(*ga.epoch + 1u)
-                     : "memory");
-    }
-  }
-}
+// NEXT-f3 completion signal: gather_signal (common.cuh).  Causality is transitive through the
+// two synchronising pairs (gpu scope inside this GPU, system scope to the peers), so a consumer
+// that acquires all P flags == epoch sees every rank's whole y shard.  (A system-scope fence
+// or atomic in every CTA measured 6-12 us per launch; one in the last CTA is cheap.)
 
 // Items of a CTA: i = t * RGb + rgl (slice t of its Sc, row group rgl of the band), warp w
 // takes i = w, w + NW, ...; item i is tiled-layout unit (s0 + t) * RG + rg0 + rgl.  The

@@ -86,6 +86,7 @@ struct StreamParams {
   const int8_t* exps_bw;   // NEXT-f1 block-wise exponents [q][8][K/8] (BW kernels; planes only in the ring)
   int bw_rows;             // rows per block, N / 8
   int bw_rgb;              // BW = 2: row groups per block (N / 128)
+  GatherArgs ga;           // NEXT-f3 fused all-gather epilogue (P == 0: off)
 };
 
 // Consumer side of one run (slice s, segment sg, row groups [rga, re)): the run's stages of su
@@ -848,8 +849,17 @@ __global__ void __launch_bounds__((NWC + 1) * 32, MINB) lut_stream_kernel(const 
     int g = 0;
     while (g + 1 < p.nseg && p.seg[g + 1].rgoff <= rgf) ++g;
     const int nl = nf - p.seg[g].rgoff * kTileRows;
-    if (nl < p.seg[g].N) p.seg[g].y[(size_t)m * p.ldy + nl] = __float2half_rn(sum);
+    if (nl < p.seg[g].N) {
+      const __half hv = __float2half_rn(sum);
+      if (p.ga.P == 0) {
+        p.seg[g].y[(size_t)m * p.ldy + nl] = hv;
+      } else {   // NEXT-f3: straight into every rank's gathered y (peer memory), buffer by call parity
+        const int b = (int)((*p.ga.epoch + 1u) & 1u);
+        for (int rr = 0; rr < p.ga.P; ++rr) p.ga.y_peers[b * p.ga.P + rr][(size_t)p.ga.rank * p.seg[0].N + nl] = hv;
+      }
+    }
   }
+  if (p.ga.P > 0) gather_signal(p.ga);   // (starts with __syncthreads)
   __syncthreads();
   trace_at(5);
   // this CTA's share of the call's 2^32 (see the header comment)
@@ -961,6 +971,7 @@ cudaError_t launch_lut_stream(const StreamLaunch& L, cudaStream_t stream) {
   p.slot_planes = L.su * qmax * kTileBytes;
   p.pdl = L.pdl;
   p.exps_bw = L.exps_bw;
+  p.ga = L.gather;
   p.bw_rows = L.seg[0].N / 8;
   p.bw_rgb = (L.exps_bw && L.seg[0].N % 128 == 0) ? L.seg[0].N / 128 : 0;
   if (L.exps_bw && L.colwise) p.bw_rgb = (L.seg[0].N + kTileRows - 1) / kTileRows;   // one row block

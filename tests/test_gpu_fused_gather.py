@@ -76,7 +76,10 @@ def _worker(rank, world, port, q, N, K, g, calls, out_q, graph):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("q,N,K,graph", [(3, 4096, 4096, False), (2, 1536, 768, False), (3, 4096, 4096, True)])
+# K > 4096 shards (the LLaMA-2-70B down_proj / OPT-66B fc2 regime) run on the all-SM streaming
+# kernel (8) with the same peer-store + flag protocol; K <= 4096 on the cluster kernel (3)
+@pytest.mark.parametrize("q,N,K,graph", [(3, 4096, 4096, False), (2, 1536, 768, False), (3, 4096, 4096, True),
+                                         (3, 2048, 9216, False), (2, 1024, 28672, True)])
 def test_fused_gather_two_ranks_one_gpu(q, N, K, graph):
     world, g, calls = 2, 128, 4
     ctx = mp.get_context("spawn")
