@@ -228,10 +228,17 @@ shiftadd_status shiftadd_lut_gemv_colwise(const uint16_t* x, const uint8_t* plan
  *   plane i's LUT from x[k] 2^{e_i[k]} and reduces the K-split through `workspace`
  *   (shiftadd_workspace_bytes_colwise(N, K) bytes, same zero-once contract as
  *   shiftadd_lut_gemm).  flags: 0 or SHIFTADD_FLAG_PDL | SHIFTADD_FLAG_SPLITK. */
+/* shiftadd_lut_gemm_colwise: the same for M <= 16 batch rows x [M][K] (row stride ldx, a
+ *   multiple of 8), y [M][N] (row stride ldy) -- a7 with column-wise scales: pairs of rows
+ *   share one weight pass (plane LUT entries hold the fp16 pair of both rows' sums, built in
+ *   fp32 and rounded once, PAPER.md:186's FP16 LUT); M = 1 is shiftadd_lut_gemv_colwise_ws. */
 size_t shiftadd_workspace_bytes_colwise(int N, int K);
 shiftadd_status shiftadd_lut_gemv_colwise_ws(const uint16_t* x, const uint8_t* planes, const int8_t* exps_col,
                                              int layout, int N, int K, int q, uint16_t* y, void* workspace,
                                              size_t workspace_bytes, unsigned flags, void* stream);
+shiftadd_status shiftadd_lut_gemm_colwise(const uint16_t* x, int ldx, const uint8_t* planes, const int8_t* exps_col,
+                                          int layout, int M, int N, int K, int q, uint16_t* y, int ldy,
+                                          void* workspace, size_t workspace_bytes, unsigned flags, void* stream);
 
 /* NEXT-f1 -- block-wise scales, "Ours (Lat.)" (Fig. 4(a)): "a block-wise
  * scaling factor design that groups 8 columns and 1/8 of the original rows to share a scaling

@@ -94,6 +94,9 @@ def lib():
         L.shiftadd_lut_gemv_colwise_ws.restype = c_int
         L.shiftadd_lut_gemv_colwise_ws.argtypes = [vp, vp, vp, c_int, c_int, c_int, c_int, vp, vp, c_size,
                                                    ctypes.c_uint, vp]
+        L.shiftadd_lut_gemm_colwise.restype = c_int
+        L.shiftadd_lut_gemm_colwise.argtypes = [vp, c_int, vp, vp, c_int, c_int, c_int, c_int, c_int, vp, c_int, vp,
+                                                c_size, ctypes.c_uint, vp]
         L.shiftadd_pack_apot2.restype = c_int
         L.shiftadd_pack_apot2.argtypes = [vp, vp, c_int, c_int, c_int, c_int, c_int, vp, vp, vp, vp, vp]
         L.shiftadd_lut_gemm_apot2.restype = c_int
@@ -342,18 +345,23 @@ def lut_gemv_blockwise(x: torch.Tensor, layer: PackedLayer, out: torch.Tensor | 
 
 def lut_gemv_colwise(x: torch.Tensor, layer: PackedLayer, out: torch.Tensor | None = None, pdl: bool = False,
                      stream=None, workspace: "Workspace | None" = None, splitk: bool = False) -> torch.Tensor:
-    """NEXT-f1: y[N] = x[K] (.) a column-wise-scaled layer, fp16 (shiftadd_lut_gemv_colwise_ws:
-    the cluster kernel for K <= 4096, else -- or with splitk -- the all-SM streaming kernel)."""
+    """NEXT-f1: y = x (.) a column-wise-scaled layer, fp16 (shiftadd_lut_gemm_colwise).  x: [K]
+    or [1][K] (returns [N]) or [M][K] with M <= 16 (returns [M][N]).  M = 1: the cluster kernel for
+    K <= 4096, else -- or with splitk -- the all-SM streaming kernel; M > 1: pairs of rows per
+    weight pass on the streaming kernel."""
     if not layer.colwise:
         raise ValueError("layer was not packed with pack_colwise")
-    xv = x.reshape(-1)
-    if xv.dtype != torch.float16 or not xv.is_cuda or xv.numel() != layer.K:
-        raise ValueError("x must be fp16 [K] on the layer's device")
-    xv = xv.contiguous()
+    vec = x.dim() == 1
+    x2 = x.reshape(1, -1) if vec else x
+    if x2.dtype != torch.float16 or not x2.is_cuda or x2.shape[1] != layer.K or x2.dim() != 2:
+        raise ValueError("x must be fp16 [K] or [M][K] on the layer's device")
+    x2 = x2.contiguous()
+    M = x2.shape[0]
     if out is None:
-        out = torch.empty(layer.N, dtype=torch.float16, device=layer.device)
-    if out.dtype != torch.float16 or out.numel() != layer.N or not out.is_contiguous():
-        raise ValueError("out must be contiguous fp16 [N]")
+        out = torch.empty((M, layer.N), dtype=torch.float16, device=layer.device)
+    out2 = out.reshape(M, layer.N)
+    if out.dtype != torch.float16 or not out.is_contiguous():
+        raise ValueError("out must be contiguous fp16 [M][N]")
     dev = layer.device
     if torch.cuda.current_device() != dev.index:
         torch.cuda.set_device(dev)
@@ -361,13 +369,13 @@ def lut_gemv_colwise(x: torch.Tensor, layer: PackedLayer, out: torch.Tensor | No
     ws = (workspace or _workspace_for(dev, stream)).get(need)
     sptr = (stream if stream is not None else torch.cuda.current_stream(dev)).cuda_stream
     flags = (FLAG_PDL if pdl else 0) | (FLAG_SPLITK if splitk else 0)
-    st = lib().shiftadd_lut_gemv_colwise_ws(xv.data_ptr(), layer.planes.data_ptr(), layer.exps.data_ptr(),
-                                            layer.layout, layer.N, layer.K, layer.q, out.data_ptr(),
-                                            ws.data_ptr() if ws is not None else None,
-                                            ws.numel() if ws is not None else 0, flags, sptr)
+    st = lib().shiftadd_lut_gemm_colwise(x2.data_ptr(), layer.K, layer.planes.data_ptr(), layer.exps.data_ptr(),
+                                         layer.layout, M, layer.N, layer.K, layer.q, out2.data_ptr(), layer.N,
+                                         ws.data_ptr() if ws is not None else None,
+                                         ws.numel() if ws is not None else 0, flags, sptr)
     if st:
-        _check(st, "shiftadd_lut_gemv_colwise_ws")
-    return out
+        _check(st, "shiftadd_lut_gemm_colwise")
+    return out.reshape(layer.N) if M == 1 else out
 
 
 def workspace_bytes(layer: PackedLayer, M: int) -> int:

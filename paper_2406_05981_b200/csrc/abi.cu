@@ -238,7 +238,65 @@ shiftadd_status shiftadd_lut_gemv_colwise(const uint16_t* x, const uint8_t* plan
 
 size_t shiftadd_workspace_bytes_colwise(int N, int K) {
   if (N < 1 || N > kMaxRows || K < kTileK || K % kTileK) return 0;
-  return stream_workspace_bytes(1, K / kTileK, (N + kTileRows - 1) / kTileRows);
+  return stream_workspace_bytes(2, K / kTileK, (N + kTileRows - 1) / kTileRows);   // covers M = 1 and pairs
+}
+
+shiftadd_status shiftadd_lut_gemm_colwise(const uint16_t* x, int ldx, const uint8_t* planes, const int8_t* exps_col,
+                                          int layout, int M, int N, int K, int q, uint16_t* y, int ldy,
+                                          void* workspace, size_t workspace_bytes, unsigned flags, void* stream) {
+  if (M == 1)
+    return shiftadd_lut_gemv_colwise_ws(x, planes, exps_col, layout, N, K, q, y, workspace, workspace_bytes, flags,
+                                        stream);
+  if (!x || !planes || !exps_col || !y) return fail(SHIFTADD_ERR_INVALID, "null pointer argument");
+  if (M < 1 || M > 16) return fail(SHIFTADD_ERR_UNSUPPORTED, "M=%d outside [1, 16]", M);
+  shiftadd_status st = check_shape(q, N, K, 8, 4);
+  if (st != SHIFTADD_OK) return st;
+  if ((st = check_layout(layout, K, 128)) != SHIFTADD_OK) return st;
+  if (layout != SHIFTADD_LAYOUT_TILED)
+    return fail(SHIFTADD_ERR_UNSUPPORTED, "column-wise GEMM needs the tiled layout");
+  if (flags & ~(SHIFTADD_FLAG_PDL | SHIFTADD_FLAG_SPLITK)) return fail(SHIFTADD_ERR_INVALID, "unknown flags 0x%x", flags);
+  if (ldx < K || ldy < N) return fail(SHIFTADD_ERR_INVALID, "ldx < K or ldy < N");
+  if (!aligned(x, 16) || (ldx % 8) || !aligned(planes, 16) || !aligned(exps_col, 8) || !aligned(y, 2))
+    return fail(SHIFTADD_ERR_INVALID, "misaligned pointer (x rows, planes 16 B; exps_col 8 B)");
+  DevInfo di;
+  if ((st = device_info(&di)) != SHIFTADD_OK) return st;
+  if (!stream_shape_ok(K, di.sms)) return fail(SHIFTADD_ERR_UNSUPPORTED, "column-wise GEMM: K=%d above 256 x #SMs", K);
+  const size_t need = shiftadd_workspace_bytes_colwise(N, K);
+  if (need > 0 && (!workspace || workspace_bytes < need || !aligned(workspace, 16)))
+    return fail(SHIFTADD_ERR_INVALID, "workspace needs %zu bytes, 16-B aligned (got %zu)", need, workspace_bytes);
+  // pairs of rows (fp16-pair LUT entries: one weight pass per 2 rows), stream-ordered
+  cudaError_t e = cudaSuccess;
+  for (int m0 = 0; m0 < M && e == cudaSuccess; m0 += 2) {
+    const int mc = M - m0 < 2 ? M - m0 : 2;
+    if (mc == 1) {
+      const shiftadd_status s1 = shiftadd_lut_gemv_colwise_ws(x + (size_t)m0 * ldx, planes, exps_col, layout, N, K, q,
+                                                              y + (size_t)m0 * ldy, workspace, workspace_bytes,
+                                                              flags | SHIFTADD_FLAG_SPLITK, stream);
+      if (s1 != SHIFTADD_OK) return s1;
+      continue;
+    }
+    StreamLaunch L = {};
+    L.x = reinterpret_cast<const __half*>(x) + (size_t)m0 * ldx;
+    L.M = 2;
+    L.ldx = ldx;
+    L.ldy = ldy;
+    L.K = K;
+    L.nseg = 1;
+    L.seg[0] = StreamSeg{planes, exps_col, reinterpret_cast<__half*>(y) + (size_t)m0 * ldy, q, N};
+    L.exps_bw = exps_col;
+    L.colwise = 1;
+    L.workspace = workspace;
+    L.grid = di.sms;
+    L.su = 16;
+    const int lut = q <= 2 ? 64 * 1024 : 128 * 1024;
+    const int slot = L.su * q * (kTileBytes + kTileExps);
+    L.nst = (kStreamSmemBudget - lut - 640) / slot;
+    L.nst = L.nst > 16 ? 16 : L.nst;
+    L.pdl = (flags & SHIFTADD_FLAG_PDL) ? 1 : 0;
+    e = launch_lut_stream(L, reinterpret_cast<cudaStream_t>(stream));
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "lut_gemm_colwise launch");
+  return SHIFTADD_OK;
 }
 
 shiftadd_status shiftadd_lut_gemv_colwise_ws(const uint16_t* x, const uint8_t* planes, const int8_t* exps_col,
@@ -277,7 +335,7 @@ shiftadd_status shiftadd_lut_gemv_colwise_ws(const uint16_t* x, const uint8_t* p
   L.su = 16;
   const int lut = q <= 2 ? 64 * 1024 : 128 * 1024;
   const int slot = L.su * q * (kTileBytes + kTileExps);
-  L.nst = (kStreamSmemBudget - lut - 512) / slot;
+  L.nst = (kStreamSmemBudget - lut - 640) / slot;
   L.nst = L.nst > 16 ? 16 : L.nst;
   L.pdl = (flags & SHIFTADD_FLAG_PDL) ? 1 : 0;
   const cudaError_t e = launch_lut_stream(L, reinterpret_cast<cudaStream_t>(stream));
@@ -339,7 +397,7 @@ shiftadd_status shiftadd_lut_gemv_blockwise(const uint16_t* x, const uint8_t* pl
     L.su = 16;
     const int lut = q <= 2 ? 64 * 1024 : 128 * 1024;
     const int slot = L.su * q * (kTileBytes + kTileExps);
-    L.nst = (kStreamSmemBudget - lut - 512) / slot;
+    L.nst = (kStreamSmemBudget - lut - 640) / slot;
     L.nst = L.nst > 16 ? 16 : L.nst;
   } else {
     L.su = 8;

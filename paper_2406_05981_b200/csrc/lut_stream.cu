@@ -559,7 +559,87 @@ __device__ __forceinline__ float unit_dot_lut(uint32_t sp, const uint32_t (&cst)
   return (pc[0] + pc[1]) + (pc[2] + pc[3]);
 }
 
-template <int NWC, int Q, bool COLW>
+// Column-wise scales for two batch rows (a7 x NEXT-f1): plane i's LUT entry holds the fp16
+// pair (row 0, row 1) of the sums of x_m[k] 2^{e_i[k]} -- built in fp32, rounded once -- at the
+// address of the fp32 entry of the M = 1 layout, so one LDS.32 per key byte serves both rows
+// (each half accumulated into fp32 by one FHADD).
+template <int NWC, int Q>
+__device__ __forceinline__ void build_lut_colw2(const StreamParams& p, int s, int warp, int lane) {
+  const uint64_t pol_keep = policy_evict_last();
+  float v[2][8];
+#pragma unroll
+  for (int m = 0; m < 2; ++m) {
+    uint4 xv = make_uint4(0, 0, 0, 0);
+    if (m < p.M) xv = ldg_keep(p.x + (size_t)m * p.ldx + (size_t)s * kTileK + 8 * lane, pol_keep);
+    const float2 f01 = __half22float2(*reinterpret_cast<const __half2*>(&xv.x));
+    const float2 f23 = __half22float2(*reinterpret_cast<const __half2*>(&xv.y));
+    const float2 f45 = __half22float2(*reinterpret_cast<const __half2*>(&xv.z));
+    const float2 f67 = __half22float2(*reinterpret_cast<const __half2*>(&xv.w));
+    v[m][0] = f01.x; v[m][1] = f01.y; v[m][2] = f23.x; v[m][3] = f23.y;
+    v[m][4] = f45.x; v[m][5] = f45.y; v[m][6] = f67.x; v[m][7] = f67.y;
+  }
+  const int K = p.S * kTileK;
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    const uint2 ev = __ldg(reinterpret_cast<const uint2*>(p.exps_bw + (size_t)i * K + (size_t)s * kTileK + 8 * lane));
+    float w[2][8];
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const float sc = pow2_bits((int)(int8_t)(((b < 4 ? ev.x : ev.y) >> (8 * (b & 3))) & 0xffu));
+      w[0][b] = v[0][b] * sc;
+      w[1][b] = v[1][b] * sc;
+    }
+    const uint32_t col = kDynBase + (uint32_t)(i >> 1) * 65536u + (uint32_t)(i & 1) * 128u + 4u * lane;
+#pragma unroll
+    for (int hh = 0; hh < 16 / NWC; ++hh) {
+      const int hi = warp + hh * NWC;
+      float H[2];
+#pragma unroll
+      for (int m = 0; m < 2; ++m)
+        H[m] = ((hi & 1 ? w[m][4] : -w[m][4]) + (hi & 2 ? w[m][5] : -w[m][5])) +
+               ((hi & 4 ? w[m][6] : -w[m][6]) + (hi & 8 ? w[m][7] : -w[m][7]));
+#pragma unroll
+      for (int lo = 0; lo < 16; ++lo) {
+        float e[2];
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+          const int a = lo & 3, b = lo >> 2;
+          const float A = a == 0 ? -w[m][0] - w[m][1] : a == 1 ? w[m][0] - w[m][1] : a == 2 ? w[m][1] - w[m][0]
+                                                                                              : w[m][0] + w[m][1];
+          const float B = b == 0 ? -w[m][2] - w[m][3] : b == 1 ? w[m][2] - w[m][3] : b == 2 ? w[m][3] - w[m][2]
+                                                                                              : w[m][2] + w[m][3];
+          e[m] = (A + B) + H[m];
+        }
+        asm volatile("st.shared.b32 [%0], %1;" ::"r"(col + ((uint32_t)(hi * 16 + lo) << 8)), "r"(pack_h2(e[0], e[1]))
+                     : "memory");
+      }
+    }
+  }
+}
+
+template <int Q>
+__device__ __forceinline__ void unit_dot_lut2(uint32_t sp, const uint32_t (&cst)[4], float (&acc)[2]) {
+  uint4 w[Q];
+#pragma unroll
+  for (int i = 0; i < Q; ++i) w[i] = lds_u4(sp + i * kTileBytes);
+  float c[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    const uint32_t base = kDynBase + (uint32_t)(i >> 1) * 65536u + (uint32_t)(i & 1) * 128u;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const uint32_t word = (j < 4) ? w[i].x : (j < 8) ? w[i].y : (j < 12) ? w[i].z : w[i].w;
+      uint32_t v;
+      asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(base + prmt(word, cst[j >> 2], step_sel(j))));
+      fhadd_lo(c[j & 1][0], v);
+      fhadd_hi(c[j & 1][1], v);
+    }
+  }
+  acc[0] = c[0][0] + c[1][0];
+  acc[1] = c[0][1] + c[1][1];
+}
+
+template <int NWC, int Q, bool COLW, bool MW2 = false>
 __device__ __forceinline__ void consume_run_lut(const StreamParams& p, const SegDev& sg, int s, int rga, int re,
                                                 RingPos& rp, uint32_t ring, uint32_t full, uint32_t empty,
                                                 const uint32_t (&cst)[4], int wu, int lane, unsigned long long ep,
@@ -572,7 +652,9 @@ __device__ __forceinline__ void consume_run_lut(const StreamParams& p, const Seg
     const int key = s * 8 + b;
     if (key != cur) {   // rebuild the q scaled LUTs for (s, b) (column-wise: for s)
       asm volatile("bar.sync 1, %0;" ::"r"(NWC * 32) : "memory");
-      if (COLW)
+      if (MW2)
+        build_lut_colw2<NWC, Q>(p, s, wu, lane);
+      else if (COLW)
         build_lut_colw<NWC, Q>(xv, p.exps_bw, p.S * kTileK, s, wu, lane);
       else
         build_lut_scaled<NWC, Q>(xv, p.exps_bw, KB, s, b, wu, lane);
@@ -583,7 +665,29 @@ __device__ __forceinline__ void consume_run_lut(const StreamParams& p, const Seg
       const int n = r1 - rg < p.su ? r1 - rg : p.su;
       const uint32_t slot = ring + (uint32_t)(rp.j * p.slot);
       mbar_wait(full + 8 * rp.j, (uint32_t)(rp.k & 1));
-      if (wu < n) {
+      if (wu < n && MW2) {
+        float acc[2];
+        unit_dot_lut2<Q>(slot + (uint32_t)(wu * Q * kTileBytes + 16 * lane), cst, acc);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + 8 * rp.j);
+#pragma unroll
+        for (int m = 0; m < 2; ++m) acc[m] += __shfl_xor_sync(0xffffffffu, acc[m], 1);
+        if (h == 0) {
+          const int u = rg + wu;
+#pragma unroll
+          for (int m = 0; m < 2; ++m) {
+            if (m < p.M) {
+              if (p.S == 1) {
+                const int nl = u * kTileRows + r;
+                if (nl < sg.N) sg.y[(size_t)m * p.ldy + nl] = __float2half_rn(acc[m]);
+              } else {
+                st_relaxed_u64(p.part + ((((size_t)m * p.RGtot + sg.rgoff + u) * p.S) + s) * kTileRows + r,
+                               ep | __float_as_uint(acc[m]));
+              }
+            }
+          }
+        }
+      } else if (wu < n) {
         float acc = unit_dot_lut<Q>(slot + (uint32_t)(wu * Q * kTileBytes + 16 * lane), cst);
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + 8 * rp.j);
@@ -606,16 +710,16 @@ __device__ __forceinline__ void consume_run_lut(const StreamParams& p, const Seg
   }
 }
 
-template <int NWC, bool COLW>
+template <int NWC, bool COLW, bool MW2 = false>
 __device__ __forceinline__ void consume_run_lut_q(const StreamParams& p, const SegDev& sg, int s, int rga, int re,
                                                   RingPos& rp, uint32_t ring, uint32_t full, uint32_t empty,
                                                   const uint32_t (&cst)[4], int wu, int lane, unsigned long long ep,
                                                   const uint4 xv, int& cur) {
   switch (sg.q) {
-    case 1: consume_run_lut<NWC, 1, COLW>(p, sg, s, rga, re, rp, ring, full, empty, cst, wu, lane, ep, xv, cur); break;
-    case 2: consume_run_lut<NWC, 2, COLW>(p, sg, s, rga, re, rp, ring, full, empty, cst, wu, lane, ep, xv, cur); break;
-    case 3: consume_run_lut<NWC, 3, COLW>(p, sg, s, rga, re, rp, ring, full, empty, cst, wu, lane, ep, xv, cur); break;
-    default: consume_run_lut<NWC, 4, COLW>(p, sg, s, rga, re, rp, ring, full, empty, cst, wu, lane, ep, xv, cur); break;
+    case 1: consume_run_lut<NWC, 1, COLW, MW2>(p, sg, s, rga, re, rp, ring, full, empty, cst, wu, lane, ep, xv, cur); break;
+    case 2: consume_run_lut<NWC, 2, COLW, MW2>(p, sg, s, rga, re, rp, ring, full, empty, cst, wu, lane, ep, xv, cur); break;
+    case 3: consume_run_lut<NWC, 3, COLW, MW2>(p, sg, s, rga, re, rp, ring, full, empty, cst, wu, lane, ep, xv, cur); break;
+    default: consume_run_lut<NWC, 4, COLW, MW2>(p, sg, s, rga, re, rp, ring, full, empty, cst, wu, lane, ep, xv, cur); break;
   }
 }
 
@@ -700,7 +804,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, MINB) lut_stream_kernel(const 
         if (two) xb = ldg_keep(p.x + (size_t)(s0 + 1) * kTileK + 8 * lane, pol_keep);
         build_lut<NWC>(xa, 0u, warp, lane);
         if (two) build_lut<NWC>(xb, 128u, warp, lane);
-      } else if (MW != 1) {
+      } else if (MW != 1 && BW != 3) {
         build_lut_mw<NWC, MW>(p, s0, 0, warp, lane);
         if (two && MW < 8) build_lut_mw<NWC, MW>(p, s0 + 1, 1, warp, lane);
       }
@@ -719,7 +823,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, MINB) lut_stream_kernel(const 
     const int r = lane >> 1, h = lane & 1;
     const int wu = warp;
     RingPos rp{0, 0};
-    if (MW == 1) {
+    if (MW == 1 || BW == 3) {   // (column-wise M = 2: fp16-pair entries at the M = 1 addresses)
       uint32_t cst[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -731,7 +835,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, MINB) lut_stream_kernel(const 
       const bool skew = p.skew && warp >= NWC / 2;
       int t = 0;
       uint4 xs[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
-      if (BW >= 2 && any) {
+      if (BW >= 2 && MW == 1 && any) {
         const uint64_t pol_keep = policy_evict_last();
         xs[0] = ldg_keep(p.x + (size_t)s0 * kTileK + 8 * lane, pol_keep);
         if (two) xs[1] = ldg_keep(p.x + (size_t)(s0 + 1) * kTileK + 8 * lane, pol_keep);
@@ -740,8 +844,8 @@ __global__ void __launch_bounds__((NWC + 1) * 32, MINB) lut_stream_kernel(const 
       for (Pos a = start; before(a, end);) {
         const int re = run_end(p, a, end);
         if (BW >= 2) {
-          consume_run_lut_q<NWC, BW == 3>(p, p.seg[a.g], a.s, a.rg, re, rp, ring, full, empty, cst, wu, lane, ep,
-                                 a.s == s0 ? xs[0] : xs[1], cur);
+          consume_run_lut_q<NWC, BW == 3, MW == 2>(p, p.seg[a.g], a.s, a.rg, re, rp, ring, full, empty, cst, wu,
+                                                   lane, ep, a.s == s0 ? xs[0] : xs[1], cur);
         } else if (BW == 1) {
           if (a.s == s0)
             consume_run_bw_q<0u>(p, p.seg[a.g], a.s, a.rg, re, rp, ring, full, empty, cst, wu, lane, ep);
@@ -926,6 +1030,8 @@ cudaError_t launch_lut_stream(const StreamLaunch& L, cudaStream_t stream) {
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(lut_stream_kernel<16, 1, 1, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(lut_stream_kernel<16, 1, 2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    if (e == cudaSuccess)
       e = cudaFuncSetAttribute(lut_stream_kernel<8, 2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 113 * 1024);
     attr_err[dev] = e;
   });
@@ -990,6 +1096,12 @@ cudaError_t launch_lut_stream(const StreamLaunch& L, cudaStream_t stream) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   c.attrs = attr;
   c.numAttrs = L.pdl ? 1 : 0;
+  if (L.exps_bw && L.colwise && MW == 2) {   // column-wise, two batch rows
+    if (L.nseg != 1) return cudaErrorInvalidValue;
+    p.lut_bytes = qmax <= 2 ? kLutSlab : 2 * kLutSlab;
+    c.dynamicSmemBytes = p.lut_bytes + L.nst * p.slot + kBarBytes;
+    return cudaLaunchKernelEx(&c, lut_stream_kernel<16, 1, 2, 3>, p);
+  }
   if (L.exps_bw) {
     if (MW != 1 || L.nseg != 1) return cudaErrorInvalidValue;
     // N % 128 == 0: scaled LUTs per (slice, row block); else the per-query scale (8 consumer

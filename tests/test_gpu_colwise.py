@@ -70,6 +70,40 @@ def test_colwise_gemv_parity(sa, q, N, K, splitk):
     assert err <= TOL, err
 
 
+@pytest.mark.parametrize("q,N,K,M", [(3, 768, 768, 2), (2, 4096, 4096, 3), (4, 1000, 8192, 2), (3, 4096, 11008, 8),
+                                     (1, 40, 512, 16)])
+def test_colwise_small_batch_parity(sa, q, N, K, M):
+    """a7 x column-wise scales: pairs of rows per weight pass (fp16-pair plane LUTs), odd M's
+    last row on the M = 1 path; every row within the oracle bar."""
+    s, a, planes, e = _layer(q, N, K, synth.seed_for(8, 40 + q, M))
+    L = sa.pack_colwise(s.to(DEV), a.to(DEV))
+    x = synth.gen_x(M, K, seed=synth.seed_for(8, 41, M))
+    y = sa.lut_gemv_colwise(x.to(DEV), L, pdl=True)
+    torch.cuda.synchronize()
+    assert tuple(y.shape) == (M, N)
+    err = oracle.err_floor(y.float().cpu().numpy(), oracle.gemm_colwise(x.numpy(), planes, e))
+    assert err <= TOL, err
+
+
+def test_colwise_pair_rows_basis_vectors_exact(sa):
+    """M = 2: row m = e_{j_m} gives the fp16 column j_m exactly (an fp16 LUT entry of one
+    scaled activation is exact), and swapping the rows swaps the outputs bit for bit."""
+    q, N, K = 3, 80, 1024
+    s, a, planes, e = _layer(q, N, K, synth.seed_for(8, 50))
+    L = sa.pack_colwise(s.to(DEV), a.to(DEV))
+    W = oracle.dequant_colwise(planes, e, K)
+    x = torch.zeros((2, K), dtype=torch.float16)
+    x[0, 7] = 1.0
+    x[1, 600] = 1.0
+    y = sa.lut_gemv_colwise(x.to(DEV), L).cpu().numpy()
+    assert np.array_equal(y[0], oracle.to_fp16(W[:, 7])) and np.array_equal(y[1], oracle.to_fp16(W[:, 600]))
+    xr = synth.gen_x(2, K, seed=9)
+    y1 = sa.lut_gemv_colwise(xr.to(DEV), L)
+    y2 = sa.lut_gemv_colwise(xr.flip(0).contiguous().to(DEV), L)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2.flip(0))
+
+
 @pytest.mark.parametrize("K,splitk", [(512, False), (512, True), (8192, False)])
 def test_colwise_basis_vector_gives_rounded_column_exactly(sa, K, splitk):
     q, N = 3, 80

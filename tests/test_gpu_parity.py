@@ -407,6 +407,29 @@ def test_misaligned_exponents_use_register_ring(sa, q, N, K):
         assert oracle.err_floor(y.float().cpu().numpy(), y_ref) <= TOL
 
 
+@pytest.mark.parametrize("q,N,K,M", [(4, 1024, 1024, 5), (2, 4096, 11008, 8), (3, 272, 1024, 16), (4, 300, 4096, 12)])
+def test_misaligned_exponents_small_batch_split_k_kernel(sa, q, N, K, M):
+    """An exponent array that is not 16-B aligned sends M > 1 to the small-batch split-K kernel
+    (gemm_tiled_mb.cu, kernel 2): its row-chunk loop for M > 4 (chunks of 4 rows re-walking the
+    CTA's units, S * ceil(M/4) arrivals per row group) at q = 4 and at the LLaMA-2-7B down_proj
+    shape; the same y as the oracle, and the counter region is left zeroed."""
+    g = 128
+    signs, alpha = synth.gen_layer(q, N, K, g, seed=synth.seed_for(6, 8, q + M), device=DEV)
+    layer = sa.pack(signs, alpha, g, layout=sa.LAYOUT_TILED)
+    buf = torch.empty(layer.exps.numel() + 16, dtype=torch.int8, device=DEV)
+    ex = buf[5:5 + layer.exps.numel()]
+    ex.copy_(layer.exps)
+    assert ex.data_ptr() % 16 != 0
+    moved = sa.PackedLayer(layer.planes, ex, q, N, K, g, layer.layout, layer.counts)
+    x = synth.gen_x(M, K, seed=13 + M)
+    ws = sa.Workspace(DEV)
+    y = sa.lut_gemm(x.to(DEV), moved, workspace=ws, pdl=True)
+    torch.cuda.synchronize()
+    planes, exps, _ = oracle.pack_canonical(signs.cpu().numpy(), alpha.cpu().numpy(), g)
+    assert oracle.err_floor(y.float().cpu().numpy(), oracle.gemm(x.numpy(), planes, exps, g)) <= TOL
+    assert int(ws.buf[:65536 * 4].count_nonzero()) == 0
+
+
 @pytest.mark.parametrize("M,kid", [(2, 5), (3, 6), (4, 6), (7, 8)])
 def test_small_batch_ring_exact_invariants(sa, M, kid):
     """The small-batch kernels (cluster rings with float2 / float4 entries; M = 7: the streaming
