@@ -87,7 +87,35 @@ struct StreamParams {
   int bw_rows;             // rows per block, N / 8
   int bw_rgb;              // BW = 2: row groups per block (N / 128)
   GatherArgs ga;           // NEXT-f3 fused all-gather epilogue (P == 0: off)
+  int dev_mode;            // development builds only (co-roof experiments), 0 otherwise
 };
+
+#ifdef SHIFTADD_DEV_TRACE
+// co-roof experiment (dev builds): the lookups and adds of unit_dot2 with key words made in
+// registers -- no LDS.128 of the staged key bytes (results meaningless)
+template <int Q, uint32_t HOFF>
+__device__ __forceinline__ void unit_dot2_regs(int lane, int seed, const uint32_t (&cst)[4], float (&acc)[2]) {
+  acc[0] = 0.f;
+  acc[1] = 0.f;
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    float pp[2][4];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint32_t b = (uint32_t)(lane * 0x01030507 + seed * 0x0b0d1113 + i * 0x11111111 + u * 0x2f2f2f2f);
+      const uint4 w = make_uint4(b, b * 3u, b * 5u, b * 7u);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const uint32_t word = (j < 4) ? w.x : (j < 8) ? w.y : (j < 12) ? w.z : w.w;
+        const float v = lds_f32(kDynBase + HOFF + prmt(word, cst[j >> 2], step_sel(j)));
+        pp[u][j & 3] = j < 4 ? v : pp[u][j & 3] + v;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) acc[u] += (pp[u][0] + pp[u][1]) + (pp[u][2] + pp[u][3]);
+  }
+}
+#endif
 
 // Consumer side of one run (slice s, segment sg, row groups [rga, re)): the run's stages of su
 // units, taken two at a time -- warp w processes unit w of stage t and unit w of stage t + 1
@@ -122,6 +150,9 @@ __device__ __forceinline__ void consume_run(const StreamParams& p, const SegDev&
     if (rg == rga) trace_clk(8, c0);
     const bool u0 = wu < n0, u1 = wu < n1;
     float acc[2] = {0.f, 0.f};
+#ifdef SHIFTADD_DEV_TRACE
+    if (u0 && (p.dev_mode & 8)) unit_dot2_regs<Q, HOFF>(lane, rg, cst, acc); else
+#endif
     if (u0)
       unit_dot2<Q, HOFF>(slot0 + (uint32_t)(wu * Q * kTileBytes + 16 * lane),
                          slot0 + (uint32_t)(p.slot_planes + wu * Q * kTileExps + lane),
@@ -774,6 +805,13 @@ __global__ void __launch_bounds__((NWC + 1) * 32, MINB) lut_stream_kernel(const 
           }
           const uint32_t bp = (uint32_t)(n * sg.q * kTileBytes), be = BW ? 0u : (uint32_t)(n * sg.q * kTileExps);
           const uint32_t fb = full + 8 * rp.j;
+#ifdef SHIFTADD_DEV_TRACE
+          if (p.dev_mode & 16) {   // co-roof experiment: no copies (no HBM, no TMA writes)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(fb) : "memory");
+            rg += n;
+            continue;
+          }
+#endif
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(bp + be) : "memory");
           const uint32_t dst = ring + (uint32_t)(rp.j * p.slot);
           bulk_g2s(dst, sg.planes + (ub + rg) * sg.q * kTileBytes, bp, fb, pol);
@@ -1085,6 +1123,7 @@ cudaError_t launch_lut_stream(const StreamLaunch& L, cudaStream_t stream) {
   p.skew = 1;
 #ifdef SHIFTADD_DEV_TRACE
   if (g_dev_variant & 2) p.skew = 0;
+  p.dev_mode = g_dev_variant & (8 | 16);
 #endif
   cudaLaunchConfig_t c = {};
   c.gridDim = dim3(L.grid);
