@@ -643,6 +643,21 @@ def main():
     if group is not None:
         torch.distributed.all_reduce(e2e_ms, op=torch.distributed.ReduceOp.MAX, group=group)
     e2e_val = step_bytes_full * e2e_steps / (float(e2e_ms.item()) * 1e-3) / 1e9
+    # the same step issued eagerly through the Python API every time (no graph): includes the
+    # host cost of 130 ctypes calls per token (argument checks, validation, cudaLaunchKernelEx)
+    eager_steps = 20
+    with torch.cuda.stream(stream):
+        e2e_step()
+    barrier()
+    t0 = time.perf_counter()
+    e0.record(stream)
+    with torch.cuda.stream(stream):
+        for _ in range(eager_steps):
+            e2e_step()
+    e1.record(stream)
+    barrier()
+    eager_wall = (time.perf_counter() - t0) / eager_steps
+    eager_dev = e0.elapsed_time(e1) / eager_steps * 1e-3
 
     if rank == 0:
         us_step = ms / args.steps * 1e3
@@ -667,7 +682,11 @@ def main():
             "e2e": {"value": round(e2e_val, 2), "unit": "GB/s", "h2d_bytes_per_step": xh.numel() * 2,
                     "d2h_bytes_per_step": yh.numel() * 2, "steps": e2e_steps,
                     "how": "graph-replayed steps with the step's pinned host inputs copied in and outputs "
-                           "copied out by shiftadd_copy kernels inside the PDL chain"},
+                           "copied out by shiftadd_copy kernels inside the PDL chain",
+                    "eager": {"value": round(step_bytes_full / eager_dev / 1e9, 2), "unit": "GB/s",
+                              "us_per_step": round(eager_dev * 1e6, 1), "wall_us_per_step": round(eager_wall * 1e6, 1),
+                              "how": "the same step issued through the Python API each time (no graph): "
+                                     "130 ctypes calls per token, CUDA events; wall = host clock"}},
         }
         if ws_size == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_leg(sa, dev)
