@@ -325,6 +325,14 @@ shiftadd_status shiftadd_lut_gemv_gather(const uint16_t* x, const uint8_t* plane
                                          int N, int K, int q, int g, uint16_t* const* y_peers,
                                          uint32_t* const* flag_peers, int P, int rank, uint32_t* epoch,
                                          void* workspace, size_t workspace_bytes, unsigned flags, void* stream);
+/* shiftadd_lut_gemm_gather: the same for M <= 8 batch rows (x [M][K], row stride ldx): every
+ *   rank's gathered buffer holds y [M][P*N] (row m at m*P*N, this rank's rows at rank*N);
+ *   M > 1 runs on the all-SM streaming kernel (one weight pass, M-wide fp16 LUT entries).
+ *   shiftadd_lut_gemv_gather is the M = 1 form. */
+shiftadd_status shiftadd_lut_gemm_gather(const uint16_t* x, int ldx, const uint8_t* planes, const int8_t* exps,
+                                         int layout, int M, int N, int K, int q, int g, uint16_t* const* y_peers,
+                                         uint32_t* const* flag_peers, int P, int rank, uint32_t* epoch,
+                                         void* workspace, size_t workspace_bytes, unsigned flags, void* stream);
 shiftadd_status shiftadd_gather_wait(const uint32_t* flags_local, int P, uint32_t* epoch, void* stream);
 
 /* §8(d) e2e -- stream-ordered copy between device memory and pinned (page-locked, UVA-mapped)

@@ -107,6 +107,9 @@ def lib():
         L.shiftadd_lut_gemv_gather.restype = c_int
         L.shiftadd_lut_gemv_gather.argtypes = [vp, vp, vp, c_int, c_int, c_int, c_int, c_int, vp, vp, c_int, c_int,
                                                vp, vp, c_size, ctypes.c_uint, vp]
+        L.shiftadd_lut_gemm_gather.restype = c_int
+        L.shiftadd_lut_gemm_gather.argtypes = [vp, c_int, vp, vp, c_int, c_int, c_int, c_int, c_int, c_int, vp, vp,
+                                               c_int, c_int, vp, vp, c_size, ctypes.c_uint, vp]
         L.shiftadd_gather_wait.restype = c_int
         L.shiftadd_gather_wait.argtypes = [vp, c_int, vp, vp]
         L.shiftadd_copy.restype = c_int

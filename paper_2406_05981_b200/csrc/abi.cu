@@ -482,10 +482,12 @@ shiftadd_status shiftadd_bcq_quantize(const float* w, int N, int K, int q, int g
   return SHIFTADD_OK;
 }
 
-shiftadd_status shiftadd_lut_gemv_gather(const uint16_t* x, const uint8_t* planes, const int8_t* exps, int layout,
-                                         int N, int K, int q, int g, uint16_t* const* y_peers,
+shiftadd_status shiftadd_lut_gemm_gather(const uint16_t* x, int ldx, const uint8_t* planes, const int8_t* exps,
+                                         int layout, int M, int N, int K, int q, int g, uint16_t* const* y_peers,
                                          uint32_t* const* flag_peers, int P, int rank, uint32_t* epoch,
                                          void* workspace, size_t workspace_bytes, unsigned flags, void* stream) {
+  if (M < 1 || M > 8) return fail(SHIFTADD_ERR_UNSUPPORTED, "fused gather: M=%d outside [1, 8]", M);
+  if (M > 1 && (ldx < K || ldx % 8)) return fail(SHIFTADD_ERR_INVALID, "ldx must be >= K and a multiple of 8");
   if (!x || !planes || !exps || !y_peers || !flag_peers || !epoch || !workspace)
     return fail(SHIFTADD_ERR_INVALID, "null pointer argument");
   shiftadd_status st = check_shape(q, N, K, g, 4);
@@ -499,7 +501,7 @@ shiftadd_status shiftadd_lut_gemv_gather(const uint16_t* x, const uint8_t* plane
   if (!aligned(x, 16) || !aligned(planes, 16)) return fail(SHIFTADD_ERR_INVALID, "misaligned x / planes");
   DevInfo di;
   if ((st = device_info(&di)) != SHIFTADD_OK) return st;
-  if (!cluster_applicable(N, K, q, di.sms) || K > 4096) {
+  if (!cluster_applicable(N, K, q, di.sms) || K > 4096 || M > 1) {
     // K > 4096 (LLaMA-2-70B down_proj, OPT-66B fc2 shards): the all-SM streaming kernel (8),
     // its owner CTAs storing into every rank's buffer
     if (K < 2 * kTileK || !stream_shape_ok(K, di.sms) || !aligned(exps, 16))
@@ -507,17 +509,22 @@ shiftadd_status shiftadd_lut_gemv_gather(const uint16_t* x, const uint8_t* plane
     const size_t need = stream_workspace_bytes(1, K / kTileK, (N + kTileRows - 1) / kTileRows);
     if (workspace_bytes < need)
       return fail(SHIFTADD_ERR_INVALID, "workspace needs %zu bytes (got %zu)", need, workspace_bytes);
+    const size_t need_m = stream_workspace_bytes(M, K / kTileK, (N + kTileRows - 1) / kTileRows);
+    if (workspace_bytes < need_m)
+      return fail(SHIFTADD_ERR_INVALID, "workspace needs %zu bytes (got %zu)", need_m, workspace_bytes);
     StreamLaunch L = {};
     L.x = reinterpret_cast<const __half*>(x);
-    L.M = 1;
-    L.ldx = K;
+    L.M = M;
+    L.ldx = M > 1 ? ldx : K;
+    L.ldy = N;
     L.K = K;
     L.nseg = 1;
     L.seg[0] = StreamSeg{planes, exps, nullptr, q, N};
     L.workspace = workspace;
-    L.grid = di.sms;
+    const LaunchPlan pc = plan_stream(M, q, K, di.sms);
+    L.grid = pc.grid;
     L.su = 16;
-    L.nst = stream_stages(q, kStreamSmemBudget, L.su, 1);
+    L.nst = stream_stages(q, kStreamSmemBudget, L.su, mw_of(M));
     L.pdl = (flags & SHIFTADD_FLAG_PDL) ? 1 : 0;
     L.gather.y_peers = reinterpret_cast<__half* const*>(y_peers);
     L.gather.flag_peers = flag_peers;
@@ -554,6 +561,14 @@ shiftadd_status shiftadd_lut_gemv_gather(const uint16_t* x, const uint8_t* plane
   const cudaError_t e = launch_gemv_cluster(a, plan_gemv_cluster(N, K, q, di.sms));
   if (e != cudaSuccess) return cuda_fail(e, "lut_gemv_gather launch");
   return SHIFTADD_OK;
+}
+
+shiftadd_status shiftadd_lut_gemv_gather(const uint16_t* x, const uint8_t* planes, const int8_t* exps, int layout,
+                                         int N, int K, int q, int g, uint16_t* const* y_peers,
+                                         uint32_t* const* flag_peers, int P, int rank, uint32_t* epoch,
+                                         void* workspace, size_t workspace_bytes, unsigned flags, void* stream) {
+  return shiftadd_lut_gemm_gather(x, K, planes, exps, layout, 1, N, K, q, g, y_peers, flag_peers, P, rank, epoch,
+                                  workspace, workspace_bytes, flags, stream);
 }
 
 shiftadd_status shiftadd_gather_wait(const uint32_t* flags_local, int P, uint32_t* epoch, void* stream) {

@@ -995,9 +995,10 @@ __global__ void __launch_bounds__((NWC + 1) * 32, MINB) lut_stream_kernel(const 
       const __half hv = __float2half_rn(sum);
       if (p.ga.P == 0) {
         p.seg[g].y[(size_t)m * p.ldy + nl] = hv;
-      } else {   // NEXT-f3: straight into every rank's gathered y (peer memory), buffer by call parity
+      } else {   // NEXT-f3: straight into every rank's gathered y [M][P N] (peer memory), buffer by call parity
         const int b = (int)((*p.ga.epoch + 1u) & 1u);
-        for (int rr = 0; rr < p.ga.P; ++rr) p.ga.y_peers[b * p.ga.P + rr][(size_t)p.ga.rank * p.seg[0].N + nl] = hv;
+        const size_t o = ((size_t)m * p.ga.P + p.ga.rank) * p.seg[0].N + nl;
+        for (int rr = 0; rr < p.ga.P; ++rr) p.ga.y_peers[b * p.ga.P + rr][o] = hv;
       }
     }
   }

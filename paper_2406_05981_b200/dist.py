@@ -104,22 +104,25 @@ class FusedGatherLinear:
     gathered buffer (shiftadd_lut_gemv_gather), followed by an on-stream flag wait
     (shiftadd_gather_wait) -- no NCCL call on the data path.
 
-    Each rank allocates two gathered buffers [P*n] (double-buffered by call parity, see
+    Each rank allocates two gathered buffers [max_m][P*n] (double-buffered by call parity, see
     include/shiftadd.h) and a flag array uint32[P]; their CUDA IPC handles are exchanged once
     over ``group`` (any backend; gloo works) and mapped into every process.  Peers on other
     GPUs are reached over NVLink through the IPC mappings; ranks may also share one GPU
     (that is how the single-GPU test exercises the protocol)."""
 
-    def __init__(self, layer: PackedLayer, N_full: int, group=None):
+    def __init__(self, layer: PackedLayer, N_full: int, group=None, max_m: int = 1):
         self.layer = layer
         self.group = group
         self.P = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.n = layer.N
+        self.max_m = max_m
         if self.n * self.P != N_full:
             raise ValueError("N_full must equal P * local rows")
+        if not 1 <= max_m <= 8:
+            raise ValueError("max_m must be in [1, 8]")
         dev = layer.device
-        self.ybuf = [torch.zeros(self.P * self.n, dtype=torch.float16, device=dev) for _ in range(2)]
+        self.ybuf = [torch.zeros(max_m * self.P * self.n, dtype=torch.float16, device=dev) for _ in range(2)]
         self.flags = torch.zeros(self.P, dtype=torch.int32, device=dev)
         mine = [_share(self.ybuf[0]), _share(self.ybuf[1]), _share(self.flags)]
         allh = [None] * self.P
@@ -141,21 +144,22 @@ class FusedGatherLinear:
         self.epoch = torch.zeros(1, dtype=torch.int32, device=dev)                 # device call counter
         self.workspace = Workspace(dev)
         from . import workspace_bytes
-        self.workspace.get(max(workspace_bytes(layer, 1), 256 * 1024 + 16))
+        self.workspace.get(max(workspace_bytes(layer, max_m), 256 * 1024 + 16))
         self.calls = 0                                                             # host mirror (parity)
         torch.cuda.synchronize(dev)
         dist.barrier(group=group)
 
     def __call__(self, x: torch.Tensor, pdl: bool = False, stream=None, layer: PackedLayer | None = None):
-        """y [1][P*n] for x [K] or [1][K] fp16; the returned view is valid until call + 2.
+        """y [M][P*n] for x [K] or [M][K] fp16 (M <= max_m); the returned view is valid until call + 2.
         ``layer`` may substitute another packed layer of the same shape (rotating copies).
         The call counter is on the device (graph capture works); the returned view follows
         the host's count of calls, so a replayed graph should hold an even number of calls
         of this layer when its outputs are read."""
         L = layer if layer is not None else self.layer
-        xv = x.reshape(-1)
-        if xv.dtype != torch.float16 or xv.numel() != L.K:
-            raise ValueError("x must be fp16 [K]")
+        xv = x.reshape(-1, L.K) if x.dim() == 2 else x.reshape(1, -1)
+        M = xv.shape[0]
+        if xv.dtype != torch.float16 or xv.shape[1] != L.K or not 1 <= M <= self.max_m:
+            raise ValueError("x must be fp16 [K] or [M][K] with M <= max_m")
         xv = xv.contiguous()
         self.calls += 1
         par = self.calls & 1
@@ -163,13 +167,13 @@ class FusedGatherLinear:
         sptr = (stream if stream is not None else torch.cuda.current_stream(dev)).cuda_stream
         ws = self.workspace.buf
         lib_ = lib()
-        st = lib_.shiftadd_lut_gemv_gather(xv.data_ptr(), L.planes.data_ptr(), L.exps.data_ptr(), L.layout, self.n,
-                                          L.K, L.q, L.g, self.y_ptrs.data_ptr(), self.flag_ptrs.data_ptr(),
+        st = lib_.shiftadd_lut_gemm_gather(xv.data_ptr(), L.K, L.planes.data_ptr(), L.exps.data_ptr(), L.layout, M,
+                                          self.n, L.K, L.q, L.g, self.y_ptrs.data_ptr(), self.flag_ptrs.data_ptr(),
                                           self.P, self.rank, self.epoch.data_ptr(), ws.data_ptr(), ws.numel(),
                                           FLAG_PDL if pdl else 0, sptr)
         if st:
-            _check(st, "shiftadd_lut_gemv_gather")
+            _check(st, "shiftadd_lut_gemm_gather")
         st = lib_.shiftadd_gather_wait(self.flags.data_ptr(), self.P, self.epoch.data_ptr(), sptr)
         if st:
             _check(st, "shiftadd_gather_wait")
-        return self.ybuf[par].view(1, -1)
+        return self.ybuf[par][:M * self.P * self.n].view(M, -1)

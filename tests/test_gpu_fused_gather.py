@@ -27,7 +27,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q, N, K, g, calls, out_q, graph):
+def _worker(rank, world, port, q, N, K, g, calls, out_q, graph, M=1):
     import sys
     sys.path.insert(0, ROOT)
     import torch.distributed as dist
@@ -42,8 +42,8 @@ def _worker(rank, world, port, q, N, K, g, calls, out_q, graph):
         n0, n1 = sdist.shard_range(N, world, rank)
         L = sa.pack(signs[:, n0:n1].contiguous().cuda(), alpha[:, n0:n1].contiguous().cuda(), g,
                     layout=sa.LAYOUT_TILED)
-        layer = sdist.FusedGatherLinear(L, N)
-        xs = [synth.gen_x(1, K, seed=70 + c).cuda() for c in range(calls)]
+        layer = sdist.FusedGatherLinear(L, N, max_m=M)
+        xs = [synth.gen_x(M, K, seed=70 + c).cuda() for c in range(calls)]
         outs = []
         if not graph:
             for c in range(calls):
@@ -53,7 +53,7 @@ def _worker(rank, world, port, q, N, K, g, calls, out_q, graph):
             # capture two calls (one per buffer) once, replay for every pair of inputs: the
             # epochs and buffer parity come from the device counter
             xin = torch.empty_like(xs[0])
-            ys = [torch.empty(world * (N // world), dtype=torch.float16, device="cuda") for _ in range(2)]
+            ys = [torch.empty(M * world * (N // world), dtype=torch.float16, device="cuda") for _ in range(2)]
             st = torch.cuda.Stream()
             torch.cuda.synchronize()
             gph = torch.cuda.CUDAGraph()
@@ -66,7 +66,7 @@ def _worker(rank, world, port, q, N, K, g, calls, out_q, graph):
                 xin2.copy_(xs[c + 1])
                 gph.replay()
                 torch.cuda.synchronize()
-                outs += [ys[0].clone().view(1, -1), ys[1].clone().view(1, -1)]
+                outs += [ys[0].clone().view(M, -1), ys[1].clone().view(M, -1)]
         torch.cuda.synchronize()
         out_q.put((rank, [o.cpu().numpy() for o in outs], None))
     except Exception as e:  # noqa: BLE001
@@ -81,11 +81,22 @@ def _worker(rank, world, port, q, N, K, g, calls, out_q, graph):
 @pytest.mark.parametrize("q,N,K,graph", [(3, 4096, 4096, False), (2, 1536, 768, False), (3, 4096, 4096, True),
                                          (3, 2048, 9216, False), (2, 1024, 28672, True)])
 def test_fused_gather_two_ranks_one_gpu(q, N, K, graph):
+    _run_case(q, N, K, graph, 1)
+
+
+# batch rows (M <= 8): the streaming kernel with M-wide LUT entries, gathered y [M][P n]
+@pytest.mark.parametrize("q,N,K,graph,M", [(3, 2048, 4096, False, 3), (2, 1024, 9216, True, 5)])
+def test_fused_gather_small_batch_two_ranks_one_gpu(q, N, K, graph, M):
+    _run_case(q, N, K, graph, M)
+
+
+def _run_case(q, N, K, graph, M):
     world, g, calls = 2, 128, 4
     ctx = mp.get_context("spawn")
     out_q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, N, K, g, calls, out_q, graph)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, N, K, g, calls, out_q, graph, M))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = {}
@@ -99,9 +110,9 @@ def test_fused_gather_two_ranks_one_gpu(q, N, K, graph):
     signs, alpha = synth.gen_layer(q, N, K, g, seed=synth.seed_for(1, 60))
     planes, exps, _ = oracle.pack_canonical(signs.numpy(), alpha.numpy(), g)
     for c in range(calls):
-        x = synth.gen_x(1, K, seed=70 + c)
+        x = synth.gen_x(M, K, seed=70 + c)
         ref = oracle.gemm(x.numpy(), planes, exps, g)
         for r in range(world):
-            y = res[r][c].astype(np.float32).reshape(1, -1)
+            y = res[r][c].astype(np.float32).reshape(M, -1)
             assert oracle.err_floor(y, ref) <= 2e-3, (c, r)
         assert np.array_equal(res[0][c], res[1][c])      # every rank holds the same gathered y
