@@ -7,7 +7,9 @@ sys.path.insert(0, ROOT)
 import torch
 import paper_2406_05981_b200 as sa
 import synth
-if os.environ.get("SHIFTADD_LIB") == "dev":
+if os.environ.get("SHIFTADD_LIB", "").endswith(".so"):   # an alternative build, for A/B timing
+    sa._LIB_PATH = os.path.join(ROOT, os.environ["SHIFTADD_LIB"])
+elif os.environ.get("SHIFTADD_LIB") == "dev":
     sa._LIB_PATH = os.path.join(ROOT, "paper_2406_05981_b200", "libshiftadd_dev.so")
     L = sa.lib()
     L.shiftadd_dev_set_variant.argtypes = [ctypes.c_int]
