@@ -226,3 +226,33 @@ def test_program_encode_and_validation_happen_on_the_host(L):
     assert L.shiftadd_program_encode(calls, 0, ctypes.addressof(buf), nb) == 2
     # a valid program on a machine without a GPU: the launch reports a CUDA error, no crash
     assert L.shiftadd_lut_gemv_program(calls, 2, fake, nb, fake, ws, 0, None) == 7
+
+
+def test_round2_entry_points_validate_before_any_launch(L):
+    """Column-wise with a workspace (any K, M <= 16), fused gather for M <= 8, fused segments:
+    malformed calls are rejected on the host; well-formed ones reach the device check."""
+    _r1, p = _buf(1 << 20)
+    ws = 1 << 19
+    assert L.shiftadd_workspace_bytes_colwise(4096, 8192) == 256 * 1024 + 256 + 256 + 2 * 32 * 256 * 16 * 8
+    assert L.shiftadd_workspace_bytes_colwise(4096, 8000) == 0
+    # column-wise M = 1 (workspace form) and M <= 16
+    assert L.shiftadd_lut_gemv_colwise_ws(None, p, p, 1, 64, 8192, 3, p, p, ws, 0, None) == 2
+    assert L.shiftadd_lut_gemv_colwise_ws(p, p, p, 1, 64, 8192, 3, p, p, ws, 16, None) == 2      # unknown flag
+    assert L.shiftadd_lut_gemv_colwise_ws(p, p, p, 0, 64, 8192, 3, p, p, ws, 0, None) == 6       # canonical
+    assert L.shiftadd_lut_gemm_colwise(p, 8192, p, p, 1, 17, 64, 8192, 3, p, 64, p, ws, 0, None) == 6   # M > 16
+    assert L.shiftadd_lut_gemm_colwise(p, 8000, p, p, 1, 4, 64, 8192, 3, p, 64, p, ws, 0, None) == 2    # ldx < K
+    assert L.shiftadd_lut_gemm_colwise(p, 8192, p, p, 1, 4, 64, 8192, 3, p, 32, p, ws, 0, None) == 2    # ldy < N
+    assert L.shiftadd_lut_gemm_colwise(p, 8192, p, p, 1, 4, 64, 8192, 3, p, 64, p, ws, 0, None) == 7    # valid
+    # fused gather, M <= 8
+    g = (p, p, 2, 0, p, p, ws, 0, None)
+    assert L.shiftadd_lut_gemm_gather(p, 4096, p, p, 1, 9, 64, 4096, 3, 128, *g) == 6          # M > 8
+    assert L.shiftadd_lut_gemm_gather(p, 4000, p, p, 1, 3, 64, 4096, 3, 128, *g) == 2          # ldx < K
+    assert L.shiftadd_lut_gemm_gather(p, 4096, p, p, 1, 3, 64, 4096, 3, 128, *g) == 7          # valid
+    # fused segments: unknown flag, too many segments
+    import paper_2406_05981_b200 as sa
+    segs = (sa._Segment * 5)()
+    assert L.shiftadd_lut_gemv_fused(p, 4096, 128, 1, 5, segs, p, ws, 0, None) == 2
+    for i in range(2):
+        segs[i] = sa._Segment(p.value, p.value, 64, 2, p.value)
+    assert L.shiftadd_lut_gemv_fused(p, 4096, 128, 1, 2, segs, p, ws, 8, None) == 2              # unknown flag
+    assert L.shiftadd_lut_gemv_fused(p, 4096, 128, 1, 2, segs, p, ws, 2, None) == 7              # SPLITK: valid
