@@ -643,21 +643,33 @@ def main():
     if group is not None:
         torch.distributed.all_reduce(e2e_ms, op=torch.distributed.ReduceOp.MAX, group=group)
     e2e_val = step_bytes_full * e2e_steps / (float(e2e_ms.item()) * 1e-3) / 1e9
-    # the same step issued eagerly through the Python API every time (no graph): includes the
-    # host cost of 130 ctypes calls per token (argument checks, validation, cudaLaunchKernelEx)
-    eager_steps = 20
-    with torch.cuda.stream(stream):
-        e2e_step()
-    barrier()
-    t0 = time.perf_counter()
-    e0.record(stream)
-    with torch.cuda.stream(stream):
-        for _ in range(eager_steps):
-            e2e_step()
-    e1.record(stream)
-    barrier()
-    eager_wall = (time.perf_counter() - t0) / eager_steps
-    eager_dev = e0.elapsed_time(e1) / eager_steps * 1e-3
+    # the same step issued eagerly every time (no graph), host cost included: (a) through the
+    # per-projection Python API (130 ctypes calls per token), (b) through shiftadd_lut_gemv_chain
+    # (3 C calls per token: copy in, the 128 launches from C, copy out); N = 1
+    def eager_time(fn, n):
+        with torch.cuda.stream(stream):
+            fn()
+        barrier()
+        t0 = time.perf_counter()
+        e0.record(stream)
+        with torch.cuda.stream(stream):
+            for _ in range(n):
+                fn()
+        e1.record(stream)
+        barrier()
+        return (time.perf_counter() - t0) / n, e0.elapsed_time(e1) / n * 1e-3
+
+    eager_wall, eager_dev = eager_time(e2e_step, 20)
+    chain_wall = chain_dev = None
+    if group is None:
+        chain = sa.Chain([(xd[xs_off[li]:xs_off[li + 1]], Lc.layers, e2e_outs[li], True)
+                          for li, Lc in enumerate(launches)])
+
+        def chain_step():
+            sa.copy(xd, xh, pdl=True, src_ready=True, stream=stream)
+            chain(stream=stream)
+            sa.copy(yh, yd, pdl=True, stream=stream)
+        chain_wall, chain_dev = eager_time(chain_step, 50)
 
     if rank == 0:
         us_step = ms / args.steps * 1e3
@@ -686,7 +698,12 @@ def main():
                     "eager": {"value": round(step_bytes_full / eager_dev / 1e9, 2), "unit": "GB/s",
                               "us_per_step": round(eager_dev * 1e6, 1), "wall_us_per_step": round(eager_wall * 1e6, 1),
                               "how": "the same step issued through the Python API each time (no graph): "
-                                     "130 ctypes calls per token, CUDA events; wall = host clock"}},
+                                     "130 ctypes calls per token, CUDA events; wall = host clock"},
+                    "eager_chain": None if chain_dev is None else {
+                        "value": round(step_bytes_full / chain_dev / 1e9, 2), "unit": "GB/s",
+                        "us_per_step": round(chain_dev * 1e6, 1), "wall_us_per_step": round(chain_wall * 1e6, 1),
+                        "how": "no graph: copy in, shiftadd_lut_gemv_chain (the 128 launches issued from C), "
+                               "copy out -- 3 API calls per token"}},
         }
         if ws_size == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_leg(sa, dev)

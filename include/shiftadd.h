@@ -191,6 +191,17 @@ shiftadd_status shiftadd_lut_gemv_program(const shiftadd_call* calls, int ncalls
                                           size_t program_bytes, void* workspace, size_t workspace_bytes,
                                           unsigned flags, void* stream);
 
+/* The same ordered calls issued from the host as one kernel per call (no persistent kernel):
+ * each call goes through shiftadd_lut_gemm (one segment) or shiftadd_lut_gemv_fused, all on
+ * `stream`, so a decode step costs one C call instead of one per projection.  With
+ * SHIFTADD_FLAG_PDL every launch is a programmatic dependent of the previous one (x read after
+ * the previous call completed: the decoder's dependency, as SHIFTADD_CALL_WAIT).  Workspace:
+ * shiftadd_workspace_bytes_chain(calls) bytes (the calls share it in order).  Errors name the
+ * failing call; calls before it have been enqueued. */
+size_t shiftadd_workspace_bytes_chain(const shiftadd_call* calls, int ncalls);
+shiftadd_status shiftadd_lut_gemv_chain(const shiftadd_call* calls, int ncalls, void* workspace,
+                                        size_t workspace_bytes, unsigned flags, void* stream);
+
 /* Batch-1 convenience: shiftadd_lut_gemm with M = 1, ldx = K, ldy = N. */
 shiftadd_status shiftadd_lut_gemv(const uint16_t* x, const uint8_t* planes, const int8_t* exps,
                                   int layout, int N, int K, int q, int g, uint16_t* y,

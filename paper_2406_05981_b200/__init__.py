@@ -23,7 +23,8 @@ __all__ = [
     "LAYOUT_CANONICAL", "LAYOUT_TILED", "FLAG_PDL", "FLAG_SPLITK", "EXP_ZERO", "ShiftAddError", "lib",
     "PackedLayer", "packed_bytes", "pack", "lut_gemm", "lut_gemv", "workspace_bytes",
     "gemm_plan", "Workspace", "pack_colwise", "lut_gemv_colwise", "pack_apot2", "bcq_quantize",
-    "lut_gemv_fused", "workspace_bytes_fused", "pack_blockwise", "lut_gemv_blockwise", "Program", "CALL_WAIT",
+    "lut_gemv_fused", "workspace_bytes_fused", "pack_blockwise", "lut_gemv_blockwise", "Program", "Chain",
+    "CALL_WAIT",
 ]
 
 LAYOUT_CANONICAL = 0
@@ -135,6 +136,10 @@ def lib():
         L.shiftadd_lut_gemv_program.restype = c_int
         L.shiftadd_lut_gemv_program.argtypes = [ctypes.POINTER(_Call), c_int, vp, c_size, vp, c_size,
                                                 ctypes.c_uint, vp]
+        L.shiftadd_workspace_bytes_chain.restype = c_size
+        L.shiftadd_workspace_bytes_chain.argtypes = [ctypes.POINTER(_Call), c_int]
+        L.shiftadd_lut_gemv_chain.restype = c_int
+        L.shiftadd_lut_gemv_chain.argtypes = [ctypes.POINTER(_Call), c_int, vp, c_size, ctypes.c_uint, vp]
         L.shiftadd_gemm_plan.restype = c_int
         L.shiftadd_gemm_plan.argtypes = [c_int] * 6 + [ctypes.POINTER(c_int * 4)]
         v = L.shiftadd_abi_version()
@@ -534,6 +539,53 @@ def lut_gemv(x: torch.Tensor, layer: PackedLayer, **kw) -> torch.Tensor:
 CALL_WAIT = 1
 
 
+def _encode_calls(calls):
+    arr = (_Call * len(calls))()
+    keep = []
+    for j, (x, layers, outs, wait) in enumerate(calls):
+        x = x.reshape(-1)
+        if x.dtype != torch.float16 or not x.is_cuda or not 1 <= len(layers) <= 4 or len(outs) != len(layers):
+            raise ValueError("call %d: fp16 x on the device and 1..4 segments with outputs" % j)
+        for L, y in zip(layers, outs):
+            if L.K != x.numel() or L.g != layers[0].g or L.layout != LAYOUT_TILED or L.colwise or \
+                    L.exps2 is not None:
+                raise ValueError("call %d: tiled row-wise layers with the K and g of x" % j)
+            if y.dtype != torch.float16 or y.numel() != L.N or not y.is_contiguous():
+                raise ValueError("call %d: outputs must be contiguous fp16 [N_i]" % j)
+        c = arr[j]
+        c.x, c.K, c.g, c.nseg, c.flags = x.data_ptr(), x.numel(), layers[0].g, len(layers), CALL_WAIT if wait else 0
+        for i, (L, y) in enumerate(zip(layers, outs)):
+            c.seg[i] = _Segment(L.planes.data_ptr(), L.exps.data_ptr(), L.N, L.q, y.data_ptr())
+        keep.append((x, layers, outs))
+    return arr, keep
+
+
+class Chain:
+    """An ordered list of calls launched from C as one kernel per call (shiftadd_lut_gemv_chain):
+    a decode step costs one ctypes call.  calls: as for Program; with pdl=True every launch
+    waits for the previous one (the ``wait`` entries are implied).  The tensors must stay alive
+    and in place while the Chain is used."""
+
+    def __init__(self, calls, device=None):
+        if not calls:
+            raise ValueError("empty chain")
+        self.device = torch.device(device) if device is not None else calls[0][1][0].device
+        self.calls, self._keep = _encode_calls(calls)
+        self.n = len(calls)
+        need = int(lib().shiftadd_workspace_bytes_chain(self.calls, self.n))
+        self.workspace = Workspace(self.device)
+        self.workspace.get(need)
+
+    def __call__(self, stream=None, pdl: bool = True):
+        if torch.cuda.current_device() != self.device.index:
+            torch.cuda.set_device(self.device)
+        sptr = (stream if stream is not None else torch.cuda.current_stream(self.device)).cuda_stream
+        ws = self.workspace.buf
+        _check(lib().shiftadd_lut_gemv_chain(self.calls, self.n, ws.data_ptr() if ws is not None else None,
+                                             ws.numel() if ws is not None else 0, FLAG_PDL if pdl else 0, sptr),
+               "shiftadd_lut_gemv_chain")
+
+
 class Program:
     """A decode step as one persistent launch (shiftadd_lut_gemv_program, kernel id 9).
 
@@ -548,23 +600,7 @@ class Program:
         if not calls:
             raise ValueError("empty program")
         self.device = torch.device(device) if device is not None else calls[0][1][0].device
-        arr = (_Call * len(calls))()
-        self._keep = []
-        for j, (x, layers, outs, wait) in enumerate(calls):
-            x = x.reshape(-1)
-            if x.dtype != torch.float16 or not x.is_cuda or not 1 <= len(layers) <= 4 or len(outs) != len(layers):
-                raise ValueError("call %d: fp16 x on the device and 1..4 segments with outputs" % j)
-            for L, y in zip(layers, outs):
-                if L.K != x.numel() or L.g != layers[0].g or L.layout != LAYOUT_TILED or L.colwise or \
-                        L.exps2 is not None:
-                    raise ValueError("call %d: tiled row-wise layers with the K and g of x" % j)
-                if y.dtype != torch.float16 or y.numel() != L.N or not y.is_contiguous():
-                    raise ValueError("call %d: outputs must be contiguous fp16 [N_i]" % j)
-            c = arr[j]
-            c.x, c.K, c.g, c.nseg, c.flags = x.data_ptr(), x.numel(), layers[0].g, len(layers), CALL_WAIT if wait else 0
-            for i, (L, y) in enumerate(zip(layers, outs)):
-                c.seg[i] = _Segment(L.planes.data_ptr(), L.exps.data_ptr(), L.N, L.q, y.data_ptr())
-            self._keep.append((x, layers, outs))
+        arr, self._keep = _encode_calls(calls)
         self.calls, self.n = arr, len(calls)
         nb = int(lib().shiftadd_program_bytes(self.n))
         host = torch.empty(nb, dtype=torch.uint8).pin_memory()

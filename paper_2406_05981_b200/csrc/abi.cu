@@ -891,6 +891,45 @@ shiftadd_status shiftadd_lut_gemv_program(const shiftadd_call* calls, int ncalls
   return SHIFTADD_OK;
 }
 
+// ------------------------------------------------------------------ host-side chain of calls
+shiftadd_status shiftadd_lut_gemv_chain(const shiftadd_call* calls, int ncalls, void* workspace,
+                                        size_t workspace_bytes, unsigned flags, void* stream) {
+  if (!calls || ncalls < 1) return fail(SHIFTADD_ERR_INVALID, "need ncalls >= 1 and a call array");
+  if (flags & ~SHIFTADD_FLAG_PDL) return fail(SHIFTADD_ERR_INVALID, "unknown flags 0x%x", flags);
+  for (int j = 0; j < ncalls; ++j) {
+    const shiftadd_call& c = calls[j];
+    shiftadd_status st;
+    if (c.nseg == 1) {
+      const shiftadd_segment& sg = c.seg[0];
+      st = shiftadd_lut_gemm(c.x, c.K, sg.planes, sg.exps, SHIFTADD_LAYOUT_TILED, 1, sg.N, c.K, sg.q, c.g, sg.y, sg.N,
+                             workspace, workspace_bytes, flags, stream);
+    } else {
+      st = shiftadd_lut_gemv_fused(c.x, c.K, c.g, SHIFTADD_LAYOUT_TILED, c.nseg, c.seg, workspace, workspace_bytes,
+                                   flags, stream);
+    }
+    if (st != SHIFTADD_OK) {
+      const std::string detail = g_last_error;
+      return fail(st, "chain call %d: %s", j, detail.c_str());
+    }
+  }
+  return SHIFTADD_OK;
+}
+
+size_t shiftadd_workspace_bytes_chain(const shiftadd_call* calls, int ncalls) {
+  if (!calls || ncalls < 1) return 0;
+  size_t need = 0;
+  for (int j = 0; j < ncalls; ++j) {
+    const shiftadd_call& c = calls[j];
+    size_t b = 0;
+    if (c.nseg == 1)
+      b = shiftadd_workspace_bytes(SHIFTADD_LAYOUT_TILED, 1, c.seg[0].N, c.K, c.seg[0].q, c.g);
+    else
+      b = shiftadd_workspace_bytes_fused(SHIFTADD_LAYOUT_TILED, 1, c.K, c.g, c.nseg, c.seg);
+    need = b > need ? b : need;
+  }
+  return need;
+}
+
 shiftadd_status shiftadd_lut_gemv(const uint16_t* x, const uint8_t* planes, const int8_t* exps, int layout,
                                   int N, int K, int q, int g, uint16_t* y, void* workspace,
                                   size_t workspace_bytes, unsigned flags, void* stream) {

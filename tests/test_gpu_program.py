@@ -153,3 +153,27 @@ def test_program_repeated_launches_eager_and_graph(sa):
         for (cases, outs), ref in zip(cases_all, first):
             for y, r in zip(outs, ref):
                 assert torch.equal(y, r)
+
+
+def test_chain_matches_individual_calls_bit_for_bit(sa):
+    """shiftadd_lut_gemv_chain issues the same kernels as the per-call entry points: outputs are
+    bit-identical to lut_gemm / lut_gemv_fused called one by one (and meet the oracle bar)."""
+    calls, refs = [], []
+    for j, (K, segs, _) in enumerate(MIXED):
+        x = synth.gen_x(1, K, seed=synth.seed_for(9, 600 + j, K)).view(-1).to(DEV)
+        cases = [_layer(sa, q, N, K, synth.seed_for(9, 610 + 10 * j + i, q)) for i, (q, N) in enumerate(segs)]
+        outs = [torch.empty(c[0].N, dtype=torch.float16, device=DEV) for c in cases]
+        calls.append((x, [c[0] for c in cases], outs, True))
+        refs.append((x, cases))
+    sa.Chain(calls)()
+    torch.cuda.synchronize()
+    for (x, cases), (_, _, outs, _) in zip(refs, calls):
+        layers = [c[0] for c in cases]
+        if len(layers) == 1:
+            ind = [sa.lut_gemm(x, layers[0], pdl=True).view(-1)]
+        else:
+            ind = sa.lut_gemv_fused(x, layers, pdl=True)
+        torch.cuda.synchronize()
+        for (L, planes, exps), y, yi in zip(cases, outs, ind):
+            assert torch.equal(y, yi), (L.N, L.K)
+            assert _err(y, x.cpu().numpy(), planes, exps) <= TOL
