@@ -84,6 +84,14 @@ size_t tiled_rows(int N) { return (size_t)((N + kTileRows - 1) / kTileRows); }
 
 int mw_of(int M) { return M == 1 ? 1 : M == 2 ? 2 : M <= 4 ? 4 : 8; }
 
+// Kernel 8, M = 1: one slice per CTA (one LUT build, one run per segment) beats the
+// weight-balanced split on layers with many slices and little work per CTA (measured:
+// LLaMA-2-7B down_proj, S = 43 on 129 SMs, 9.3 vs 9.8 us in the dev build), not on large or
+// few-slice layers (70B gate/up S = 32: 27.1 vs 26.0; q/k/v-sized S = 16: 13.2 vs 13.1).
+bool stream_one_slice(int S, double plane_bytes, int sms) {
+  return S >= 24 && S <= sms && plane_bytes <= 16e6;
+}
+
 // Streaming kernel (id 8) geometry for a launch of Mc <= 8 rows (or the first chunk of M).
 LaunchPlan plan_stream(int M, int q, int K, int sms) {
   const int MW = mw_of(M > 8 ? 8 : M);
@@ -686,6 +694,10 @@ shiftadd_status shiftadd_lut_gemm(const uint16_t* x, int ldx, const uint8_t* pla
       L.workspace = workspace;
       const LaunchPlan pc = plan_stream(mc, q, K, di.sms);
       L.grid = pc.grid;
+      if (mc == 1 && stream_one_slice(K / kTileK, (double)q * N * K / 8, di.sms)) {
+        L.one_slice = 1;
+        L.grid = (K / kTileK) * (di.sms / (K / kTileK));
+      }
       L.su = 16;
       L.nst = stream_stages(q, kStreamSmemBudget, L.su, mw_of(mc));
       L.pdl = (flags & SHIFTADD_FLAG_PDL) ? 1 : 0;
@@ -778,6 +790,14 @@ shiftadd_status shiftadd_lut_gemv_fused(const uint16_t* x, int K, int g, int lay
   L.su = 16;
   L.nst = stream_stages(qmax, kStreamSmemBudget, L.su, 1);
   L.pdl = (flags & SHIFTADD_FLAG_PDL) ? 1 : 0;
+  {
+    double pb = 0;
+    for (int i = 0; i < nseg; ++i) pb += (double)segs[i].q * segs[i].N * K / 8;
+    if (stream_one_slice(K / kTileK, pb, di.sms)) {
+      L.one_slice = 1;
+      L.grid = (K / kTileK) * (di.sms / (K / kTileK));
+    }
+  }
   // K <= 4096: the cluster TMA ring (kernel 10, DSMEM reduction, no workspace) unless
   // SHIFTADD_FLAG_SPLITK; otherwise (or if no cluster shape fits) the all-SM streaming kernel
   // (measured on B200: q/k/v 4096 x 3 at 2/3/2 bits 8.2 vs 9.1 us; gate/up 11008 x 2 at 2/3

@@ -1085,7 +1085,7 @@ cudaError_t launch_lut_stream(const StreamLaunch& L, cudaStream_t stream) {
   p.S = L.K / kTileK;
   const int MW = p.M == 1 ? 1 : p.M == 2 ? 2 : p.M <= 4 ? 4 : 8;
   if (p.M > 8) return cudaErrorInvalidValue;
-  p.one_slice = MW == 8 ? 1 : 0;
+  p.one_slice = (MW == 8 || (L.one_slice && MW == 1 && !L.exps_bw)) ? 1 : 0;
   p.lut_bytes = stream_lut_bytes(MW);
   p.nseg = L.nseg;
   int rg = 0, w = 0, qmax = 1;
@@ -1128,6 +1128,12 @@ cudaError_t launch_lut_stream(const StreamLaunch& L, cudaStream_t stream) {
 #endif
   cudaLaunchConfig_t c = {};
   c.gridDim = dim3(L.grid);
+#ifdef SHIFTADD_DEV_TRACE
+  if ((g_dev_variant & 128) && MW == 1 && !L.exps_bw && p.S > 1 && p.S <= L.grid) {   // experiment: one slice per CTA
+    p.one_slice = 1;
+    c.gridDim = dim3(p.S * (L.grid / p.S));
+  }
+#endif
   c.blockDim = dim3((L.half || (L.exps_bw && p.bw_rgb == 0)) ? 9 * 32 : 17 * 32);
   c.dynamicSmemBytes = p.lut_bytes + L.nst * p.slot + kBarBytes;
   c.stream = stream;
