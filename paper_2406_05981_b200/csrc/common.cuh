@@ -52,6 +52,22 @@ __device__ __forceinline__ void check_dyn_base() {
   if (dyn_smem_base() != kDynBase) __trap();
 }
 
+// Bounds-checked debug builds (-DSHIFTADD_BOUNDS_CHECK, tools/check_build.sh; this pool has
+// compute-sanitizer disabled): every shared-memory access through the wrappers below, every
+// bulk-copy destination and DSMEM store, and every split-K partial word store traps if it
+// leaves the launch's dynamic shared memory / the partial region.  Cluster-window addresses
+// carry the rank in bits 24+, stripped before the check.  Product builds compile it away.
+#ifdef SHIFTADD_BOUNDS_CHECK
+__device__ __forceinline__ void smem_check(uint32_t addr, uint32_t bytes) {
+  uint32_t dyn;
+  asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+  const uint32_t a = addr & 0x00ffffffu;
+  if (a < kDynBase || a + bytes > kDynBase + dyn || (a & (bytes >= 16 ? 15u : bytes - 1u))) __trap();
+}
+#else
+__device__ __forceinline__ void smem_check(uint32_t, uint32_t) {}
+#endif
+
 // PTX prmt.b32 (default mode).  Unlike __byte_perm, the selector's per-nibble msb is honoured:
 // it replicates the sign bit of the selected byte over the target byte.
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
@@ -61,19 +77,23 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
 }
 
 __device__ __forceinline__ float lds_f32(uint32_t addr) {
+  smem_check(addr, 4);
   float v;
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
   return v;
 }
 __device__ __forceinline__ float4 lds_f32x4(uint32_t addr) {
+  smem_check(addr, 16);
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
   return v;
 }
 __device__ __forceinline__ void sts_f32(uint32_t addr, float v) {
+  smem_check(addr, 4);
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }
 __device__ __forceinline__ void sts_f32x4(uint32_t addr, float4 v) {
+  smem_check(addr, 16);
   asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                : "memory");
 }

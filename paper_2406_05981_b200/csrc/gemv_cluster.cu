@@ -105,6 +105,8 @@ __device__ __forceinline__ void mbar_init1(uint32_t bar) {
 }
 __device__ __forceinline__ void bulk_load_x(uint32_t dst, const void* src, uint32_t bytes, uint32_t xbar,
                                             uint64_t pol, bool expect = true) {
+  smem_check(dst, bytes);
+  smem_check(xbar, 8);
   if (expect)
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(xbar), "r"(bytes) : "memory");
   asm volatile(
@@ -115,6 +117,8 @@ __device__ __forceinline__ void bulk_load_x(uint32_t dst, const void* src, uint3
 // Asynchronous 4-byte store into CTA `rank`'s shared memory that completes 4 transaction
 // bytes on that CTA's mbarrier (both addresses given in this CTA's window, mapped here).
 __device__ __forceinline__ void st_async_f32(uint32_t local_addr, uint32_t local_bar, uint32_t rank, float v) {
+  smem_check(local_addr, 4);
+  smem_check(local_bar, 8);
   uint32_t ra, rb;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local_addr), "r"(rank));
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(local_bar), "r"(rank));
@@ -715,8 +719,10 @@ gemv_cluster_ring_kernel(const __half* __restrict__ x, const uint8_t* __restrict
         const uint32_t se = ring + (uint32_t)(j * RC::stage + RC::stage_planes + warp * Q * kTileExps + lane);
 #pragma unroll
         for (int k = 0; k < Q; ++k) {
+          smem_check(sp + (uint32_t)(k * kTileBytes), 16);
           asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(w[k].x), "=r"(w[k].y), "=r"(w[k].z),
                        "=r"(w[k].w) : "r"(sp + (uint32_t)(k * kTileBytes)));
+          smem_check(se + (uint32_t)(k * kTileExps), 1);
           asm volatile("ld.shared.s8 %0, [%1];" : "=r"(e[k]) : "r"(se + (uint32_t)(k * kTileExps)));
         }
         const int ts = H16 ? (i >= RGb) + (i >= 2 * RGb) + (i >= 3 * RGb) : (i >= RGb ? 1 : 0);
@@ -810,8 +816,10 @@ __device__ __forceinline__ float fused_dot(uint32_t sp, uint32_t se, bool odd, c
   int e[Q];
 #pragma unroll
   for (int k = 0; k < Q; ++k) {
+    smem_check(sp + (uint32_t)(k * kTileBytes), 16);
     asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(w[k].x), "=r"(w[k].y), "=r"(w[k].z), "=r"(w[k].w)
                  : "r"(sp + (uint32_t)(k * kTileBytes)));
+    smem_check(se + (uint32_t)(k * kTileExps), 1);
     asm volatile("ld.shared.s8 %0, [%1];" : "=r"(e[k]) : "r"(se + (uint32_t)(k * kTileExps)));
   }
   return odd ? unit_dot_c<Q, kDynBase, false>(w, e, e, cstO) : unit_dot_c<Q, kDynBase, false>(w, e, e, cstE);
@@ -1144,8 +1152,10 @@ gemm_cluster_ring_m2_kernel(const __half* __restrict__ x, int ldx, const uint8_t
         const uint32_t se = ring + (uint32_t)(j * RC::stage + RC::stage_planes + warp * Q * kTileExps + lane);
 #pragma unroll
         for (int k = 0; k < Q; ++k) {
+          smem_check(sp + (uint32_t)(k * kTileBytes), 16);
           asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(w[k].x), "=r"(w[k].y), "=r"(w[k].z),
                        "=r"(w[k].w) : "r"(sp + (uint32_t)(k * kTileBytes)));
+          smem_check(se + (uint32_t)(k * kTileExps), 1);
           asm volatile("ld.shared.s8 %0, [%1];" : "=r"(e[k]) : "r"(se + (uint32_t)(k * kTileExps)));
         }
         const int ts = i >= RGb ? 1 : 0, rgl = i - ts * RGb;
@@ -1385,8 +1395,10 @@ gemm_cluster_ring_m4_kernel(const __half* __restrict__ x, int ldx, int M, const 
         const uint32_t se = ring + (uint32_t)(j * RC::stage + RC::stage_planes + warp * Q * kTileExps + lane);
 #pragma unroll
         for (int k = 0; k < Q; ++k) {
+          smem_check(sp + (uint32_t)(k * kTileBytes), 16);
           asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(w[k].x), "=r"(w[k].y), "=r"(w[k].z),
                        "=r"(w[k].w) : "r"(sp + (uint32_t)(k * kTileBytes)));
+          smem_check(se + (uint32_t)(k * kTileExps), 1);
           asm volatile("ld.shared.s8 %0, [%1];" : "=r"(e[k]) : "r"(se + (uint32_t)(k * kTileExps)));
         }
         float4 v = unit_dot_m4<Q>(w, e, cst);

@@ -78,6 +78,7 @@ struct ProgParams {
   uint64_t hash;
   unsigned long long* ctr;
   unsigned long long* part[2];
+  size_t part_words;   // words per region (bounds-checked builds)
   int nst, slot, slot_planes;
 };
 
@@ -104,7 +105,8 @@ struct Ring {
 template <int Q, uint32_t HOFF>
 __device__ __forceinline__ void consume_run(const ProgSeg& sg, int S, int s, int rga, int re, RingPos& rp,
                                             const Ring& R, const uint32_t (&cst)[4], int wu, int lane,
-                                            unsigned long long ep, unsigned long long* part, bool skew) {
+                                            unsigned long long ep, unsigned long long* part, size_t part_words,
+                                            bool skew) {
   const int r = lane >> 1, h = lane & 1;
   unsigned long long* prow = part + ((size_t)sg.rgoff * S + s) * kTileRows + r;
   bool single = skew;
@@ -143,7 +145,11 @@ __device__ __forceinline__ void consume_run(const ProgSeg& sg, int S, int s, int
             const int nl = u * kTileRows + r;
             if (nl < sg.N) sg.y[nl] = __float2half_rn(acc[k]);
           } else {
-            st_relaxed_u64(prow + (size_t)u * S * kTileRows, ep | __float_as_uint(acc[k]));
+            unsigned long long* const q = prow + (size_t)u * S * kTileRows;
+#ifdef SHIFTADD_BOUNDS_CHECK
+            if (q < part || q >= part + part_words) __trap();
+#endif
+            st_relaxed_u64(q, ep | __float_as_uint(acc[k]));
           }
         }
       }
@@ -155,12 +161,13 @@ __device__ __forceinline__ void consume_run(const ProgSeg& sg, int S, int s, int
 template <uint32_t HOFF>
 __device__ __forceinline__ void consume_run_q(const ProgSeg& sg, int S, int s, int rga, int re, RingPos& rp,
                                               const Ring& R, const uint32_t (&cst)[4], int wu, int lane,
-                                              unsigned long long ep, unsigned long long* part, bool skew) {
+                                              unsigned long long ep, unsigned long long* part, size_t part_words,
+                                              bool skew) {
   switch (sg.q) {
-    case 1: consume_run<1, HOFF>(sg, S, s, rga, re, rp, R, cst, wu, lane, ep, part, skew); break;
-    case 2: consume_run<2, HOFF>(sg, S, s, rga, re, rp, R, cst, wu, lane, ep, part, skew); break;
-    case 3: consume_run<3, HOFF>(sg, S, s, rga, re, rp, R, cst, wu, lane, ep, part, skew); break;
-    default: consume_run<4, HOFF>(sg, S, s, rga, re, rp, R, cst, wu, lane, ep, part, skew); break;
+    case 1: consume_run<1, HOFF>(sg, S, s, rga, re, rp, R, cst, wu, lane, ep, part, part_words, skew); break;
+    case 2: consume_run<2, HOFF>(sg, S, s, rga, re, rp, R, cst, wu, lane, ep, part, part_words, skew); break;
+    case 3: consume_run<3, HOFF>(sg, S, s, rga, re, rp, R, cst, wu, lane, ep, part, part_words, skew); break;
+    default: consume_run<4, HOFF>(sg, S, s, rga, re, rp, R, cst, wu, lane, ep, part, part_words, skew); break;
   }
 }
 
@@ -332,9 +339,9 @@ __global__ void __launch_bounds__((kNWC + 1) * 32, 1) lut_program_kernel(const _
     for (Pos a = start; before(a, end);) {
       const int re = run_end(cl, a, end);
       if (a.s == s0)
-        consume_run_q<0u>(cl.seg[a.g], S, a.s, a.rg, re, rp, R, cst, warp, lane, ep, part, skew);
+        consume_run_q<0u>(cl.seg[a.g], S, a.s, a.rg, re, rp, R, cst, warp, lane, ep, part, pp.part_words, skew);
       else
-        consume_run_q<128u>(cl.seg[a.g], S, a.s, a.rg, re, rp, R, cst, warp, lane, ep, part, skew);
+        consume_run_q<128u>(cl.seg[a.g], S, a.s, a.rg, re, rp, R, cst, warp, lane, ep, part, pp.part_words, skew);
       next_run(cl, a, re);
     }
     if (tid == 0) ptrace(c, pp.ncalls, j, 3);
@@ -503,6 +510,7 @@ cudaError_t launch_lut_program(const void* program, int ncalls, uint64_t hash, i
   p.ctr = reinterpret_cast<unsigned long long*>(ws);
   p.part[0] = reinterpret_cast<unsigned long long*>(ws + 256);
   p.part[1] = reinterpret_cast<unsigned long long*>(ws + 256 + region);
+  p.part_words = region / sizeof(unsigned long long);
   p.nst = nst;
   p.slot = 16 * qmax * (kTileBytes + kTileExps);
   p.slot_planes = 16 * qmax * kTileBytes;

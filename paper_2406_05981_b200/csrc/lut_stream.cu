@@ -88,7 +88,16 @@ struct StreamParams {
   int bw_rgb;              // BW = 2: row groups per block (N / 128)
   GatherArgs ga;           // NEXT-f3 fused all-gather epilogue (P == 0: off)
   int dev_mode;            // development builds only (co-roof experiments), 0 otherwise
+  const unsigned long long* part_end;   // end of the partial region (bounds-checked builds)
 };
+
+// A split-K partial word store (bounds-checked builds: inside [part, part_end)).
+__device__ __forceinline__ void st_part(const StreamParams& p, unsigned long long* q, unsigned long long v) {
+#ifdef SHIFTADD_BOUNDS_CHECK
+  if (q < p.part || q >= p.part_end) __trap();
+#endif
+  stream_dev::st_relaxed_u64(q, v);
+}
 
 #ifdef SHIFTADD_DEV_TRACE
 // co-roof experiment (dev builds): the lookups and adds of unit_dot2 with key words made in
@@ -175,7 +184,7 @@ __device__ __forceinline__ void consume_run(const StreamParams& p, const SegDev&
             const int nl = u * kTileRows + r;
             if (nl < sg.N) sg.y[nl] = __float2half_rn(acc[k]);
           } else {
-            st_relaxed_u64(prow + (size_t)u * p.S * kTileRows, ep | __float_as_uint(acc[k]));
+            st_part(p, prow + (size_t)u * p.S * kTileRows, ep | __float_as_uint(acc[k]));
           }
         }
       }
@@ -363,7 +372,7 @@ __device__ __forceinline__ void consume_run_mw(const StreamParams& p, const SegD
               if (nl < sg.N) sg.y[(size_t)m * p.ldy + nl] = __float2half_rn(acc[m]);
             } else {
               const size_t w = ((((size_t)m * p.RGtot + sg.rgoff + u) * p.S) + s) * kTileRows + r;
-              st_relaxed_u64(p.part + w, ep | __float_as_uint(acc[m]));
+              st_part(p, p.part + w, ep | __float_as_uint(acc[m]));
             }
           }
         }
@@ -479,7 +488,7 @@ __device__ __forceinline__ void consume_run_bw(const StreamParams& p, const SegD
           if (nl < sg.N) sg.y[nl] = __float2half_rn(acc);
         } else {
           const size_t w = (((size_t)sg.rgoff + u) * p.S + s) * kTileRows + r;
-          st_relaxed_u64(p.part + w, ep | __float_as_uint(acc));
+          st_part(p, p.part + w, ep | __float_as_uint(acc));
         }
       }
     } else {
@@ -712,7 +721,7 @@ __device__ __forceinline__ void consume_run_lut(const StreamParams& p, const Seg
                 const int nl = u * kTileRows + r;
                 if (nl < sg.N) sg.y[(size_t)m * p.ldy + nl] = __float2half_rn(acc[m]);
               } else {
-                st_relaxed_u64(p.part + ((((size_t)m * p.RGtot + sg.rgoff + u) * p.S) + s) * kTileRows + r,
+                st_part(p, p.part + ((((size_t)m * p.RGtot + sg.rgoff + u) * p.S) + s) * kTileRows + r,
                                ep | __float_as_uint(acc[m]));
               }
             }
@@ -729,7 +738,7 @@ __device__ __forceinline__ void consume_run_lut(const StreamParams& p, const Seg
             const int nl = u * kTileRows + r;
             if (nl < sg.N) sg.y[nl] = __float2half_rn(acc);
           } else {
-            st_relaxed_u64(p.part + (((size_t)sg.rgoff + u) * p.S + s) * kTileRows + r, ep | __float_as_uint(acc));
+            st_part(p, p.part + (((size_t)sg.rgoff + u) * p.S + s) * kTileRows + r, ep | __float_as_uint(acc));
           }
         }
       } else {
@@ -1109,6 +1118,7 @@ cudaError_t launch_lut_stream(const StreamLaunch& L, cudaStream_t stream) {
     char* ws = static_cast<char*>(L.workspace) + kStreamWsOff;
     p.done = reinterpret_cast<unsigned long long*>(ws);
     p.part = reinterpret_cast<unsigned long long*>(ws + 256);
+    p.part_end = p.part + (size_t)p.M * p.S * p.RGtot * kTileRows;
   }
   p.nst = L.nst;
   p.su = L.su;

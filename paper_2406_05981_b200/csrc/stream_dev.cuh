@@ -9,9 +9,11 @@ namespace shiftadd {
 namespace stream_dev {
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  smem_check(bar, 8);
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  smem_check(bar, 8);
   uint32_t done = 0;
   do {
     asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
@@ -19,19 +21,24 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   } while (!done);
 }
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  smem_check(bar, 8);
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, uint64_t pol) {
+  smem_check(dst, bytes);
+  smem_check(bar, 8);
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
       ::"r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(pol) : "memory");
 }
 __device__ __forceinline__ uint4 lds_u4(uint32_t addr) {
+  smem_check(addr, 16);
   uint4 v;
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
   return v;
 }
 __device__ __forceinline__ int lds_s8(uint32_t addr) {
+  smem_check(addr, 1);
   int v;
   asm volatile("ld.shared.s8 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;

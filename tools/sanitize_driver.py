@@ -11,6 +11,9 @@ import oracle  # noqa: E402
 import paper_2406_05981_b200 as sa  # noqa: E402
 import synth  # noqa: E402
 
+if os.environ.get("SHIFTADD_LIB_PATH"):   # e.g. the bounds-checked build (tools/check_build.sh)
+    sa._LIB_PATH = os.environ["SHIFTADD_LIB_PATH"]
+
 dev = torch.device("cuda:0")
 bad = []
 
@@ -34,6 +37,8 @@ def rowwise(q, N, K, M, **kw):
 rowwise(3, 256, 1024, 1)                      # cluster kernel (3)
 rowwise(3, 272, 1024, 1, splitk=True)         # streaming kernel (8), straddling chunks
 rowwise(2, 64, 256, 1, splitk=True)           # streaming, S = 1
+rowwise(2, 256, 6144, 1)                      # streaming, one slice per CTA (S = 24)
+rowwise(3, 100, 9216, 1)                      # streaming, weight-balanced split
 rowwise(3, 272, 1024, 2)                      # cluster ring M = 2 (5)
 rowwise(3, 272, 1024, 3)                      # cluster ring M = 3..4 (6)
 for M in (2, 4, 8, 12):                       # streaming MW = 2, 4, 8 and two row chunks
@@ -75,6 +80,15 @@ for N in (256, 40):
     y = sa.lut_gemv_blockwise(xb.to(dev), L, pdl=True)
     torch.cuda.synchronize()
     check("blockwise N%d" % N, y, oracle.gemm_blockwise(xb.numpy(), p, e))
+# column-wise scales: cluster kernel, streaming kernel (K > 4096), pairs of rows
+for (qc, Nc, Kc, Mc) in ((2, 200, 1024, 1), (3, 100, 8192, 1), (2, 96, 1024, 3)):
+    sc, ac = synth.gen_layer_colwise(qc, Nc, Kc, seed=synth.seed_for(12, 80, Kc + Mc))
+    pc, ec, _ = oracle.pack_colwise(sc.numpy(), ac.numpy())
+    Lc = sa.pack_colwise(sc.to(dev), ac.to(dev))
+    xc2 = synth.gen_x(Mc, Kc, seed=8 + Mc)
+    yc = sa.lut_gemv_colwise(xc2.to(dev), Lc, pdl=True)
+    torch.cuda.synchronize()
+    check("colwise K%d M%d" % (Kc, Mc), yc.reshape(Mc, Nc), oracle.gemm_colwise(xc2.numpy(), pc, ec))
 # canonical layout (generic kernel)
 s, a = synth.gen_layer(2, 64, 512, 64, seed=5)
 p, e, _ = oracle.pack_canonical(s.numpy(), a.numpy(), 64)
