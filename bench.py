@@ -676,7 +676,8 @@ def main():
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": ws_size, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 5), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "u8 keys, fp32 LUT/accumulate, fp16 in/out",
+            "scaling": "strong", "vs_baseline": None, "dtype": "fp32",
+            "dtype_detail": "u8 key bytes index fp32 LUT entries, fp32 accumulate, fp16 x in / y out",
             "data": "synthetic greedy-BCQ layers (synth.py), random activations with outlier channels",
             "config": {"workload": WORKLOAD, "us_per_token": round(us_step, 2),
                        "us_per_call_avg": round(us_step / len(launches), 3), "launches_per_step": len(launches),
