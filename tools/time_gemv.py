@@ -11,6 +11,13 @@ import torch  # noqa: E402
 import paper_2406_05981_b200 as sa  # noqa: E402
 import synth  # noqa: E402
 
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if os.environ.get("SHIFTADD_LIB") == "dev":   # the dev build and its experiment variants
+    import ctypes
+    sa._LIB_PATH = os.path.join(ROOT, "paper_2406_05981_b200", "libshiftadd_dev.so")
+    sa.lib().shiftadd_dev_set_variant.argtypes = [ctypes.c_int]
+    sa.lib().shiftadd_dev_set_variant(int(os.environ.get("VARIANT", "0")))
+
 ap = argparse.ArgumentParser()
 ap.add_argument("shapes", nargs="+")
 ap.add_argument("--pdl", action="store_true")
