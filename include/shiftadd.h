@@ -296,6 +296,17 @@ shiftadd_status shiftadd_pack_apot2(const int8_t* signs, const float* alpha, int
 shiftadd_status shiftadd_lut_gemm_apot2(const uint16_t* x, int ldx, const uint8_t* planes, const int8_t* exps,
                                         const int8_t* exps2, int layout, int M, int N, int K, int q, int g,
                                         uint16_t* y, int ldy, unsigned flags, void* stream);
+/* shiftadd_lut_gemm_apot2_ws: the same with a workspace, which lets tiled batch-1 layers the
+ *   cluster kernel cannot take (K > 4096: the LLaMA-2-70B / OPT-66B shapes; or with
+ *   SHIFTADD_FLAG_SPLITK) run on the all-SM streaming kernel (id 8) with the second-term codes
+ *   streamed beside the exponents (exps, exps2 16-B aligned; workspace
+ *   shiftadd_workspace_bytes_apot2(N, K) bytes, same zero-once contract as shiftadd_lut_gemm).
+ *   flags: 0 or SHIFTADD_FLAG_PDL | SHIFTADD_FLAG_SPLITK. */
+size_t shiftadd_workspace_bytes_apot2(int N, int K);
+shiftadd_status shiftadd_lut_gemm_apot2_ws(const uint16_t* x, int ldx, const uint8_t* planes, const int8_t* exps,
+                                           const int8_t* exps2, int layout, int M, int N, int K, int q, int g,
+                                           uint16_t* y, int ldy, void* workspace, size_t workspace_bytes,
+                                           unsigned flags, void* stream);
 
 /* NEXT-f4 -- Alg. 1 alternating multi-bit BCQ quantiser, the step before
  * shiftadd_pack.  Per scale group (g consecutive k of one output row of w fp32 [N][K]):

@@ -98,6 +98,11 @@ def lib():
         L.shiftadd_lut_gemm_colwise.restype = c_int
         L.shiftadd_lut_gemm_colwise.argtypes = [vp, c_int, vp, vp, c_int, c_int, c_int, c_int, c_int, vp, c_int, vp,
                                                 c_size, ctypes.c_uint, vp]
+        L.shiftadd_workspace_bytes_apot2.restype = c_size
+        L.shiftadd_workspace_bytes_apot2.argtypes = [c_int, c_int]
+        L.shiftadd_lut_gemm_apot2_ws.restype = c_int
+        L.shiftadd_lut_gemm_apot2_ws.argtypes = [vp, c_int, vp, vp, vp, c_int, c_int, c_int, c_int, c_int, c_int,
+                                                 vp, c_int, vp, c_size, ctypes.c_uint, vp]
         L.shiftadd_pack_apot2.restype = c_int
         L.shiftadd_pack_apot2.argtypes = [vp, vp, c_int, c_int, c_int, c_int, c_int, vp, vp, vp, vp, vp]
         L.shiftadd_lut_gemm_apot2.restype = c_int
@@ -448,20 +453,23 @@ def lut_gemm(x: torch.Tensor, layer: PackedLayer, out: torch.Tensor | None = Non
         lut_gemv_blockwise(x2[0], layer, out=out[0], pdl=pdl, workspace=workspace, stream=stream)
         return out[0] if squeeze else out
     if layer.colwise:
-        if M != 1:
-            raise ShiftAddError("column-wise layers: batch-1 only (shiftadd_lut_gemv_colwise)")
-        lut_gemv_colwise(x2[0], layer, out=out[0], pdl=pdl, stream=stream)
+        lut_gemv_colwise(x2, layer, out=out[:, :layer.N] if M > 1 else out[0], pdl=pdl, stream=stream,
+                         workspace=workspace, splitk=splitk)
         return out[0] if squeeze else out
     if layer.exps2 is not None:
         if torch.cuda.current_device() != dev.index:
             torch.cuda.set_device(dev)
         sptr = (stream if stream is not None else torch.cuda.current_stream(dev)).cuda_stream
-        st = lib().shiftadd_lut_gemm_apot2(x2.data_ptr(), x2.stride(0), layer.planes.data_ptr(),
-                                           layer.exps.data_ptr(), layer.exps2.data_ptr(), layer.layout, M,
-                                           layer.N, layer.K, layer.q, layer.g, out.data_ptr(), out.stride(0),
-                                           FLAG_PDL if pdl else 0, sptr)
+        need = int(lib().shiftadd_workspace_bytes_apot2(layer.N, layer.K)) if layer.layout == LAYOUT_TILED else 0
+        ws = (workspace or _workspace_for(dev, stream)).get(need)
+        st = lib().shiftadd_lut_gemm_apot2_ws(x2.data_ptr(), x2.stride(0), layer.planes.data_ptr(),
+                                              layer.exps.data_ptr(), layer.exps2.data_ptr(), layer.layout, M,
+                                              layer.N, layer.K, layer.q, layer.g, out.data_ptr(), out.stride(0),
+                                              ws.data_ptr() if ws is not None else None,
+                                              ws.numel() if ws is not None else 0,
+                                              (FLAG_PDL if pdl else 0) | (FLAG_SPLITK if splitk else 0), sptr)
         if st:
-            _check(st, "shiftadd_lut_gemm_apot2")
+            _check(st, "shiftadd_lut_gemm_apot2_ws")
         return out[0] if squeeze else out
     need = layer._ws_bytes.get(M)
     if need is None:

@@ -431,6 +431,19 @@ shiftadd_status shiftadd_pack_apot2(const int8_t* signs, const float* alpha, int
 shiftadd_status shiftadd_lut_gemm_apot2(const uint16_t* x, int ldx, const uint8_t* planes, const int8_t* exps,
                                         const int8_t* exps2, int layout, int M, int N, int K, int q, int g,
                                         uint16_t* y, int ldy, unsigned flags, void* stream) {
+  return shiftadd_lut_gemm_apot2_ws(x, ldx, planes, exps, exps2, layout, M, N, K, q, g, y, ldy, nullptr, 0, flags,
+                                    stream);
+}
+
+size_t shiftadd_workspace_bytes_apot2(int N, int K) {
+  if (N < 1 || N > kMaxRows || K < kTileK || K % kTileK) return 0;
+  return stream_workspace_bytes(1, K / kTileK, (N + kTileRows - 1) / kTileRows);
+}
+
+shiftadd_status shiftadd_lut_gemm_apot2_ws(const uint16_t* x, int ldx, const uint8_t* planes, const int8_t* exps,
+                                           const int8_t* exps2, int layout, int M, int N, int K, int q, int g,
+                                           uint16_t* y, int ldy, void* workspace, size_t workspace_bytes,
+                                           unsigned flags, void* stream) {
   if (!x || !planes || !exps || !exps2 || !y) return fail(SHIFTADD_ERR_INVALID, "null pointer argument");
   shiftadd_status st = check_shape(q, N, K, g, 4);
   if (st != SHIFTADD_OK) return st;
@@ -438,16 +451,42 @@ shiftadd_status shiftadd_lut_gemm_apot2(const uint16_t* x, int ldx, const uint8_
   if (M < 1) return fail(SHIFTADD_ERR_INVALID, "M=%d < 1", M);
   if (M > 16) return fail(SHIFTADD_ERR_UNSUPPORTED, "M=%d > 16", M);
   if (ldx < K || ldy < N) return fail(SHIFTADD_ERR_INVALID, "ldx=%d < K=%d or ldy=%d < N=%d", ldx, K, ldy, N);
-  if (flags & ~SHIFTADD_FLAG_PDL) return fail(SHIFTADD_ERR_INVALID, "unknown flags 0x%x", flags);
+  if (flags & ~(SHIFTADD_FLAG_PDL | SHIFTADD_FLAG_SPLITK)) return fail(SHIFTADD_ERR_INVALID, "unknown flags 0x%x", flags);
   if (!aligned(x, 16) || (M > 1 && (ldx % 8)) || !aligned(planes, 16) || !aligned(y, 2))
     return fail(SHIFTADD_ERR_INVALID, "misaligned pointer (x rows and planes need 16 B)");
   if (layout == SHIFTADD_LAYOUT_TILED && M != 1)
     return fail(SHIFTADD_ERR_UNSUPPORTED, "additive-PoT-2 tiled path is batch-1 (use the canonical layout)");
   DevInfo di;
   if ((st = device_info(&di)) != SHIFTADD_OK) return st;
-  if (layout == SHIFTADD_LAYOUT_TILED && !cluster_applicable(N, K, q, di.sms))
-    return fail(SHIFTADD_ERR_UNSUPPORTED, "additive-PoT-2 tiled path: K=%d N=%d q=%d outside the cluster kernel", K,
-                N, q);
+  // the cluster kernel for K <= 4096 (and, without a workspace, wherever it applies)
+  const bool cluster = layout == SHIFTADD_LAYOUT_TILED && !(flags & SHIFTADD_FLAG_SPLITK) &&
+                       (K <= 4096 || !workspace) && cluster_applicable(N, K, q, di.sms);
+  if (layout == SHIFTADD_LAYOUT_TILED && !cluster) {
+    // the all-SM streaming kernel (id 8) with the second-term codes as a third ring array
+    if (K < 2 * kTileK || !stream_shape_ok(K, di.sms) || !aligned(exps, 16) || !aligned(exps2, 16))
+      return fail(SHIFTADD_ERR_UNSUPPORTED, "additive-PoT-2 tiled path: K=%d N=%d q=%d has no kernel", K, N, q);
+    const size_t need = shiftadd_workspace_bytes_apot2(N, K);
+    if (!workspace || workspace_bytes < need || !aligned(workspace, 16))
+      return fail(SHIFTADD_ERR_INVALID, "workspace needs %zu bytes, 16-B aligned (got %zu)", need, workspace_bytes);
+    StreamLaunch L = {};
+    L.x = reinterpret_cast<const __half*>(x);
+    L.M = 1;
+    L.ldx = K;
+    L.K = K;
+    L.nseg = 1;
+    L.seg[0] = StreamSeg{planes, exps, reinterpret_cast<__half*>(y), q, N};
+    L.exps2 = exps2;
+    L.workspace = workspace;
+    L.grid = di.sms;
+    L.su = 16;
+    const int slot = L.su * q * (kTileBytes + 2 * kTileExps);
+    L.nst = (kStreamSmemBudget - 64 * 1024 - 640) / slot;
+    L.nst = L.nst > 16 ? 16 : L.nst;
+    L.pdl = (flags & SHIFTADD_FLAG_PDL) ? 1 : 0;
+    const cudaError_t e = launch_lut_stream(L, reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "lut_gemm_apot2 (streaming) launch");
+    return SHIFTADD_OK;
+  }
   GemmArgs a;
   a.x = reinterpret_cast<const __half*>(x);
   a.ldx = ldx;
@@ -463,7 +502,7 @@ shiftadd_status shiftadd_lut_gemm_apot2(const uint16_t* x, int ldx, const uint8_
   a.ldy = ldy;
   a.workspace = nullptr;
   a.workspace_bytes = 0;
-  a.flags = flags;
+  a.flags = flags & SHIFTADD_FLAG_PDL;
   a.stream = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t e;
   if (layout == SHIFTADD_LAYOUT_CANONICAL) e = launch_gemm_generic(a, plan_generic(M, N, K, q, g, di.sms));

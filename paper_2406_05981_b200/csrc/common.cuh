@@ -266,6 +266,7 @@ struct StreamLaunch {
   int colwise;             // 1: exps_bw holds NEXT-f1 column-wise exponents [q][K] instead
   GatherArgs gather;       // NEXT-f3 (M = 1, one segment, K >= 512): y into every rank's buffer
   int one_slice;           // M = 1: one slice per CTA (grid = S x floor(#SMs / S)), see abi.cu
+  const int8_t* exps2;     // NEXT-f2 second additive-PoT term codes (M = 1, one segment; tiled like exps)
 };
 
 // The persistent decode program (lut_program.cu, kernel id 9): ordered calls of the fused form.

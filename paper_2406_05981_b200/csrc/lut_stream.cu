@@ -89,6 +89,8 @@ struct StreamParams {
   GatherArgs ga;           // NEXT-f3 fused all-gather epilogue (P == 0: off)
   int dev_mode;            // development builds only (co-roof experiments), 0 otherwise
   const unsigned long long* part_end;   // end of the partial region (bounds-checked builds)
+  const int8_t* exps2;     // NEXT-f2 (BW = 5): second-term codes, streamed as a third array
+  int slot_exps2;          // its offset in a ring slot
 };
 
 // A split-K partial word store (bounds-checked builds: inside [part, part_end)).
@@ -126,10 +128,54 @@ __device__ __forceinline__ void unit_dot2_regs(int lane, int seed, const uint32_
 }
 #endif
 
+// NEXT-f2, additive PoT with two terms (Eq. 2): per plane the 128-k chunk
+// sum p gives v1 = p 2^{P1} (exponent add) plus the second term sign(c2) v1 2^{-|c2|}
+// (shift_apot2, common.cuh) -- the cluster kernel's arithmetic, on two units at once.
+template <int Q, uint32_t HOFF>
+__device__ __forceinline__ void unit_dot2_ap2(uint32_t sp0, uint32_t se0, uint32_t sq0, uint32_t sp1, uint32_t se1,
+                                              uint32_t sq1, bool v1, const uint32_t (&cst)[4], float (&acc)[2]) {
+  uint4 w[2][Q];
+  int e[2][Q], c[2][Q];
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    w[0][i] = lds_u4(sp0 + i * kTileBytes);
+    e[0][i] = lds_s8(se0 + i * kTileExps);
+    c[0][i] = lds_s8(sq0 + i * kTileExps);
+    if (v1) {
+      w[1][i] = lds_u4(sp1 + i * kTileBytes);
+      e[1][i] = lds_s8(se1 + i * kTileExps);
+      c[1][i] = lds_s8(sq1 + i * kTileExps);
+    } else {
+      w[1][i] = make_uint4(0, 0, 0, 0);
+      e[1][i] = SHIFTADD_EXP_ZERO;
+      c[1][i] = 0;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < Q; ++i) {
+    float pp[2][4];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const uint32_t word = (j < 4) ? w[u][i].x : (j < 8) ? w[u][i].y : (j < 12) ? w[u][i].z : w[u][i].w;
+        const float v = lds_f32(kDynBase + HOFF + prmt(word, cst[j >> 2], step_sel(j)));
+        pp[u][j & 3] = j < 4 ? v : pp[u][j & 3] + v;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const float t1 = shift_pow2((pp[u][0] + pp[u][1]) + (pp[u][2] + pp[u][3]), e[u][i]);
+      const float vt = t1 + shift_apot2(t1, c[u][i]);
+      acc[u] = i == 0 ? vt : acc[u] + vt;
+    }
+  }
+}
+
 // Consumer side of one run (slice s, segment sg, row groups [rga, re)): the run's stages of su
 // units, taken two at a time -- warp w processes unit w of stage t and unit w of stage t + 1
 // together, then releases both.
-template <int Q, uint32_t HOFF>
+template <int Q, uint32_t HOFF, bool AP2 = false>
 __device__ __forceinline__ void consume_run(const StreamParams& p, const SegDev& sg, int s, int rga, int re,
                                             RingPos& rp, int& t, uint32_t ring, uint32_t full, uint32_t empty,
                                             const uint32_t (&cst)[4], int wu, int lane, unsigned long long ep,
@@ -162,7 +208,14 @@ __device__ __forceinline__ void consume_run(const StreamParams& p, const SegDev&
 #ifdef SHIFTADD_DEV_TRACE
     if (u0 && (p.dev_mode & 8)) unit_dot2_regs<Q, HOFF>(lane, rg, cst, acc); else
 #endif
-    if (u0)
+    if (u0 && AP2)
+      unit_dot2_ap2<Q, HOFF>(slot0 + (uint32_t)(wu * Q * kTileBytes + 16 * lane),
+                             slot0 + (uint32_t)(p.slot_planes + wu * Q * kTileExps + lane),
+                             slot0 + (uint32_t)(p.slot_exps2 + wu * Q * kTileExps + lane),
+                             slot1 + (uint32_t)(wu * Q * kTileBytes + 16 * lane),
+                             slot1 + (uint32_t)(p.slot_planes + wu * Q * kTileExps + lane),
+                             slot1 + (uint32_t)(p.slot_exps2 + wu * Q * kTileExps + lane), u1, cst, acc);
+    else if (u0)
       unit_dot2<Q, HOFF>(slot0 + (uint32_t)(wu * Q * kTileBytes + 16 * lane),
                          slot0 + (uint32_t)(p.slot_planes + wu * Q * kTileExps + lane),
                          slot1 + (uint32_t)(wu * Q * kTileBytes + 16 * lane),
@@ -194,16 +247,16 @@ __device__ __forceinline__ void consume_run(const StreamParams& p, const SegDev&
   }
 }
 
-template <uint32_t HOFF>
+template <uint32_t HOFF, bool AP2 = false>
 __device__ __forceinline__ void consume_run_q(const StreamParams& p, const SegDev& sg, int s, int rga, int re,
                                               RingPos& rp, int& t, uint32_t ring, uint32_t full, uint32_t empty,
                                               const uint32_t (&cst)[4], int wu, int lane, unsigned long long ep,
                                               bool skew) {
   switch (sg.q) {
-    case 1: consume_run<1, HOFF>(p, sg, s, rga, re, rp, t, ring, full, empty, cst, wu, lane, ep, skew); break;
-    case 2: consume_run<2, HOFF>(p, sg, s, rga, re, rp, t, ring, full, empty, cst, wu, lane, ep, skew); break;
-    case 3: consume_run<3, HOFF>(p, sg, s, rga, re, rp, t, ring, full, empty, cst, wu, lane, ep, skew); break;
-    default: consume_run<4, HOFF>(p, sg, s, rga, re, rp, t, ring, full, empty, cst, wu, lane, ep, skew); break;
+    case 1: consume_run<1, HOFF, AP2>(p, sg, s, rga, re, rp, t, ring, full, empty, cst, wu, lane, ep, skew); break;
+    case 2: consume_run<2, HOFF, AP2>(p, sg, s, rga, re, rp, t, ring, full, empty, cst, wu, lane, ep, skew); break;
+    case 3: consume_run<3, HOFF, AP2>(p, sg, s, rga, re, rp, t, ring, full, empty, cst, wu, lane, ep, skew); break;
+    default: consume_run<4, HOFF, AP2>(p, sg, s, rga, re, rp, t, ring, full, empty, cst, wu, lane, ep, skew); break;
   }
 }
 
@@ -808,11 +861,12 @@ __global__ void __launch_bounds__((NWC + 1) * 32, MINB) lut_stream_kernel(const 
         for (int rg = a.rg; rg < re; ++t, rp.next(p.nst)) {
           if (rp.k > 0) mbar_wait(empty + 8 * rp.j, (uint32_t)((rp.k - 1) & 1));
           int n = re - rg < p.su ? re - rg : p.su;
-          if (BW >= 2) {   // stages do not cross a row-block boundary (column-wise: one block)
+          if (BW == 2 || BW == 3) {   // stages do not cross a row-block boundary (column-wise: one block)
             const int bend = (rg / p.bw_rgb + 1) * p.bw_rgb;
             n = bend - rg < n ? bend - rg : n;
           }
-          const uint32_t bp = (uint32_t)(n * sg.q * kTileBytes), be = BW ? 0u : (uint32_t)(n * sg.q * kTileExps);
+          const uint32_t bp = (uint32_t)(n * sg.q * kTileBytes);
+          const uint32_t be = (BW && BW != 5) ? 0u : (uint32_t)(n * sg.q * kTileExps);
           const uint32_t fb = full + 8 * rp.j;
 #ifdef SHIFTADD_DEV_TRACE
           if (p.dev_mode & 16) {   // co-roof experiment: no copies (no HBM, no TMA writes)
@@ -821,10 +875,12 @@ __global__ void __launch_bounds__((NWC + 1) * 32, MINB) lut_stream_kernel(const 
             continue;
           }
 #endif
-          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(bp + be) : "memory");
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb),
+                       "r"(bp + (BW == 5 ? 2u : 1u) * be) : "memory");
           const uint32_t dst = ring + (uint32_t)(rp.j * p.slot);
           bulk_g2s(dst, sg.planes + (ub + rg) * sg.q * kTileBytes, bp, fb, pol);
-          if (!BW) bulk_g2s(dst + (uint32_t)p.slot_planes, sg.exps + (ub + rg) * sg.q * kTileExps, be, fb, pol);
+          if (!BW || BW == 5) bulk_g2s(dst + (uint32_t)p.slot_planes, sg.exps + (ub + rg) * sg.q * kTileExps, be, fb, pol);
+          if (BW == 5) bulk_g2s(dst + (uint32_t)p.slot_exps2, p.exps2 + (ub + rg) * sg.q * kTileExps, be, fb, pol);
           rg += n;
         }
         next_run(p, a, re);
@@ -844,7 +900,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, MINB) lut_stream_kernel(const 
       if (tid == 32 && p.S > 1)   // a lane whose x does not gate warp 0
         asm volatile("st.shared.u32 [%0], %1;" ::"r"(s_epoch), "r"((unsigned)(ld_relaxed_u64(p.done) >> 32) + 1u)
                      : "memory");
-      if (MW == 1 && BW < 2) {
+      if (MW == 1 && (BW < 2 || BW == 5)) {
         const uint64_t pol_keep = policy_evict_last();
         const uint4 xa = ldg_keep(p.x + (size_t)s0 * kTileK + 8 * lane, pol_keep);
         uint4 xb = xa;
@@ -882,7 +938,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, MINB) lut_stream_kernel(const 
       const bool skew = p.skew && warp >= NWC / 2;
       int t = 0;
       uint4 xs[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
-      if (BW >= 2 && MW == 1 && any) {
+      if (BW >= 2 && BW <= 3 && MW == 1 && any) {
         const uint64_t pol_keep = policy_evict_last();
         xs[0] = ldg_keep(p.x + (size_t)s0 * kTileK + 8 * lane, pol_keep);
         if (two) xs[1] = ldg_keep(p.x + (size_t)(s0 + 1) * kTileK + 8 * lane, pol_keep);
@@ -890,7 +946,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, MINB) lut_stream_kernel(const 
       int cur = -1;
       for (Pos a = start; before(a, end);) {
         const int re = run_end(p, a, end);
-        if (BW >= 2) {
+        if (BW == 2 || BW == 3) {
           consume_run_lut_q<NWC, BW == 3, MW == 2>(p, p.seg[a.g], a.s, a.rg, re, rp, ring, full, empty, cst, wu,
                                                    lane, ep, a.s == s0 ? xs[0] : xs[1], cur);
         } else if (BW == 1) {
@@ -899,9 +955,10 @@ __global__ void __launch_bounds__((NWC + 1) * 32, MINB) lut_stream_kernel(const 
           else
             consume_run_bw_q<128u>(p, p.seg[a.g], a.s, a.rg, re, rp, ring, full, empty, cst, wu, lane, ep);
         } else if (a.s == s0) {
-          consume_run_q<0u>(p, p.seg[a.g], a.s, a.rg, re, rp, t, ring, full, empty, cst, wu, lane, ep, skew);
+          consume_run_q<0u, BW == 5>(p, p.seg[a.g], a.s, a.rg, re, rp, t, ring, full, empty, cst, wu, lane, ep, skew);
         } else {
-          consume_run_q<128u>(p, p.seg[a.g], a.s, a.rg, re, rp, t, ring, full, empty, cst, wu, lane, ep, skew);
+          consume_run_q<128u, BW == 5>(p, p.seg[a.g], a.s, a.rg, re, rp, t, ring, full, empty, cst, wu, lane, ep,
+                                       skew);
         }
         next_run(p, a, re);
       }
@@ -1080,6 +1137,8 @@ cudaError_t launch_lut_stream(const StreamLaunch& L, cudaStream_t stream) {
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(lut_stream_kernel<16, 1, 2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(lut_stream_kernel<16, 1, 1, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    if (e == cudaSuccess)
       e = cudaFuncSetAttribute(lut_stream_kernel<8, 2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 113 * 1024);
     attr_err[dev] = e;
   });
@@ -1124,6 +1183,9 @@ cudaError_t launch_lut_stream(const StreamLaunch& L, cudaStream_t stream) {
   p.su = L.su;
   p.slot = L.su * qmax * (kTileBytes + kTileExps);
   p.slot_planes = L.su * qmax * kTileBytes;
+  p.exps2 = L.exps2;
+  p.slot_exps2 = p.slot;
+  if (L.exps2) p.slot += L.su * qmax * kTileExps;   // the second-term codes after the exponents
   p.pdl = L.pdl;
   p.exps_bw = L.exps_bw;
   p.ga = L.gather;
@@ -1166,6 +1228,11 @@ cudaError_t launch_lut_stream(const StreamLaunch& L, cudaStream_t stream) {
     if (p.bw_rgb > 0) return cudaLaunchKernelEx(&c, lut_stream_kernel<16, 1, 1, 2>, p);
     if (L.su != 8) return cudaErrorInvalidValue;
     return cudaLaunchKernelEx(&c, lut_stream_kernel<8, 1, 1, 1>, p);
+  }
+  if (L.exps2) {   // NEXT-f2: M = 1, one segment
+    if (MW != 1 || L.nseg != 1 || L.exps_bw) return cudaErrorInvalidValue;
+    c.dynamicSmemBytes = p.lut_bytes + L.nst * p.slot + kBarBytes;
+    return cudaLaunchKernelEx(&c, lut_stream_kernel<16, 1, 1, 5>, p);
   }
   if (L.half && MW == 1) return cudaLaunchKernelEx(&c, lut_stream_kernel<8, 2, 1>, p);
   switch (MW) {

@@ -152,7 +152,11 @@ def test_apot2_validation_happens_before_any_launch(L):
     assert L.shiftadd_pack_apot2(p, p, 3, 16, 256, 128, 1, p, p, None, None, None) == 2
     assert L.shiftadd_lut_gemm_apot2(p, 512, p, p, None, 1, 1, 64, 512, 3, 128, p, 64, 0, None) == 2
     assert L.shiftadd_lut_gemm_apot2(p, 512, p, p, p, 1, 2, 64, 512, 3, 128, p, 64, 0, None) == 6
-    assert L.shiftadd_lut_gemm_apot2(p, 512, p, p, p, 1, 1, 64, 512, 3, 128, p, 64, 2, None) == 2
+    assert L.shiftadd_lut_gemm_apot2(p, 512, p, p, p, 1, 1, 64, 512, 3, 128, p, 64, 8, None) == 2   # unknown flag
+    # the workspace form: K > 4096 tiled needs the workspace (streaming kernel), validated on the host
+    assert L.shiftadd_workspace_bytes_apot2(64, 8192) > 0
+    assert L.shiftadd_lut_gemm_apot2_ws(p, 8192, p, p, p, 1, 1, 64, 8192, 3, 128, p, 64, p, 16, 8, None) == 2
+    assert L.shiftadd_lut_gemm_apot2_ws(p, 8192, p, p, p, 1, 2, 64, 8192, 3, 128, p, 64, p, 1 << 16, 0, None) == 6
 
 
 def test_quantize_validation_happens_before_any_launch(L):

@@ -46,15 +46,19 @@ def test_apot2_pack_bit_exact(sa, layout):
     assert int(np.count_nonzero(e2)) > 0.9 * e2.size     # nearly every group has a 2nd term
 
 
-@pytest.mark.parametrize("q,N,K", [(3, 768, 768), (1, 40, 512), (2, 4096, 4096), (3, 16384, 4096),
-                                   (2, 2048, 8192)])
-def test_apot2_tiled_gemv_parity(sa, q, N, K):
+# K <= 4096: cluster kernel (and the streaming kernel with splitk); K > 4096 -- the LLaMA-2-7B
+# down_proj, a 70B-gate-like K = 8192 and a ragged K = 28672 shape -- on the streaming kernel
+@pytest.mark.parametrize("q,N,K,splitk", [(3, 768, 768, False), (1, 40, 512, False), (2, 4096, 4096, False),
+                                          (3, 16384, 4096, False), (2, 2048, 8192, False), (3, 768, 768, True),
+                                          (2, 4096, 4096, True), (2, 4096, 11008, False), (3, 3000, 8192, False),
+                                          (4, 600, 28672, False)])
+def test_apot2_tiled_gemv_parity(sa, q, N, K, splitk):
     g = 128
     s, a = synth.gen_layer(q, N, K, g, seed=synth.seed_for(9, q, N % 7))
     planes, e1, e2, _ = oracle.pack_apot2(s.numpy(), a.numpy(), g)
     L = sa.pack_apot2(s.to(DEV), a.to(DEV), g, layout=sa.LAYOUT_TILED)
     x = synth.gen_x(1, K, seed=synth.seed_for(9, 99))
-    y = sa.lut_gemm(x.to(DEV), L, pdl=True)
+    y = sa.lut_gemm(x.to(DEV), L, pdl=True, splitk=splitk)
     torch.cuda.synchronize()
     err = oracle.err_floor(y.float().cpu().numpy(), oracle.gemm_apot2(x.numpy(), planes, e1, e2, g))
     assert err <= TOL, err
@@ -73,8 +77,8 @@ def test_apot2_canonical_gemm_parity(sa, M, g):
     assert err <= TOL, err
 
 
-@pytest.mark.parametrize("layout", [1, 0])
-def test_apot2_exact_two_term_scales_basis_vectors(sa, layout):
+@pytest.mark.parametrize("layout,splitk", [(1, False), (1, True), (0, False)])
+def test_apot2_exact_two_term_scales_basis_vectors(sa, layout, splitk):
     """alpha = +-(2^A + sigma 2^B), A - B >= 2, is represented exactly by two terms, so for
     x = e_j the output is fp16(sum_i alpha_i s_i[:, j]) -- computed from alpha, not the oracle."""
     rng = np.random.default_rng(7)
@@ -88,7 +92,7 @@ def test_apot2_exact_two_term_scales_basis_vectors(sa, layout):
     W = (s.astype(np.float64) * np.repeat(alpha.astype(np.float64), g, axis=2)).sum(axis=0)
     for j in (0, 9, 128, 300, K - 1):
         x = synth.gen_special_x("basis", 1, K, j=j)
-        y = sa.lut_gemm(x.to(DEV), L).cpu().numpy()
+        y = sa.lut_gemm(x.to(DEV), L, splitk=splitk).cpu().numpy()
         assert np.array_equal(y[0], oracle.to_fp16(W[:, j]))
 
 
