@@ -89,6 +89,15 @@ for (qc, Nc, Kc, Mc) in ((2, 200, 1024, 1), (3, 100, 8192, 1), (2, 96, 1024, 3))
     yc = sa.lut_gemv_colwise(xc2.to(dev), Lc, pdl=True)
     torch.cuda.synchronize()
     check("colwise K%d M%d" % (Kc, Mc), yc.reshape(Mc, Nc), oracle.gemm_colwise(xc2.numpy(), pc, ec))
+# additive PoT, two terms: cluster kernel and the streaming kernel (K > 4096)
+for (qa, Na, Ka) in ((2, 128, 1024), (3, 100, 6144)):
+    sA2, aA2 = synth.gen_layer(qa, Na, Ka, 128, seed=synth.seed_for(12, 90, Ka))
+    pA2, e1A2, e2A2, _ = oracle.pack_apot2(sA2.numpy(), aA2.numpy(), 128)
+    LA2 = sa.pack_apot2(sA2.to(dev), aA2.to(dev), 128, layout=sa.LAYOUT_TILED)
+    xA2 = synth.gen_x(1, Ka, seed=9)
+    yA2 = sa.lut_gemm(xA2.to(dev), LA2, pdl=True)
+    torch.cuda.synchronize()
+    check("apot2 K%d" % Ka, yA2, oracle.gemm_apot2(xA2.numpy(), pA2, e1A2, e2A2, 128))
 # canonical layout (generic kernel)
 s, a = synth.gen_layer(2, 64, 512, 64, seed=5)
 p, e, _ = oracle.pack_canonical(s.numpy(), a.numpy(), 64)
