@@ -12,7 +12,9 @@ import paper_2406_05981_b200 as sa  # noqa: E402
 import synth  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-if os.environ.get("SHIFTADD_LIB") == "dev":   # the dev build and its experiment variants
+if os.environ.get("SHIFTADD_LIB", "").endswith(".so"):   # an alternative build, for A/B timing
+    sa._LIB_PATH = os.path.join(ROOT, os.environ["SHIFTADD_LIB"])
+elif os.environ.get("SHIFTADD_LIB") == "dev":   # the dev build and its experiment variants
     import ctypes
     sa._LIB_PATH = os.path.join(ROOT, "paper_2406_05981_b200", "libshiftadd_dev.so")
     sa.lib().shiftadd_dev_set_variant.argtypes = [ctypes.c_int]
