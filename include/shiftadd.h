@@ -191,7 +191,8 @@ shiftadd_status shiftadd_lut_gemv_program(const shiftadd_call* calls, int ncalls
                                           size_t program_bytes, void* workspace, size_t workspace_bytes,
                                           unsigned flags, void* stream);
 
-/* The same ordered calls issued from the host as one kernel per call (no persistent kernel):
+/* The same ordered calls issued from the host as one kernel per call (no persistent kernel;
+ * each call is the shift-and-LUT linear layer of PAPER.md:182-187):
  * each call goes through shiftadd_lut_gemm (one segment) or shiftadd_lut_gemv_fused, all on
  * `stream`, so a decode step costs one C call instead of one per projection.  With
  * SHIFTADD_FLAG_PDL every launch is a programmatic dependent of the previous one (x read after
