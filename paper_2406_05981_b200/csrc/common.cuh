@@ -6,9 +6,26 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+
 #include "shiftadd.h"
 
 namespace shiftadd {
+
+// Runs f() (kernel-attribute setup: attributes are per device) once on each device that
+// launches, thread-safely, and returns its result for the current device.  Every call site
+// passes its own lambda, so each gets its own flags.
+template <class F>
+cudaError_t once_per_device(F f) {
+  static std::once_flag once[64];
+  static cudaError_t err[64];
+  int dev = 0;
+  const cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  std::call_once(once[dev], [&] { err[dev] = f(); });
+  return err[dev];
+}
 
 // Device-tiled layout geometry (include/shiftadd.h, SHIFTADD_LAYOUT_TILED).
 constexpr int kTileRows = 16;    // output rows per tile

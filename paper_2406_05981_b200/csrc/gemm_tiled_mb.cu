@@ -298,11 +298,11 @@ constexpr int kNW = 16;
 
 template <int Q, int MC>
 cudaError_t launch_q(const GemmArgs& a, const LaunchPlan& p) {
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
+  const cudaError_t attr_err = once_per_device([] {
+    cudaError_t attr_err = cudaSuccess;
     attr_err = cudaFuncSetAttribute(gemm_tiled_mb_kernel<Q, kNW, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     kDynSmemMb);
+    return attr_err;
   });
   if (attr_err != cudaSuccess) return attr_err;
   const int S = a.K / kTileK;

@@ -1196,13 +1196,13 @@ gemm_cluster_ring_m2_kernel(const __half* __restrict__ x, int ldx, const uint8_t
 
 template <int Q>
 cudaError_t launch_m2_q(const GemmArgs& a, const LaunchPlan& p, int C) {
-  static std::once_flag once;
-  static cudaError_t err = cudaSuccess;
-  std::call_once(once, [] {
+  const cudaError_t err = once_per_device([] {
+    cudaError_t err = cudaSuccess;
     err = cudaFuncSetAttribute(gemm_cluster_ring_m2_kernel<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                M2Map::total);
     if (err == cudaSuccess)
       err = cudaFuncSetAttribute(gemm_cluster_ring_m2_kernel<Q>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    return err;
   });
   if (err != cudaSuccess) return err;
   const int S = a.K / kTileK;
@@ -1440,13 +1440,13 @@ gemm_cluster_ring_m4_kernel(const __half* __restrict__ x, int ldx, int M, const 
 
 template <int Q>
 cudaError_t launch_m4_q(const GemmArgs& a, const LaunchPlan& p, int C) {
-  static std::once_flag once;
-  static cudaError_t err = cudaSuccess;
-  std::call_once(once, [] {
+  const cudaError_t err = once_per_device([] {
+    cudaError_t err = cudaSuccess;
     err = cudaFuncSetAttribute(gemm_cluster_ring_m4_kernel<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                M4Map::total);
     if (err == cudaSuccess)
       err = cudaFuncSetAttribute(gemm_cluster_ring_m4_kernel<Q>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    return err;
   });
   if (err != cudaSuccess) return err;
   const int S = a.K / kTileK;
@@ -1500,14 +1500,14 @@ int variant_smem(int v) { return v == kFull4 ? Smem<4>::total : v >= kRing ? Rin
 
 template <int Q, bool H16 = false>
 cudaError_t set_ring_attrs() {
-  static std::once_flag once;
-  static cudaError_t err = cudaSuccess;
-  std::call_once(once, [] {
+  const cudaError_t err = once_per_device([] {
+    cudaError_t err = cudaSuccess;
     err = cudaFuncSetAttribute(gemv_cluster_ring_kernel<Q, H16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                RingCfg<Q>::smem);
     if (err == cudaSuccess)
       err = cudaFuncSetAttribute(gemv_cluster_ring_kernel<Q, H16>,
                                  cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    return err;
   });
   return err;
 }
@@ -1535,14 +1535,14 @@ int occupancy_ring_clusters(int C) {
 
 template <int Q, int SCM, int NW, int REGS, bool COLW = false, bool AP2 = false>
 cudaError_t set_attrs() {
-  static std::once_flag once;
-  static cudaError_t err = cudaSuccess;
-  std::call_once(once, [] {
+  const cudaError_t err = once_per_device([] {
+    cudaError_t err = cudaSuccess;
     err = cudaFuncSetAttribute(gemv_cluster_kernel<Q, SCM, NW, REGS, COLW, AP2>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<SCM>::total);
     if (err == cudaSuccess)   // clusters of up to 16 (column-wise; one slice per CTA)
       err = cudaFuncSetAttribute(gemv_cluster_kernel<Q, SCM, NW, REGS, COLW, AP2>,
                                  cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    return err;
   });
   return err;
 }
@@ -1662,13 +1662,13 @@ int fused_cluster_grid(int K, int RGtot, int* C_out) {
 }
 
 cudaError_t launch_fused_impl(const StreamLaunch& L, cudaStream_t stream) {
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
+  const cudaError_t attr_err = once_per_device([] {
+    cudaError_t attr_err = cudaSuccess;
     attr_err = cudaFuncSetAttribute(gemv_cluster_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     RingCfg<1>::smem);
     if (attr_err == cudaSuccess)
       attr_err = cudaFuncSetAttribute(gemv_cluster_fused_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    return attr_err;
   });
   if (attr_err != cudaSuccess) return attr_err;
   FusedArgs A = {};

@@ -451,11 +451,11 @@ constexpr int kDynSmem = kLutBytes + 16;  // 64 KB LUT + the dynamic mode's unit
 
 template <int Q, int NW, int REGS, int MODE>
 cudaError_t launch_k(const GemmArgs& a, const LaunchPlan& p) {
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
+  const cudaError_t attr_err = once_per_device([] {
+    cudaError_t attr_err = cudaSuccess;
     attr_err = cudaFuncSetAttribute(gemv_tiled_kernel<Q, NW, REGS, MODE>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
+    return attr_err;
   });
   if (attr_err != cudaSuccess) return attr_err;
   const int S = a.K / kTileK;
@@ -710,11 +710,11 @@ gemv_stream_kernel(const __half* __restrict__ x, const uint8_t* __restrict__ pla
 
 template <int Q>
 cudaError_t launch_stream_q(const GemmArgs& a, const LaunchPlan& p) {
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
+  const cudaError_t attr_err = once_per_device([] {
+    cudaError_t attr_err = cudaSuccess;
     attr_err = cudaFuncSetAttribute(gemv_stream_kernel<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     StreamSmem<Q>::total);
+    return attr_err;
   });
   if (attr_err != cudaSuccess) return attr_err;
   const int S = a.K / kTileK;

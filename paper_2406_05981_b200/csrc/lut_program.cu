@@ -26,6 +26,8 @@
 // dependency is "counter >= (L << 32) + j G"; calls without SHIFTADD_CALL_WAIT still wait for
 // call j-2 (its partial region is reused by call j).  Partial words carry the 32-bit tag
 // L ncalls + j + 1 and alternate between two regions by call parity.
+#include <mutex>
+
 #include "stream_dev.cuh"
 
 namespace shiftadd {
@@ -490,16 +492,17 @@ cudaError_t launch_lut_program(const void* program, int ncalls, uint64_t hash, i
                                void* workspace, int sms, cudaStream_t stream) {
   int smem = 0;
   const int nst = program_qmax_stages(qmax, &smem);
-  static bool attr_set[64] = {};
+  // kernel attributes are per device: set them once on each device that launches
+  static std::once_flag once[64];
+  static cudaError_t attr_err[64];
   int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return e;
+  const cudaError_t de = cudaGetDevice(&dev);
+  if (de != cudaSuccess) return de;
   if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
-  if (!attr_set[dev]) {
-    e = cudaFuncSetAttribute(lut_program_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_set[dev] = true;
-  }
+  std::call_once(once[dev], [dev] {
+    attr_err[dev] = cudaFuncSetAttribute(lut_program_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  });
+  if (attr_err[dev] != cudaSuccess) return attr_err[dev];
   ProgParams p = {};
   p.hdr = static_cast<const ProgHeader*>(program);
   p.calls = reinterpret_cast<const ProgCall*>(p.hdr + 1);
