@@ -264,6 +264,13 @@ struct GemmArgs {
 constexpr int kMaxSegments = 4;
 // its workspace region: after the split-K counters and the fused-gather launch counter
 constexpr size_t kStreamWsOff = kCounterBytes + 256;
+// Workspace map: [0, kCounterBytes) per-row-group arrival counters (kernels 1, 2; left zero);
+// kCounterBytes: the fused-gather launch counter (left zero); kStreamWsOff: kernel 8's epoch
+// word (never written by anything else); kPartOff: the split-K partials of whichever kernel
+// runs (kernels 1, 2: fp32; kernel 8: {epoch, fp32} words).  Partials of different calls may
+// overlap -- they are rewritten every call -- but nothing may overwrite the counters or the
+// epoch word, whose values carry over from call to call.
+constexpr size_t kPartOff = kStreamWsOff + 256;
 struct StreamSeg {
   const uint8_t* planes;
   const int8_t* exps;

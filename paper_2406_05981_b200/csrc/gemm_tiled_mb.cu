@@ -310,7 +310,7 @@ cudaError_t launch_q(const GemmArgs& a, const LaunchPlan& p) {
   const long long U = (long long)S * RG;
   const size_t Npad = (size_t)RG * kTileRows;
   unsigned* sync = S > 1 ? reinterpret_cast<unsigned*>(a.workspace) : nullptr;
-  float* partial = S > 1 ? reinterpret_cast<float*>(reinterpret_cast<char*>(a.workspace) + kCounterBytes) : nullptr;
+  float* partial = S > 1 ? reinterpret_cast<float*>(reinterpret_cast<char*>(a.workspace) + kPartOff) : nullptr;
   (void)Npad;
   const int pdl = (a.flags & SHIFTADD_FLAG_PDL) ? 1 : 0;
   cudaLaunchConfig_t cfg = {};
@@ -343,7 +343,7 @@ size_t workspace_gemm_tiled_mb(int M, int N, int K) {
   const size_t S = K / kTileK;
   if (S <= 1) return 0;
   const size_t RG = (N + kTileRows - 1) / kTileRows;
-  return kCounterBytes + (size_t)M * S * RG * kTileRows * sizeof(float);
+  return kPartOff + (size_t)M * S * RG * kTileRows * sizeof(float);
 }
 
 cudaError_t launch_gemm_tiled_mb(const GemmArgs& a, const LaunchPlan& p) {

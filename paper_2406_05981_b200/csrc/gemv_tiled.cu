@@ -462,7 +462,7 @@ cudaError_t launch_k(const GemmArgs& a, const LaunchPlan& p) {
   const int RG = (a.N + kTileRows - 1) / kTileRows;
   const long long U = (long long)S * RG;
   unsigned* sync = S > 1 ? reinterpret_cast<unsigned*>(a.workspace) : nullptr;
-  float* partial = S > 1 ? reinterpret_cast<float*>(reinterpret_cast<char*>(a.workspace) + kCounterBytes) : nullptr;
+  float* partial = S > 1 ? reinterpret_cast<float*>(reinterpret_cast<char*>(a.workspace) + kPartOff) : nullptr;
   const int pdl = (a.flags & SHIFTADD_FLAG_PDL) ? 1 : 0;
   const int dyn_kc = (cfg().dyn && S > 1 && S <= 1024 && p.grid % S == 0 && p.grid / S >= 2) ? p.grid / S : 0;
 
@@ -721,7 +721,7 @@ cudaError_t launch_stream_q(const GemmArgs& a, const LaunchPlan& p) {
   const int RG = (a.N + kTileRows - 1) / kTileRows;
   const long long U = (long long)S * RG;
   unsigned* sync = reinterpret_cast<unsigned*>(a.workspace);
-  float* partial = reinterpret_cast<float*>(reinterpret_cast<char*>(a.workspace) + kCounterBytes);
+  float* partial = reinterpret_cast<float*>(reinterpret_cast<char*>(a.workspace) + kPartOff);
   const int pdl = (a.flags & SHIFTADD_FLAG_PDL) ? 1 : 0;
   constexpr int npre = 1;   // stages requested before griddepcontrol.wait (measured best)
   unsigned long long* trace = nullptr;
@@ -790,7 +790,7 @@ size_t workspace_gemv_tiled(int N, int K) {
   const size_t S = K / kTileK;
   if (S <= 1) return 0;
   const size_t RG = (N + kTileRows - 1) / kTileRows;
-  return kCounterBytes + S * RG * kTileRows * sizeof(float);
+  return kPartOff + S * RG * kTileRows * sizeof(float);
 }
 
 cudaError_t launch_gemv_tiled(const GemmArgs& a, const LaunchPlan& p) {

@@ -176,8 +176,8 @@ __device__ __forceinline__ void consume_run_q(const ProgSeg& sg, int S, int s, i
 // CTA c's weight range of call cl (units assigned by their starting weight offset)
 __device__ __forceinline__ void cta_range(const ProgCall& cl, long long c, long long G, Pos& a, Pos& b) {
   const long long W = (long long)cl.S * cl.Ws;
-  a = pos_at(cl, c * W / G);
-  b = pos_at(cl, (c + 1) * W / G);
+  a = pos_at(cl, split_point(c, W, G));
+  b = pos_at(cl, split_point(c + 1, W, G));
 }
 
 // x of a call into L2 ahead of its dependency wait: a prefetch is only a hint (L2 is the point
@@ -354,7 +354,8 @@ __global__ void __launch_bounds__((kNWC + 1) * 32, 1) lut_program_kernel(const _
     if (S > 1) {
       // a5 owner phase: rows of the flattened row groups [c RGtot / G, (c+1) RGtot / G), T
       // threads per row over the slices in order (kernel 8's scheme)
-      const int og0 = (int)(c * cl.RGtot / G), og1 = (int)((c + 1) * cl.RGtot / G);
+      const int og0 = (int)((unsigned)c * (unsigned)cl.RGtot / (unsigned)G);   // 32-bit: G <= 256, RGtot <= 65536
+      const int og1 = (int)((unsigned)(c + 1) * (unsigned)cl.RGtot / (unsigned)G);
       const int MR = (og1 - og0) * kTileRows;
       for (int rb = 0; rb < MR; rb += kNC) {
         const int CR = MR - rb < kNC ? MR - rb : kNC;

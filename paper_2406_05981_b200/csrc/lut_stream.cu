@@ -826,11 +826,11 @@ __global__ void __launch_bounds__((NWC + 1) * 32, MINB) lut_stream_kernel(const 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (p.pdl) pdl_launch_dependents();
   const long long G = gridDim.x, W = (long long)p.S * p.Ws, c = blockIdx.x;
-  long long wlo = c * W / G, whi = (c + 1) * W / G;
+  long long wlo = split_point(c, W, G), whi = split_point(c + 1, W, G);
   if (p.one_slice) {   // G = S x cps: CTA c covers part c % cps of slice c / cps
-    const long long cps = G / p.S, sl = c / cps, sub = c % cps;
-    wlo = sl * p.Ws + sub * p.Ws / cps;
-    whi = sl * p.Ws + (sub + 1) * p.Ws / cps;
+    const unsigned cps = (unsigned)G / (unsigned)p.S, sl = (unsigned)c / cps, sub = (unsigned)c % cps;
+    wlo = (long long)sl * p.Ws + split_point(sub, p.Ws, cps);
+    whi = (long long)sl * p.Ws + split_point(sub + 1, p.Ws, cps);
   }
   const Pos start = pos_at(p, wlo);
   const Pos end = pos_at(p, whi);
@@ -1001,7 +1001,9 @@ __global__ void __launch_bounds__((NWC + 1) * 32, MINB) lut_stream_kernel(const 
 
   unsigned ep;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(ep) : "r"(s_epoch) : "memory");
-  const int og0 = (int)(c * p.RGtot / G), og1 = (int)((c + 1) * p.RGtot / G);
+  // (G <= 256 and RGtot <= 65536: 32-bit products, so a 32-bit division on the critical path)
+  const int og0 = (int)((unsigned)c * (unsigned)p.RGtot / (unsigned)G);
+  const int og1 = (int)((unsigned)(c + 1) * (unsigned)p.RGtot / (unsigned)G);
   const int R = (og1 - og0) * kTileRows;
   const int MR = p.M * R;   // (batch row m, output row) pairs owned
   // T threads per row; thread it takes row it % MR (consecutive lanes: consecutive rows of one
@@ -1106,7 +1108,7 @@ int stream_stages(int qmax, int budget, int su, int MW) {
 
 size_t stream_workspace_bytes(int M, int S, int RGtot) {
   if (S <= 1) return 0;   // no split-K: the kernel touches no workspace
-  return kStreamWsOff + 256 + (size_t)M * S * RGtot * kTileRows * sizeof(unsigned long long);
+  return kPartOff + (size_t)M * S * RGtot * kTileRows * sizeof(unsigned long long);
 }
 
 bool stream_shape_ok(int K, int sms) {
@@ -1176,7 +1178,7 @@ cudaError_t launch_lut_stream(const StreamLaunch& L, cudaStream_t stream) {
   if (p.S > 1) {
     char* ws = static_cast<char*>(L.workspace) + kStreamWsOff;
     p.done = reinterpret_cast<unsigned long long*>(ws);
-    p.part = reinterpret_cast<unsigned long long*>(ws + 256);
+    p.part = reinterpret_cast<unsigned long long*>(ws + (kPartOff - kStreamWsOff));
     p.part_end = p.part + (size_t)p.M * p.S * p.RGtot * kTileRows;
   }
   p.nst = L.nst;

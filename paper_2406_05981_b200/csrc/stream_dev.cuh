@@ -178,11 +178,20 @@ struct Pos {
 };
 
 // First unit whose weight offset is >= w (units are assigned by their starting offset).
+// floor(c W / G) for c <= G <= 256 and W < 2^31 without 64-bit division:
+// c W / G = c (W / G) + c (W % G) / G, every product below 2^31.
+__device__ __forceinline__ long long split_point(long long c, long long W, long long G) {
+  const unsigned q = (unsigned)W / (unsigned)G, rm = (unsigned)W % (unsigned)G;
+  return (long long)((unsigned)c * q + ((unsigned)c * rm) / (unsigned)G);
+}
+
 template <class P>
 __device__ __forceinline__ Pos pos_at(const P& p, long long w) {
   Pos r;
-  r.s = (int)(w / p.Ws);
-  int wi = (int)(w - (long long)r.s * p.Ws);
+  // w <= S x Ws < 2^31 (S <= 256, Ws <= 4 x 65536 x segments): 32-bit division (a 64-bit
+  // one is a ~100-instruction routine on the launch's critical path)
+  r.s = (int)((unsigned)w / (unsigned)p.Ws);
+  int wi = (int)w - r.s * p.Ws;
   r.g = 0;
   while (r.g + 1 < p.nseg && p.seg[r.g + 1].woff <= wi) ++r.g;
   const int q = p.seg[r.g].q;

@@ -80,8 +80,9 @@ def test_packed_bytes_rejects_bad_shapes(L):
 
 
 def test_workspace_bytes(L):
-    # tiled M=1 (streaming kernel): counter region + epoch word + {epoch, fp32} partials
-    # [RG][S][16]; S == 1 needs none.  M>1 (small-batch kernel): counters + fp32 partials.
+    # tiled M=1 (streaming kernel): counter region + gather counter + epoch word + {epoch,
+    # fp32} partials [RG][S][16]; S == 1 needs none.  Every kernel's partials start after the
+    # epoch word (kPartOff = 256 KB + 512), so none overwrites another's carried-over state.
     S, RG = 4096 // 256, 4096 // 16
     C = 65536 * 4  # per-row-group counters
     assert L.shiftadd_workspace_bytes(1, 1, 4096, 4096, 3, 128) == C + 256 + 256 + S * RG * 16 * 8
@@ -89,7 +90,8 @@ def test_workspace_bytes(L):
     assert L.shiftadd_workspace_bytes(1, 8, 4096, 4096, 3, 128) == C + 512 + 8 * S * RG * 16 * 8
     # M = 16: the larger of the streaming kernel (two row chunks of 8 reuse one region) and the
     # small-batch split-K kernel (fp32 partials for all 16 rows)
-    assert L.shiftadd_workspace_bytes(1, 16, 4096, 4096, 3, 128) == max(C + 512 + 8 * S * RG * 16 * 8, C + 16 * S * RG * 16 * 4)
+    assert L.shiftadd_workspace_bytes(1, 16, 4096, 4096, 3, 128) == max(C + 512 + 8 * S * RG * 16 * 8,
+                                                                        C + 512 + 16 * S * RG * 16 * 4)
     assert L.shiftadd_workspace_bytes(0, 1, 4096, 4096, 3, 128) == 0
     assert L.shiftadd_workspace_bytes(1, 17, 4096, 4096, 3, 128) == 0
 

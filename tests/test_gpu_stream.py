@@ -240,3 +240,33 @@ def test_small_batch_mw8_exact_invariants(sa):
     ym = sa.lut_gemm(-xr, layer, splitk=True)
     torch.cuda.synchronize()
     assert torch.equal(ym.float(), -yp.float())
+
+
+def test_workspace_shared_across_kernel_kinds(sa):
+    """One workspace used in turn by the round-1 split-K kernels (1: misaligned exponents, M = 1;
+    2: misaligned exponents, M = 8), the streaming kernel (8) on a tiny layer whose CTA 0 finishes
+    before most CTAs start (the epoch word must survive the other kernels' fp32 partials), and
+    the fused gather's counter region: every result stays at the oracle bar, many times over."""
+    ws = sa.Workspace(DEV)
+    big, pb, eb = _case(sa, 3, 1000, 2048, synth.seed_for(8, 90))
+    buf = torch.empty(big.exps.numel() + 16, dtype=torch.int8, device=DEV)
+    ex = buf[3:3 + big.exps.numel()]
+    ex.copy_(big.exps)
+    moved = sa.PackedLayer(big.planes, ex, big.q, big.N, big.K, big.g, big.layout, big.counts)
+    tiny, pt, et = _case(sa, 1, 40, 512, synth.seed_for(8, 91))
+    xb = synth.gen_x(8, 2048, seed=92)
+    xt = synth.gen_x(1, 512, seed=93)
+    ref_b1 = oracle.gemm(xb.numpy()[:1], pb, eb, 128)
+    ref_b8 = oracle.gemm(xb.numpy(), pb, eb, 128)
+    ref_t = oracle.gemm(xt.numpy(), pt, et, 128)
+    xb_d, xt_d = xb.to(DEV), xt.to(DEV)
+    for it in range(6):
+        y1 = sa.lut_gemm(xb_d[:1], moved, workspace=ws, pdl=True)            # kernel 1
+        y8 = sa.lut_gemm(xb_d, moved, workspace=ws, pdl=True)                # kernel 2, M = 8
+        ys = [sa.lut_gemm(xt_d, tiny, workspace=ws, pdl=True, splitk=True).clone() for _ in range(8)]   # kernel 8
+        torch.cuda.synchronize()
+        assert oracle.err_floor(y1.float().cpu().numpy(), ref_b1) <= TOL
+        assert oracle.err_floor(y8.float().cpu().numpy(), ref_b8) <= TOL
+        for y in ys:
+            assert oracle.err_floor(y.float().cpu().numpy(), ref_t) <= TOL, it
+    assert int(ws.buf[:65536 * 4 + 16].count_nonzero()) == 0    # counters and the gather counter left zero
