@@ -403,6 +403,44 @@ def time_layer_row(sa, dev, stream, ws, l2, peak, label, segs, K, kind, ws_size)
             "rotating_copies": R, "l2_defeat": "R x %.1f MB = %.0f MB > 4 x L2" % (lb / 1e6, R * lb / 1e6)}
 
 
+def fused_gather_row(sa, sdist, dev, stream, group, ws_size, rank, peak, short):
+    """NEXT-f3 at N > 1: this rank's shard of the LLaMA-2-70B down_proj (8192 x 28672, 3-bit,
+    configs[3]) through FusedGatherLinear -- the GEMV's owner CTAs store y into every rank's
+    gathered buffer, a flag wait replaces the NCCL all-gather -- timed as a graph of back-to-back
+    calls (each followed by its wait), max over ranks."""
+    N, K, q = 8192, 28672, 3
+    n = N // ws_size
+    signs, alpha = synth.gen_layer(q, n, K, G, seed=synth.seed_for(3, 2, rank), device=dev)
+    layer = sdist.FusedGatherLinear(sa.pack(signs, alpha, G, layout=sa.LAYOUT_TILED), N, group)
+    del signs, alpha
+    x = synth.gen_x(1, K, seed=synth.seed_for(3, 3), device=dev).view(-1)
+    reps = 4 if short else 40
+    with torch.cuda.stream(stream):
+        for _ in range(4):
+            y = layer(x, pdl=True, stream=stream)
+    stream.synchronize()
+    ok = bool(torch.isfinite(y.float()).all())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        for _ in range(reps):
+            layer(x, pdl=True, stream=stream)
+    with torch.cuda.stream(stream):
+        g.replay()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        g.replay()
+        e1.record(stream)
+    stream.synchronize()
+    us = torch.tensor([e0.elapsed_time(e1) * 1e3 / reps], dtype=torch.float64, device=dev)
+    torch.distributed.all_reduce(us, op=torch.distributed.ReduceOp.MAX, group=group)
+    us = float(us.item())
+    b = alg_bytes(1, q, n, K)
+    return {"layer": "llama70b down 8192x28672 q3, N-shard %d + fused gather" % ws_size, "K": K, "rows_per_rank": n,
+            "us_per_call": round(us, 3), "GBps_per_rank": round(b / us * 1e-3, 1),
+            "frac_per_rank": round(b / us * 1e-3 / peak, 4), "finite": ok,
+            "how": "graph of %d calls (GEMV with peer-store epilogue + flag wait), max over ranks" % reps}
+
+
 # ------------------------------------------------------------------ product arm
 def main():
     ap = argparse.ArgumentParser()
@@ -414,6 +452,9 @@ def main():
     ap.add_argument("--no-layers", action="store_true", help="skip the per-layer rows")
     ap.add_argument("--no-program", action="store_true", help="skip the persistent-program (kernel 9) row")
     ap.add_argument("--dry-run", action="store_true", help="N>1 plumbing only: build the shards, run 2 steps")
+    ap.add_argument("--gather", default="nccl", choices=["nccl", "fused"],
+                    help="N>1: also time the LLaMA-2-70B down_proj shard with the all-gather fused into the "
+                         "GEMV epilogue (peer stores + flags, NEXT-f3)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -475,9 +516,12 @@ def main():
         for _ in range(2):
             step()
     stream.synchronize()
+    fused_row = fused_gather_row(sa, sdist, dev, stream, group, ws_size, rank, peak, args.dry_run) \
+        if group is not None and args.gather == "fused" else None
     if args.dry_run:
         if rank == 0:
-            print(json.dumps({"dry_run": True, "n_gpus": ws_size, "launches_per_step": len(launches)}), flush=True)
+            print(json.dumps({"dry_run": True, "n_gpus": ws_size, "launches_per_step": len(launches),
+                              "fused_gather": fused_row}), flush=True)
         if group is not None:
             torch.distributed.destroy_process_group()
         return 0
@@ -688,7 +732,8 @@ def main():
                        "l2_defeat": "inputs larger than L2: the step reads all %.2f GB of resident weights "
                                     "once (L2 %d MB)" % (step_bytes_full / ws_size / 1e9, l2 >> 20),
                        "parallelism": ("N-shard x%d + NCCL all-gather per launch" % ws_size) if ws_size > 1
-                       else "single GPU", "pdl": True, "persistent_program": program_row, "layers": per_layer},
+                       else "single GPU", "pdl": True, "persistent_program": program_row,
+                       "fused_gather": fused_row, "layers": per_layer},
             "roofline": roofline,
             "clocks": clocks,
             "gpu_launches": args.steps * len(launches),

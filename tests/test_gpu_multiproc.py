@@ -93,9 +93,12 @@ def test_sharded_linear_two_ranks_one_gpu():
 def test_bench_dry_run_two_ranks():
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
-           os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run", "--steps", "2", "--warmup", "3"]
+           os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run", "--steps", "2", "--warmup", "3",
+           "--gather", "fused"]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, cwd=ROOT)
     assert res.returncode == 0, (res.stdout + res.stderr)[-4000:]
     lines = [json.loads(s) for s in res.stdout.splitlines() if s.startswith("{")]
     assert lines and lines[-1]["dry_run"] and lines[-1]["n_gpus"] == 2
     assert lines[-1]["launches_per_step"] == 128
+    fg = lines[-1]["fused_gather"]   # the 70B down_proj shard with the fused all-gather epilogue
+    assert fg["finite"] and fg["rows_per_rank"] == 4096 and fg["us_per_call"] > 0
